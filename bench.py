@@ -1,0 +1,467 @@
+"""Benchmark: recolor optimizer steps/s + rendered Mpix/s on the B200 (BASELINE.json).
+
+Workload (default `--config c3`, BASELINE.json configs[2], the config the metric
+is quoted on; it fits one B200): synthetic 1M-gaussian scene, SH degree 3, 64
+views at 1920x1080, mask selection (brush at the ball centroid in view 0,
+radius 0.15 W, unproject 0.7, outlier filter, tint (1, 0.2, 0.2)) + recolor
+refit.  One timed "step" = one optimizer iteration: per GPU one view is
+preprocessed + binned from scratch (no cross-step caching), coloured,
+rasterised, loss + image gradient, backward, and every rank applies Adam to
+all 1M x 48 coefficients.  N GPUs: one process per GPU (torchrun), views drawn
+G = N per step from the reference RNG stream, per-gaussian channel sums
+all-gathered over NCCL; `value` = view-steps/s of the whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3]
+    python bench.py --impl reference ...   # the CPU reference path (oracle port)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(n=10_000, deg=0, views=4, width=256, height=256),
+    "c2": dict(n=200_000, deg=3, views=16, width=800, height=800),
+    "c3": dict(n=1_000_000, deg=3, views=64, width=1920, height=1080),
+}
+METRIC = "recolor opt steps/sec + rendered Mpix/s (1M gaussians, 1080p) at 1/2/4/8 B200"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.index = index
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i
+                          and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def build_workload(cfg, rank, dev):
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import device as D
+    from paper_2511_18441_b200.synthetic import ring_cameras, scaled_scene
+
+    t0 = time.time()
+    scene, n_plane = scaled_scene(cfg["n"], cfg["deg"], seed=0)
+    cams = ring_cameras(cfg["width"], cfg["height"], cfg["views"])
+    ds = D.device_scene(scene)
+    sh0 = D.sh_to_device(scene.sh)
+    h, w = cfg["height"], cfg["width"]
+    gt = torch.empty((len(cams), h, w, 3), dtype=torch.float32, device=dev)
+    for i, (intr, pose) in enumerate(cams):  # self-consistent GT (loss == 0 before the edit)
+        v = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
+        v.color(sh0)
+        v.render(None, 0, out=gt[i])
+        v.close()
+    # select-from-mask on view 0 (host-side steps, once per commit)
+    intr0, pose0 = cams[0]
+    centroid = scene.positions[n_plane:].mean(axis=0)
+    cam = pose0.rotation @ centroid + pose0.translation
+    u = intr0.fx * cam[0] / cam[2] + intr0.cx
+    vv = intr0.fy * cam[1] / cam[2] + intr0.cy
+    brush = P.apply_stroke(P.new_mask(intr0, pose0), "brush", [(float(u), float(vv))], 0.15 * w)
+    v0 = D.View(ds, intr0, pose0, P.DEFAULT_CONFIG)
+    depth0 = v0.depth(0.5).cpu().numpy()
+    v0.close()
+    cloud = P.remove_outliers(P.unproject(brush, depth0, 0.7, 0), 16, 0.007)
+    setup_s = time.time() - t0
+    return scene, cams, ds, sh0, gt, cloud, setup_s
+
+
+def sync_max(t, world):
+    import torch
+    if world == 1:
+        return t
+    x = torch.tensor([t], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+    return float(x.item())
+
+
+def run_gpu(args):
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import device as D
+    from paper_2511_18441_b200.engine import RefitEngine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+        group = torch.distributed.group.WORLD
+    cfg = CONFIGS[args.config]
+    npix = cfg["width"] * cfg["height"]
+    scene, cams, ds, sh0, gt, cloud, setup_s = build_workload(cfg, rank, dev)
+
+    # ---- selection pass (views sharded statically across ranks, counts all-reduced)
+    pts = D.to_device(cloud.points, torch.float64)
+    mine = list(range(rank, len(cams), world))
+    sp = P.SelectionPass(ds, cams, gt)
+    sp.run(pts, (1.0, 0.2, 0.2), indices=mine[:1])  # warm-up
+    sp = P.SelectionPass(ds, cams, gt)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sp.run(pts, (1.0, 0.2, 0.2), indices=mine)
+    if world > 1:
+        torch.distributed.all_reduce(sp.hits)
+        torch.distributed.all_reduce(sp.wsum)
+        for i in range(len(cams)):  # every rank needs every edited target for the refit
+            torch.distributed.broadcast(sp.edited[i], src=i % world)
+    e1.record()
+    torch.cuda.synchronize()
+    sel_ms = sync_max(e0.elapsed_time(e1), world)
+    for v in sp.views:
+        if v is not None:
+            v.close()
+    masked_px = int(sp.masks.sum().item())
+
+    # ---- recolor refit: K timed steps
+    opt_cfg = P.OptimizerConfig()
+    targets = [sp.edited[i] for i in range(len(cams))]
+    eng = RefitEngine(ds, sh0.clone(), cams, targets, opt_cfg, seed=7, cache_views=False, group=group)
+    for _ in range(args.warmup):
+        eng.step()
+    eng.drain()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            eng.step()
+        e1.record()
+        torch.cuda.synchronize()
+    step_ms = sync_max(e0.elapsed_time(e1), world) / args.steps
+    recs = eng.drain()
+    if world > 1:
+        torch.distributed.barrier()
+
+    # ---- stage breakdown + per-kernel roofline (one view, CUDA events on this stream)
+    stages = stage_times(eng, cams, args.config, npix, cfg)
+    # ---- rendered Mpix/s: full forward (preprocess + bin + colour + raster) per frame
+    frames = max(8, args.steps)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(frames):
+        intr, pose = cams[(rank + i * world) % len(cams)]
+        v = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
+        v.color(eng.sh)
+        v.render(None, 0, out=eng._buf(cfg["height"], cfg["width"])[0])
+        v.close()
+    e1.record()
+    torch.cuda.synchronize()
+    frame_ms = sync_max(e0.elapsed_time(e1), world) / frames
+
+    # ---- e2e through the public API, host (pinned) targets streamed each step
+    e2e = run_e2e(args, scene, cams, sp, group, world) if rank == 0 or world > 1 else None
+
+    gpu_launches = launches_per_step(eng) * args.steps
+    if rank != 0:
+        return
+    hbm, peak_kind = peaks()
+    dom = max(stages["kernels"], key=lambda k: stages["kernels"][k]["ms"])
+    dk = stages["kernels"][dom]
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(dk["gbs"], 1), "peak": hbm,
+            "unit": "GB/s", "frac": round(dk["gbs"] / hbm, 4), "traffic": None,
+            "peak_kind": peak_kind, "bytes_per_launch": dk["bytes"], "ms_per_launch": dk["ms"],
+            "note": dk.get("note", "")}
+    cpu = cpu_baseline_sample(args, cfg) if args.cpu_baseline else None
+    value = world / (step_ms / 1000.0)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "view-steps/s (opt steps/s x views per step)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 decisions/keys/loss)", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['n']} gaussians SH deg {cfg['deg']}, "
+                               f"{cfg['views']} views {cfg['width']}x{cfg['height']}, selection + recolor",
+                   "views_per_step": world, "l2": "inputs larger than L2 (SH + Adam state "
+                   f"{cfg['n'] * 48 * 4 * 3 / 1e6:.0f} MB touched per step)", "parallelism": f"views{world}"},
+        "opt_steps_per_s": round(1000.0 / step_ms, 3),
+        "rendered_mpix_s": round(world * npix / (frame_ms / 1000.0) / 1e6, 1),
+        "render_ms_per_frame": round(frame_ms, 4),
+        "selection": {"views": len(cams), "ms": round(sel_ms, 3),
+                      "views_per_s": round(len(cams) / (sel_ms / 1000.0), 1),
+                      "masked_px": masked_px, "cloud_points": len(cloud)},
+        "interactive_job_s": round((sel_ms + 100 * step_ms) / 1000.0, 4),
+        "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items()},
+        "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
+        "roofline": roof, "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
+        "final_loss": recs[-1][4] if recs else None,
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+
+
+def launches_per_step(eng):
+    # view build: k1_cull, scan(3), compact, depth sort (bits/8 x (hist + scan(3) + scatter)),
+    # k1_record, scan(3), emit, tile sort (2 x 5), ranges; colour; render; loss (3);
+    # backward (raster + reduce); adam (fused + commit).  Counted from the code path.
+    v = eng.views[0] or None
+    bits = 55
+    return 1 + 3 + 1 + ((bits + 7) // 8) * 5 + 1 + 3 + 1 + 2 * 5 + 1 + 1 + 1 + 3 + 2 + 2
+
+
+def stage_times(eng, cams, config, npix, cfg, reps=5):
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import _native as N
+    from paper_2511_18441_b200 import device as D
+
+    intr, pose = cams[1]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(reps):
+            fn()
+        ev[1].record()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    ds = eng.dscene
+    holder = {}
+
+    def build():
+        if "v" in holder:
+            holder["v"].close()
+        holder["v"] = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
+
+    t_build = timed(build)
+    v = holder["v"]
+    t_color = timed(lambda: v.color(eng.sh))
+    img, tgt, grad = eng._buf(intr.height, intr.width)
+    t_render = timed(lambda: v.render(None, 0, out=img))
+    loss3 = torch.empty(3, dtype=torch.float64, device="cuda")
+    target = eng.targets[1]
+    t_loss = timed(lambda: D.loss_grad(img, target, 0.2, loss3=loss3, grad=grad))
+    acc = torch.empty((ds.n, 3), dtype=torch.float32, device="cuda")
+    t_bwd = timed(lambda: v.backward(grad, acc=acc))
+    m = torch.zeros_like(eng.sh)
+    vv = torch.zeros_like(eng.sh)
+    sh = eng.sh.clone()
+    step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    import ctypes
+    cfgc = D.adam_config(P.OptimizerConfig())
+    ptrs = (ctypes.c_void_p * 1)(acc.data_ptr())
+    cen = (ctypes.c_double * 3)(*D.camera_center(pose))
+
+    def adam():
+        N.call("rcgs_adam_fused", ds.handle, N.ptr(sh), N.ptr(m), N.ptr(vv), ptrs, cen, 1,
+               ctypes.byref(cfgc), None, N.ptr(step), D.stream_ptr())
+
+    t_adam = timed(adam)
+    n, k, pairs = ds.n, v.n_kept, v.n_pairs
+    passes = (v.sort_bits + 7) // 8
+    kern = {
+        # K1+K2: geometry read + depth sort passes on K keys + pair sort (2 passes)
+        "view_build": dict(ms=t_build, bytes=n * (24 + 48 + 8) + k * (24 + 48 + 8)
+                           + passes * k * 24 + pairs * (8 + 2 * 16), note="K1+K2"),
+        "color": dict(ms=t_color, bytes=k * (192 + 24 + 4 + 16)),
+        "raster_fwd": dict(ms=t_render, bytes=pairs * (4 + 48 + 16) + npix * 12,
+                           note="FP32/MUFU-issue bound; HBM bytes shown"),
+        "loss_grad": dict(ms=t_loss, bytes=npix * 36),
+        "raster_bwd": dict(ms=t_bwd, bytes=pairs * (4 + 4 + 48 + 16 + 12) + npix * 12 + k * 28 + n * 12,
+                           note="FP32-issue + shuffle bound; HBM bytes shown"),
+        "adam": dict(ms=t_adam, bytes=n * (6 * 192 + 12 + 24)),
+    }
+    for kk in kern.values():
+        kk["gbs"] = kk["bytes"] / (kk["ms"] / 1000.0) / 1e9
+    v.close()
+    return {"kernels": kern, "pairs": pairs, "kept": k}
+
+
+def run_e2e(args, scene, cams, sp, group, world):
+    """Same metric through the public API: BackgroundOptimizer with the targets
+    in pinned host memory (one H2D per step) and the step's metrics read back
+    every step (snapshot_every=1)."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from types import SimpleNamespace
+
+    edited = sp.edited.cpu()
+    masks = sp.masks.cpu().numpy().astype(bool)
+    views = tuple(P.EditedView(view=SimpleNamespace(view_id=i, intrinsics=cams[i][0], pose=cams[i][1]),
+                               mask=masks[i], image=edited[i].numpy()) for i in range(len(cams)))
+    ds = P.EditedDataset(views=views, generation=0, tint=np.array([1.0, 0.2, 0.2]))
+    cfg = P.OptimizerConfig(snapshot_every=1)
+    opt = P.BackgroundOptimizer(scene, ds, cfg, seed=7, group=group, cache_views=False, stream_targets=True)
+    opt.run_iterations(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        opt._step()
+        opt._flush()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    dt = sync_max(dt, world)
+    h, w = edited.shape[1], edited.shape[2]
+    return {"value": round(world * args.steps / dt, 3), "unit": "view-steps/s",
+            "h2d_bytes_per_step": int(h * w * 3 * 4), "d2h_bytes_per_step": 32,
+            "api": "BackgroundOptimizer(stream_targets=True), metrics read back every step"}
+
+
+# ----------------------------------------------------------------------------- CPU reference arm
+def _cpu_pixels(payload):
+    from oracle import raster as OR
+    p, us, vs = payload
+    t0 = time.perf_counter()
+    xs_done = 0
+    for u, v in zip(us, vs):
+        a = OR.alpha_block(p, np.array([float(u)]), np.array([float(v)]))
+        OR.weights_block(a)
+        xs_done += 1
+    return xs_done, time.perf_counter() - t0
+
+
+def cpu_reference(cfg, budget_s=20.0, workers=None):
+    """The reference algorithm (oracle port of render.py/losses.py/backward.py/
+    optimize.py; the dense per-pixel composite over all kept gaussians in
+    global depth order) timed on a bounded pixel sample and extrapolated to
+    one full optimizer iteration.  Returns a cpu_baseline dict."""
+    import multiprocessing as mp
+    from oracle import raster as OR
+    from paper_2511_18441_b200.synthetic import ring_cameras, scaled_scene
+
+    scene, _ = scaled_scene(cfg["n"], cfg["deg"], seed=0)
+    intr, pose = ring_cameras(cfg["width"], cfg["height"], cfg["views"])[0]
+    t0 = time.perf_counter()
+    p = OR.project(scene, intr, pose)
+    t_proj = time.perf_counter() - t0
+    workers = workers or max(1, min(os.cpu_count() or 1, 16))
+    rng = np.random.default_rng(0)
+    # calibrate: one pixel
+    _, t1 = _cpu_pixels((p, [intr.width // 2], [intr.height // 2]))
+    per_worker = max(1, int(budget_s / max(t1, 1e-6)))
+    us = rng.integers(0, intr.width, per_worker * workers)
+    vs = rng.integers(0, intr.height, per_worker * workers)
+    chunks = [(p, us[i::workers], vs[i::workers]) for i in range(workers)]
+    t0 = time.perf_counter()
+    if workers > 1:
+        with mp.get_context("fork").Pool(workers) as pool:
+            res = pool.map(_cpu_pixels, chunks)
+    else:
+        res = [_cpu_pixels(chunks[0])]
+    wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    npix = cfg["width"] * cfg["height"]
+    # forward (alpha + weights) dominates; the capture/colour/backward/loss add
+    # ~35% (einsum 19% + nonzero 15% + loss/backward/adam ~3-4%)
+    step_s = t_proj + wall / done * npix * 1.37
+    return {"value": 1.0 / step_s, "unit": "view-steps/s", "cores": workers, "kind": "port",
+            "sample": f"{done} pixels of view 0 at {cfg['n']} gaussians ({p.count} kept), dense "
+                      f"reference composite, extrapolated to {npix} px x 1.37 (capture+loss+backward+adam)",
+            "rendered_mpix_s": npix / ((t_proj + wall / done * npix) * 1e6)}
+
+
+def cpu_baseline_sample(args, cfg):
+    try:
+        return cpu_reference(cfg, budget_s=args.cpu_budget)
+    except Exception as e:  # never fail the GPU line because of the baseline
+        return {"value": None, "error": repr(e)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(cpu_reference(cfg, budget_s=args.cpu_budget / max(1, args.steps + args.warmup)))
+    base = vals[args.warmup:]
+    value = float(np.mean([b["value"] for b in base]))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "view-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.config, **cfg},
+        "cpu_baseline": {**base[-1], "value": value},
+        "e2e": {"value": value, "unit": "view-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,177 @@
+/*
+ * rcgs.h -- C ABI of the B200 (sm_100a) ReCoGS recolor hot path.
+ *
+ * The reference (`splattint`, /root/reference/pkg/src/splattint) is a pure
+ * Python package with no native seam: its "plugin interface" is the set of
+ * module-level functions re-exported by splattint/__init__.py:4-99 and bound
+ * by name in the callers (optimize.py:23-28, recolor.py:16-18,
+ * session.py:19-48).  Each entry point below is the native half of one of those
+ * functions; the Python package `paper_2511_18441_b200` binds them with ctypes
+ * and keeps the reference's names, argument meaning and
+ * error behaviour.
+ *
+ * Conventions
+ *  - Plain C types only: raw device pointers ("d_" prefix), host pointers
+ *    ("h_" prefix), sizes, and a cudaStream_t passed as void*.
+ *  - Every call returns an int status (RCGS_OK on success) and never throws;
+ *    rcgs_last_error() gives the message of the last failure on this thread.
+ *    RCGS_EINVAL maps to splattint.errors.ValidationError (errors.py:16-17),
+ *    RCGS_ECUDA to SplattintError (errors.py:4-5).
+ *  - Caller-owned: SH coefficients, Adam moments, images, masks, gradients.
+ *    Library-owned: opaque scene and per-view handles (stream-ordered device
+ *    allocations), released with the matching *_destroy call.
+ *  - Images are HWC float32 (H, W, 3) unless stated; SH is (N, 16, 3) float32.
+ */
+#ifndef RCGS_H
+#define RCGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCGS_OK 0
+#define RCGS_EINVAL 1      /* precondition violated (ValidationError)            */
+#define RCGS_ECUDA 2       /* CUDA runtime failure (SplattintError)              */
+#define RCGS_ENOMEM 3      /* device allocation failed (SplattintError)          */
+
+#define RCGS_VERSION 1
+
+typedef struct rcgs_scene rcgs_scene; /* device geometry: fp64 positions, cov3d, opacity */
+typedef struct rcgs_view rcgs_view;   /* one camera's preprocessed + binned gaussians     */
+
+/* Pinhole camera + world->camera pose (scene.py:34-75). */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double R[9]; /* row-major rotation, x_cam = R x_world + t */
+    double t[3];
+} rcgs_camera;
+
+/* RasterizerConfig (render.py:54-66). */
+typedef struct {
+    double near_clip, alpha_clamp, alpha_skip, transmittance_floor;
+    double covariance_dilation, footprint_sigmas;
+} rcgs_raster_config;
+
+/* OptimizerConfig (optimize.py:33-41), minus the loss weight. */
+typedef struct {
+    double lr_dc, lr_rest, beta1, beta2, eps;
+} rcgs_adam_config;
+
+typedef struct {
+    int64_t n_gaussians;  /* N                                               */
+    int64_t n_kept;       /* K: survivors of near clip + 3-sigma cull         */
+    int64_t n_pairs;      /* (gaussian, tile) pairs after binning              */
+    int32_t tiles_x, tiles_y, tile_size;
+    int32_t sort_bits;    /* depth-key bits actually radix-sorted              */
+} rcgs_view_info;
+
+int rcgs_version(void);
+const char* rcgs_last_error(void);
+
+/* ---- scene (replaces the geometry half of splattint.Scene, scene.py:126-186) -------- */
+/* Copies fp64 positions (N,3), opacities (N,) and derives the view-independent 3D
+ * covariance R S S^T R^T (render.py:95-100) from unit quaternions (N,4) and scales
+ * (N,3).  All inputs are device pointers; the handle owns its copies. */
+int rcgs_scene_create(const double* d_positions, const double* d_rotations,
+                      const double* d_scales, const double* d_opacities, int64_t n,
+                      int sh_degree, void* stream, rcgs_scene** out);
+int rcgs_scene_destroy(rcgs_scene* scene, void* stream);
+
+/* ---- per-view preprocess + tile binning (render.py:172-229 _project_scene) ---------- */
+/* K1 fp64 projection + 3-sigma cull, stable depth radix sort of the kept gaussians
+ * (bit-exact render.py:216 order), opacity-aware tile footprints, (tile|depth) pair
+ * sort and tile ranges.  Synchronises `stream` twice (kept count, pair count). */
+int rcgs_view_create(const rcgs_scene* scene, const rcgs_camera* cam,
+                     const rcgs_raster_config* cfg, void* stream, rcgs_view** out);
+int rcgs_view_info_get(const rcgs_view* view, rcgs_view_info* out);
+int rcgs_view_destroy(rcgs_view* view, void* stream);
+/* Kept gaussians front to back: scene index (K,) int64 and view-space z (K,) fp64. */
+int rcgs_view_kept(const rcgs_view* view, int64_t* d_index, double* d_depth, void* stream);
+
+/* SH basis (K,16) fp64 along each kept gaussian's view direction and the channel
+ * activation flags (K,3) uint8 from the last rcgs_view_color (ForwardCapture.basis /
+ * .active, render.py:88-89).  Either output may be NULL. */
+int rcgs_view_basis(const rcgs_view* view, double* d_basis, uint8_t* d_active, void* stream);
+
+/* SH colour of the kept gaussians (render.py:209-214) from SH (N,16,3) fp32;
+ * must be called before render/backward whenever SH changed. */
+int rcgs_view_color(rcgs_view* view, const float* d_sh, void* stream);
+
+/* ---- rasteriser (render.py:263-334) -------------------------------------------------- */
+/* layout 0 = HWC (H,W,3), 1 = CHW (3,H,W); d_t_final (H,W) may be NULL. */
+int rcgs_render(const rcgs_view* view, const float* h_background3, int layout,
+                float* d_image, float* d_t_final, void* stream);
+
+/* depth_from_gaussians (render.py:373-398): (H,W) fp64, +inf where T never drops
+ * below tau at a composited gaussian.  d_cross (H,W) int32 = kept rank or -1, may be NULL. */
+int rcgs_depth(const rcgs_view* view, double tau, double* d_depth, int32_t* d_cross,
+               void* stream);
+
+/* render_forward contribution lists (render.py:337-370).  Call with d_* = NULL to
+ * get the count in *h_count, then again with buffers of that size.  Order:
+ * pixel-major, then front to back (identical to the reference's np.nonzero). */
+int rcgs_capture(const rcgs_view* view, int64_t* h_count, int64_t* d_pixel, int64_t* d_kept,
+                 double* d_weight, void* stream);
+
+/* ---- loss + image gradient (losses.py:68-134), fp64 arithmetic ---------------------- */
+/* d_loss3 (device, fp64) receives {l1, ssim, total}.  d_grad (H,W,3) fp32 gets
+ * d total / d image, exactly zero when image == target (losses.py:127-130).
+ * lam == 0 skips SSIM (images may then be smaller than 11 px). */
+int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height, int32_t width,
+                   double lam, double* d_loss3, float* d_grad, void* stream);
+
+/* ---- SH backward (backward.py:22-40) ------------------------------------------------ */
+/* Per-gaussian channel sums acc[i,ch] = active[i,ch] * sum_p g[p,ch] * w_ip over the
+ * view's composited contributions, written densely as d_acc (N,3) fp32 (zero for
+ * culled gaussians).  Deterministic (no float atomics).  If d_nonfinite != NULL it
+ * is OR-ed with 1 when any sum is non-finite. */
+int rcgs_backward(const rcgs_view* view, const float* d_grad_image, float* d_acc,
+                  int32_t* d_nonfinite, void* stream);
+
+/* Expand a view's acc into the dense (N,16,3) gradient basis_k(dir_i) * acc[i,ch]. */
+int rcgs_sh_grad(const rcgs_scene* scene, const float* d_acc, const double* h_center3,
+                 float* d_grad, void* stream);
+
+/* ---- Adam (optimize.py:59-83) -------------------------------------------------------- */
+/* Fused gradient expansion + Adam over all N x 48 coefficients.  The gradient is
+ * (1/G) sum_v basis(dir_{v,i}) (x) acc_v[i] for G views (G == 1 is the reference
+ * iteration); d_accs points to G device pointers (host array).  If *d_reject != 0 the
+ * update is skipped (non-finite gradient, optimize.py:72-74); otherwise the device
+ * step counter *d_step is advanced. */
+int rcgs_adam_fused(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
+                    const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                    const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                    void* stream);
+/* Dense Adam on an explicit gradient (N,16,3) (adam_step API). */
+int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
+                    const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                    void* stream);
+/* OR 1 into *d_flag if any of d_x[0..count) is non-finite. */
+int rcgs_nonfinite_check(const float* d_x, int64_t count, int32_t* d_flag, void* stream);
+
+/* ---- selection pass (selection.py:184-235, recolor.py:30-81) ------------------------- */
+/* Stamp quad x quad squares of the visible cloud points into d_mask (H,W) uint8
+ * (caller zero-fills); visibility z <= depth * (1 + tol), fp64, bit-exact. */
+int rcgs_project_cloud(const double* d_points, int64_t m, const rcgs_camera* cam,
+                       const double* d_depth, int32_t quad, double tol, uint8_t* d_mask,
+                       void* stream);
+/* out = mask ? clip(image * tint, 0, 1) : image, for npix HWC pixels. */
+int rcgs_apply_recolor(const float* d_image, const uint8_t* d_mask, int64_t npix,
+                       const float* h_tint3, float* d_out, void* stream);
+/* fp64 variant for host-facing datasets (bit-exact recolor.py:30-39). */
+int rcgs_apply_recolor_f64(const double* d_image, const uint8_t* d_mask, int64_t npix,
+                           const double* h_tint3, double* d_out, void* stream);
+/* Per-gaussian mask statistics of one view, accumulated into the outputs:
+ * d_hits[i] += #{masked pixels p with w_ip > 0}; d_wsum[i] += round(2^32 * sum w_ip)
+ * (integer, so order-independent and exact across views and ranks). */
+int rcgs_mask_hits(const rcgs_view* view, const uint8_t* d_mask, int32_t* d_hits,
+                   uint64_t* d_wsum, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCGS_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of ``librcgs.so`` (the C ABI declared in include/rcgs.h).
+
+There is no CPU fallback: importing a compute entry point without the built
+library, or without a CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import SplattintError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "librcgs.so")
+
+RCGS_OK, RCGS_EINVAL, RCGS_ECUDA, RCGS_ENOMEM = 0, 1, 2, 3
+
+c_void_p = ctypes.c_void_p
+c_int = ctypes.c_int
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_double = ctypes.c_double
+P = ctypes.POINTER
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("fx", c_double), ("fy", c_double), ("cx", c_double), ("cy", c_double),
+                ("width", c_i32), ("height", c_i32), ("R", c_double * 9), ("t", c_double * 3)]
+
+
+class RasterConfig(ctypes.Structure):
+    _fields_ = [("near_clip", c_double), ("alpha_clamp", c_double), ("alpha_skip", c_double),
+                ("transmittance_floor", c_double), ("covariance_dilation", c_double),
+                ("footprint_sigmas", c_double)]
+
+
+class AdamConfig(ctypes.Structure):
+    _fields_ = [("lr_dc", c_double), ("lr_rest", c_double), ("beta1", c_double),
+                ("beta2", c_double), ("eps", c_double)]
+
+
+class ViewInfo(ctypes.Structure):
+    _fields_ = [("n_gaussians", c_i64), ("n_kept", c_i64), ("n_pairs", c_i64),
+                ("tiles_x", c_i32), ("tiles_y", c_i32), ("tile_size", c_i32), ("sort_bits", c_i32)]
+
+
+# name -> (argtypes); every function returns int status except the two noted.
+_SIGNATURES = {
+    "rcgs_scene_create": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int, c_void_p,
+                          P(c_void_p)],
+    "rcgs_scene_destroy": [c_void_p, c_void_p],
+    "rcgs_view_create": [c_void_p, P(Camera), P(RasterConfig), c_void_p, P(c_void_p)],
+    "rcgs_view_info_get": [c_void_p, P(ViewInfo)],
+    "rcgs_view_destroy": [c_void_p, c_void_p],
+    "rcgs_view_kept": [c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_view_color": [c_void_p, c_void_p, c_void_p],
+    "rcgs_render": [c_void_p, P(ctypes.c_float), c_int, c_void_p, c_void_p, c_void_p],
+    "rcgs_depth": [c_void_p, c_double, c_void_p, c_void_p, c_void_p],
+    "rcgs_capture": [c_void_p, P(c_i64), c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_loss_grad": [c_void_p, c_void_p, c_i32, c_i32, c_double, c_void_p, c_void_p, c_void_p],
+    "rcgs_backward": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_sh_grad": [c_void_p, c_void_p, P(c_double), c_void_p, c_void_p],
+    "rcgs_adam_fused": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
+                        P(AdamConfig), c_void_p, c_void_p, c_void_p],
+    "rcgs_adam_dense": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, P(AdamConfig), c_void_p,
+                        c_void_p, c_void_p],
+    "rcgs_nonfinite_check": [c_void_p, c_i64, c_void_p, c_void_p],
+    "rcgs_project_cloud": [c_void_p, c_i64, P(Camera), c_void_p, c_i32, c_double, c_void_p,
+                           c_void_p],
+    "rcgs_apply_recolor": [c_void_p, c_void_p, c_i64, P(ctypes.c_float), c_void_p, c_void_p],
+    "rcgs_view_basis": [c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_apply_recolor_f64": [c_void_p, c_void_p, c_i64, P(c_double), c_void_p, c_void_p],
+    "rcgs_mask_hits": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+}
+EXPORTED = tuple(_SIGNATURES) + ("rcgs_version", "rcgs_last_error")
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(require_gpu: bool = True):
+    """Load librcgs.so (once).  Raises SplattintError when it is missing or,
+    with `require_gpu`, when no CUDA device is visible."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise SplattintError(
+                    f"CUDA library not built: {LIB_PATH} is missing (run __graft_entry__.build())")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, args in _SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = c_int
+            lib.rcgs_version.restype = c_int
+            lib.rcgs_version.argtypes = []
+            lib.rcgs_last_error.restype = ctypes.c_char_p
+            lib.rcgs_last_error.argtypes = []
+            _lib = lib
+    if require_gpu:
+        import torch
+        if not torch.cuda.is_available():
+            raise SplattintError("paper_2511_18441_b200 needs a CUDA device (sm_100a); none is visible")
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == RCGS_OK:
+        return
+    msg = _lib.rcgs_last_error().decode(errors="replace")
+    if status == RCGS_EINVAL:
+        raise ValidationError(msg)
+    raise SplattintError(f"rcgs error {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    lib = load_library()
+    check(getattr(lib, name)(*args))
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()

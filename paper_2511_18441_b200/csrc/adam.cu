@@ -1,0 +1,229 @@
+// K7: SH gradient expansion fused with Adam (backward.py:36-40, optimize.py:59-83).
+//
+// The per-view backward (raster.cu) leaves one fp32 3-vector per gaussian,
+// acc[i, ch] = active * sum_p g[p, ch] w_ip.  The dense (N, 16, 3) gradient is
+// basis_k(dir_i) * acc[i, ch]; it is never materialised: each CTA takes 32
+// gaussians, one warp computes their fp64 view directions and SH bases (for
+// every view of the step) into shared memory, then 384 threads run Adam on the
+// 32 x 12 float4 chunks of SH / m / v with fully coalesced 16-byte accesses.
+// A device-side reject flag (non-finite gradient, optimize.py:72-74) skips the
+// update, and the device step counter feeds the bias corrections, so a
+// sequence of steps needs no host synchronisation.
+#include <math.h>
+
+#include "common.cuh"
+#include "shmath.cuh"
+
+namespace rcgs {
+
+constexpr int kMaxViews = 16;
+constexpr int kGPB = 32;           // gaussians per block
+constexpr int kAdamNT = kGPB * 12; // one thread per float4 of 48 coefficients
+
+struct AccViews {
+    const float* acc[kMaxViews];
+    double cen[kMaxViews][3];
+    int n;
+};
+
+struct AdamHyper {
+    float lr_dc, lr_rest, b1, b2, eps;
+};
+
+__device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const float g[4], int f0,
+                                      const AdamHyper& h, float inv_bc1, float inv_bc2) {
+    float* pp = &p.x;
+    float* mm = &m.x;
+    float* vv = &v.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int k = (f0 + j) / 3;
+        const float lr = k == 0 ? h.lr_dc : h.lr_rest;
+        mm[j] = h.b1 * mm[j] + (1.0f - h.b1) * g[j];
+        vv[j] = h.b2 * vv[j] + (1.0f - h.b2) * g[j] * g[j];
+        const float mh = mm[j] * inv_bc1, vh = vv[j] * inv_bc2;
+        pp[j] -= lr * mh / (sqrtf(vh) + h.eps);
+    }
+}
+
+__device__ __forceinline__ void bias_corr(const int64_t* step, float b1, float b2, double db1, double db2,
+                                          float& inv1, float& inv2) {
+    const double t = (double)(*step + 1);
+    inv1 = (float)(1.0 / (1.0 - pow(db1, t)));
+    inv2 = (float)(1.0 / (1.0 - pow(db2, t)));
+}
+
+__global__ void __launch_bounds__(kAdamNT) adam_fused_kernel(
+    const double* __restrict__ pos, int64_t n, int deg, float4* __restrict__ sh, float4* __restrict__ m,
+    float4* __restrict__ v, AccViews views, AdamHyper h, double db1, double db2,
+    const int32_t* __restrict__ reject, const int64_t* __restrict__ step) {
+    __shared__ float basis[kMaxViews][kGPB][16];
+    __shared__ float acc[kMaxViews][kGPB][3];
+    if (reject && *reject) return;
+    const int t = threadIdx.x;
+    const int64_t g0 = (int64_t)blockIdx.x * kGPB;
+    if (t < kGPB) {
+        const int64_t g = g0 + t;
+        if (g < n) {
+            for (int vi = 0; vi < views.n; ++vi) {
+                double x, y, z;
+                view_dir(pos, g, views.cen[vi], x, y, z);
+                double b[16];
+                sh_basis16<double>(x, y, z, deg, b);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) basis[vi][t][k] = (float)b[k];
+                const float* a = views.acc[vi] + 3 * g;
+                acc[vi][t][0] = a[0];
+                acc[vi][t][1] = a[1];
+                acc[vi][t][2] = a[2];
+            }
+        }
+    }
+    __syncthreads();
+    const int lg = t / 12, c4 = t % 12;
+    const int64_t g = g0 + lg;
+    if (g >= n) return;
+    const int f0 = 4 * c4;
+    float gr[4];
+    const float invn = 1.0f / (float)views.n;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int k = (f0 + j) / 3, ch = (f0 + j) % 3;
+        float s = 0.f;
+        for (int vi = 0; vi < views.n; ++vi) s = fmaf(basis[vi][lg][k], acc[vi][lg][ch], s);
+        gr[j] = views.n == 1 ? s : s * invn;
+    }
+    float inv1, inv2;
+    bias_corr(step, h.b1, h.b2, db1, db2, inv1, inv2);
+    const int64_t q = g * 12 + c4;
+    float4 p = sh[q], mm = m[q], vv = v[q];
+    adam4(p, mm, vv, gr, f0, h, inv1, inv2);
+    sh[q] = p;
+    m[q] = mm;
+    v[q] = vv;
+}
+
+__global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
+                                  const float4* __restrict__ grad, int64_t nq, AdamHyper h, double db1,
+                                  double db2, const int32_t* __restrict__ reject,
+                                  const int64_t* __restrict__ step) {
+    if (reject && *reject) return;
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    float inv1, inv2;
+    bias_corr(step, h.b1, h.b2, db1, db2, inv1, inv2);
+    const float4 g4 = grad[q];
+    const float gr[4] = {g4.x, g4.y, g4.z, g4.w};
+    float4 pp = p[q], mm = m[q], vv = v[q];
+    adam4(pp, mm, vv, gr, 4 * (int)(q % 12), h, inv1, inv2);
+    p[q] = pp;
+    m[q] = mm;
+    v[q] = vv;
+}
+
+__global__ void step_commit_kernel(const int32_t* __restrict__ reject, int64_t* __restrict__ step) {
+    if (!(reject && *reject)) *step += 1;
+}
+
+__global__ void sh_grad_kernel(const double* __restrict__ pos, int64_t n, int deg,
+                               const float* __restrict__ acc, Center cen, float* __restrict__ grad) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    double x, y, z;
+    view_dir(pos, g, cen.c, x, y, z);
+    double b[16];
+    sh_basis16<double>(x, y, z, deg, b);
+    const float a0 = acc[3 * g], a1 = acc[3 * g + 1], a2 = acc[3 * g + 2];
+    float* o = grad + 48 * g;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        o[3 * k] = (float)(b[k] * a0);
+        o[3 * k + 1] = (float)(b[k] * a1);
+        o[3 * k + 2] = (float)(b[k] * a2);
+    }
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ x, int64_t count, int32_t* __restrict__ flag) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+static AdamHyper hyper(const rcgs_adam_config* c) {
+    AdamHyper h;
+    h.lr_dc = (float)c->lr_dc;
+    h.lr_rest = (float)c->lr_rest;
+    h.b1 = (float)c->beta1;
+    h.b2 = (float)c->beta2;
+    h.eps = (float)c->eps;
+    return h;
+}
+
+}  // namespace rcgs
+
+using namespace rcgs;
+
+extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
+                               const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                               const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                               void* stream) {
+    RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
+    RCGS_CHECK_ARG(n_views >= 1 && n_views <= kMaxViews, "views per step must be in [1, %d]", kMaxViews);
+    cudaStream_t s = as_stream(stream);
+    if (sc->n > 0) {
+        AccViews av;
+        av.n = n_views;
+        for (int i = 0; i < n_views; ++i) {
+            av.acc[i] = h_d_accs[i];
+            for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
+        }
+        adam_fused_kernel<<<div_up(sc->n, kGPB), kAdamNT, 0, s>>>(
+            sc->pos, sc->n, sc->sh_degree, reinterpret_cast<float4*>(d_sh), reinterpret_cast<float4*>(d_m),
+            reinterpret_cast<float4*>(d_v), av, hyper(cfg), cfg->beta1, cfg->beta2, d_reject, d_step);
+        RCGS_LAUNCH_CHECK();
+    }
+    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
+                               const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                               void* stream) {
+    RCGS_CHECK_ARG(d_params && d_m && d_v && d_grads && cfg && d_step, "null argument");
+    cudaStream_t s = as_stream(stream);
+    const int64_t nq = n * 12;
+    if (nq > 0) {
+        adam_dense_kernel<<<div_up(nq, 256), 256, 0, s>>>(
+            reinterpret_cast<float4*>(d_params), reinterpret_cast<float4*>(d_m), reinterpret_cast<float4*>(d_v),
+            reinterpret_cast<const float4*>(d_grads), nq, hyper(cfg), cfg->beta1, cfg->beta2, d_reject, d_step);
+        RCGS_LAUNCH_CHECK();
+    }
+    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_sh_grad(const rcgs_scene* sc, const float* d_acc, const double* h_center3, float* d_grad,
+                            void* stream) {
+    RCGS_CHECK_ARG(sc && d_acc && h_center3 && d_grad, "null argument");
+    if (sc->n == 0) return RCGS_OK;
+    Center c;
+    for (int j = 0; j < 3; ++j) c.c[j] = h_center3[j];
+    sh_grad_kernel<<<div_up(sc->n, 256), 256, 0, as_stream(stream)>>>(sc->pos, sc->n, sc->sh_degree, d_acc, c,
+                                                                       d_grad);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_nonfinite_check(const float* d_x, int64_t count, int32_t* d_flag, void* stream) {
+    RCGS_CHECK_ARG(d_flag != nullptr, "null flag");
+    if (count <= 0) return RCGS_OK;
+    unsigned blocks = div_up(count, 256);
+    if (blocks > 4096) blocks = 4096;
+    nonfinite_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_x, count, d_flag);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}

@@ -1,0 +1,132 @@
+// Shared helpers for the rcgs CUDA library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/rcgs.h"
+
+namespace rcgs {
+
+constexpr int kTile = 16;                 // 16x16 pixel tiles, one CTA each
+constexpr int kTilePixels = kTile * kTile;
+
+void set_error(const char* fmt, ...);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define RCGS_CHECK_ARG(cond, ...)          \
+    do {                                   \
+        if (!(cond)) {                     \
+            ::rcgs::set_error(__VA_ARGS__); \
+            return RCGS_EINVAL;            \
+        }                                  \
+    } while (0)
+
+#define RCGS_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t err__ = (call);                                                       \
+        if (err__ != cudaSuccess) {                                                       \
+            ::rcgs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,                  \
+                              cudaGetErrorString(err__));                                 \
+            return RCGS_ECUDA;                                                            \
+        }                                                                                 \
+    } while (0)
+
+#define RCGS_LAUNCH_CHECK() RCGS_CUDA(cudaGetLastError())
+
+#define RCGS_TRY(expr)               \
+    do {                             \
+        int st__ = (expr);           \
+        if (st__ != RCGS_OK) return st__; \
+    } while (0)
+
+inline unsigned div_up(int64_t a, int64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Stream-ordered device allocation from the default memory pool.
+template <typename T>
+int dalloc(T** p, size_t count, cudaStream_t s) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s);
+    if (e != cudaSuccess) {
+        set_error("cudaMallocAsync(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+        return RCGS_ENOMEM;
+    }
+    return RCGS_OK;
+}
+
+template <typename T>
+void dfree(T*& p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+}
+
+// Pinned scratch for small device->host readbacks (per thread).
+void* pinned_scratch(size_t bytes);
+
+// ---- device scan / radix sort (scan.cu, radix.cu) -------------------------------
+// Exclusive scan of n uint32 counts into out (n+1 entries; out[n] = total).
+int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s);
+// Stable LSD radix sort of (key, value) pairs over key bits [0, end_bit).
+// keys/vals are double-buffered: on return *key_cur / *val_cur point at the sorted data.
+// vals_in may be null: values then start as the element index.
+int radix_sort_u64(uint64_t** key_cur, uint64_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
+                   bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
+int radix_sort_u32(uint32_t** key_cur, uint32_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
+                   bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
+
+// ---- small device math ----------------------------------------------------------
+// world->camera transform exactly as numpy/OpenBLAS evaluates P @ R.T + t
+// (oracle/c/rcgs_oracle.c restates it).
+__device__ __forceinline__ double cam_coord(const double* R, const double* t, int k, double p0,
+                                            double p1, double p2) {
+    return __dadd_rn(__fma_rn(p2, R[3 * k + 2], __fma_rn(p1, R[3 * k + 1], __dmul_rn(p0, R[3 * k + 0]))),
+                     t[k]);
+}
+
+}  // namespace rcgs
+
+// The opaque handles (shared between translation units).
+struct rcgs_scene {
+    int64_t n;
+    int sh_degree;
+    double* pos;     // (n,3)
+    double* cov3d;   // (n,6): xx, xy, xz, yy, yz, zz
+    double* opac;    // (n,)
+};
+
+// Raster record of one kept gaussian (rank s), fp32, 48 bytes.
+struct __align__(16) RasterRec {
+    float4 mean;   // mx_hi, my_hi, mx_lo, my_lo   (mean2d = hi + lo)
+    float4 conic;  // -a/2, -b, -c/2, opacity      (power = nha dx^2 + nb dx dy + nhc dy^2)
+    float4 gate;   // p_lo, p_hi, delta, unused    (skip if power < p_lo; exact check below p_hi)
+};
+
+// Exact (fp64) record for guarded decisions: the reference's own operands.
+struct ExactRec {
+    double mx, my, ca, cb, cc, op;
+};
+
+struct rcgs_view {
+    const rcgs_scene* scene;
+    rcgs_camera cam;
+    rcgs_raster_config cfg;
+    int64_t n, k, pairs;
+    int tiles_x, tiles_y, sort_bits;
+    // per kept rank s (front to back)
+    uint32_t* gid;        // (k,) scene index
+    double* z;            // (k,) view-space z (bit-exact reference depth)
+    RasterRec* rec;       // (k,)
+    ExactRec* exact;      // (k,)
+    uint32_t* offs;       // (k+1,) first emission slot of s; offs[k] = pairs
+    float4* color;        // (k,) rgb + active bits (as float 0..7) per step
+    int32_t* rank_of;     // (n,) s or -1 (culled)
+    // per pair (sorted by tile, then depth)
+    uint32_t* pair_s;     // (pairs,) rank s
+    uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
+    uint2* ranges;        // (tiles,) [start, end)
+};

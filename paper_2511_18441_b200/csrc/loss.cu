@@ -1,0 +1,314 @@
+// K5: photometric loss + image gradient (losses.py:68-134), fp64 arithmetic.
+//
+// total = (1 - lam) * L1 + lam * (1 - SSIM), SSIM with an 11-tap separable
+// gaussian (sigma 1.5), zero padding and division by the in-image kernel mass.
+// The hand-derived gradient (losses.py:104-115) is linear in five filtered
+// maps; by linearity it collapses to three:
+//   dSSIM/dy = [F(M1) + 2 y F(M2) + g F(M3)] / n,
+//   M1 = (d_mu1 - 2 d_var1 mu1 - d_cov mu2) / mass, M2 = d_var1 / mass,
+//   M3 = d_cov / mass.
+// Pass A: moments (5 maps, separable in shared memory) -> SSIM map, |y-g|,
+//         M1..M3 (fp64), per-block partial sums, "images differ" flag.
+// Pass B: separable filter of M1..M3 -> gradient (fp32 out); exactly zero when
+//         the images are identical (losses.py:127-130).
+// Pass C: fixed-order final reduction -> {l1, ssim, total} (deterministic).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace rcgs {
+
+constexpr int kR = 5;            // window half width
+constexpr int kWin = 2 * kR + 1; // 11
+constexpr int kLT = 16;          // output tile
+constexpr int kLH = kLT + 2 * kR;  // 26
+
+struct Window {
+    double w[kWin];
+};
+
+__device__ __forceinline__ double mass1d(const Window& W, int i, int len) {
+    double m = 0.0;
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) {
+        const int j = i + k - kR;
+        if (j >= 0 && j < len) m += W.w[k];
+    }
+    return m;
+}
+
+template <int NT>
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sh[2 * warp] = a;
+        sh[2 * warp + 1] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int w = 0; w < NT / 32; ++w) {
+            x += sh[2 * w];
+            y += sh[2 * w + 1];
+        }
+        a = x;
+        b = y;
+    }
+}
+
+// ---------------------------------------------------------------- pass A
+template <bool SSIM>
+__global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
+                                                   const float* __restrict__ g, int H, int W,
+                                                   Window win, double* __restrict__ maps,
+                                                   double* __restrict__ block_part,
+                                                   int32_t* __restrict__ differ) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* iy = reinterpret_cast<float*>(smem_raw);               // [26][26][3]
+    float* ig = iy + kLH * kLH * 3;                               // [26][26][3]
+    double* hs = reinterpret_cast<double*>(ig + kLH * kLH * 3);   // [5][26][16][3]
+    __shared__ double red[16];
+    const int t = threadIdx.x;
+    const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+    const int64_t npix = (int64_t)H * W;
+
+    double l1 = 0.0, ss = 0.0;
+    int diff = 0;
+    if (SSIM) {
+        for (int i = t; i < kLH * kLH * 3; i += 256) {
+            const int ch = i % 3, p = i / 3, r = p / kLH, c = p % kLH;
+            const int gy = y0 - kR + r, gx = x0 - kR + c;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
+            iy[i] = in ? y[gi] : 0.f;
+            ig[i] = in ? g[gi] : 0.f;
+        }
+        __syncthreads();
+        // horizontal pass: rows 0..25, output cols 0..15
+        for (int i = t; i < kLH * kLT * 3; i += 256) {
+            const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
+            double s1 = 0, s2 = 0, s11 = 0, s22 = 0, s12 = 0;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const int o = (r * kLH + c + k) * 3 + ch;
+                const double a = iy[o], b = ig[o], w = win.w[k];
+                s1 += w * a;
+                s2 += w * b;
+                s11 += w * (a * a);
+                s22 += w * (b * b);
+                s12 += w * (a * b);
+            }
+            const int base = (r * kLT + c) * 3 + ch;
+            const int plane = kLH * kLT * 3;
+            hs[base] = s1;
+            hs[plane + base] = s2;
+            hs[2 * plane + base] = s11;
+            hs[3 * plane + base] = s22;
+            hs[4 * plane + base] = s12;
+        }
+        __syncthreads();
+    }
+    for (int i = t; i < kLT * kLT * 3; i += 256) {
+        const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
+        const int gy = y0 + r, gx = x0 + c;
+        if (gy >= H || gx >= W) continue;
+        const int64_t pix = (int64_t)gy * W + gx;
+        const float fy = y[pix * 3 + ch], fg = g[pix * 3 + ch];
+        l1 += fabs((double)fy - (double)fg);
+        diff |= (fy != fg);
+        if (SSIM) {
+            const int plane = kLH * kLT * 3;
+            double m1 = 0, m2 = 0, m11 = 0, m22 = 0, m12 = 0;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const int base = ((r + k) * kLT + c) * 3 + ch;
+                const double w = win.w[k];
+                m1 += w * hs[base];
+                m2 += w * hs[plane + base];
+                m11 += w * hs[2 * plane + base];
+                m22 += w * hs[3 * plane + base];
+                m12 += w * hs[4 * plane + base];
+            }
+            const double mass = mass1d(win, gy, H) * mass1d(win, gx, W);
+            const double mu1 = m1 / mass, mu2 = m2 / mass;
+            const double var1 = m11 / mass - mu1 * mu1;
+            const double var2 = m22 / mass - mu2 * mu2;
+            const double cov = m12 / mass - mu1 * mu2;
+            const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
+            const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
+            ss += (a1 * a2) / (b1 * b2);
+            const double d_mu1 = 2.0 * (mu2 * a2) / (b1 * b2) - 2.0 * mu1 * a1 * a2 / (b1 * b1 * b2);
+            const double d_var1 = -(a1 * a2) / (b1 * b2 * b2);
+            const double d_cov = 2.0 * a1 / (b1 * b2);
+            const int64_t o = pix * 3 + ch;
+            maps[o] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) / mass;
+            maps[npix * 3 + o] = d_var1 / mass;
+            maps[2 * npix * 3 + o] = d_cov / mass;
+        }
+    }
+    if (__syncthreads_or(diff) && t == 0) atomicOr(differ, 1);
+    block_sum2<256>(l1, ss, red);
+    if (t == 0) {
+        const int b = blockIdx.y * gridDim.x + blockIdx.x;
+        block_part[2 * b] = l1;
+        block_part[2 * b + 1] = ss;
+    }
+}
+
+// ---------------------------------------------------------------- pass B
+template <bool SSIM>
+__global__ void __launch_bounds__(256) loss_pass_b(const float* __restrict__ y,
+                                                   const float* __restrict__ g, int H, int W,
+                                                   Window win, double lam,
+                                                   const double* __restrict__ maps,
+                                                   const int32_t* __restrict__ differ,
+                                                   float* __restrict__ grad) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* im = reinterpret_cast<double*>(smem_raw);  // [3 maps][26][26][3]
+    double* hs = im + 3 * kLH * kLH * 3;               // [3 maps][26][16][3]
+    const int t = threadIdx.x;
+    const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+    const int64_t npix = (int64_t)H * W;
+    const double n = (double)(npix * 3);
+    const bool any = *differ != 0;
+    if (SSIM && any) {
+        for (int i = t; i < kLH * kLH * 3; i += 256) {
+            const int ch = i % 3, p = i / 3, r = p / kLH, c = p % kLH;
+            const int gy = y0 - kR + r, gx = x0 - kR + c;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) im[m * kLH * kLH * 3 + i] = in ? maps[m * npix * 3 + gi] : 0.0;
+        }
+        __syncthreads();
+        for (int i = t; i < kLH * kLT * 3; i += 256) {
+            const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) s += win.w[k] * im[m * kLH * kLH * 3 + (r * kLH + c + k) * 3 + ch];
+                hs[m * kLH * kLT * 3 + (r * kLT + c) * 3 + ch] = s;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = t; i < kLT * kLT * 3; i += 256) {
+        const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
+        const int gy = y0 + r, gx = x0 + c;
+        if (gy >= H || gx >= W) continue;
+        const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+        if (!any) {
+            grad[o] = 0.f;
+            continue;
+        }
+        const float fy = y[o], fg = g[o];
+        const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
+        double out = (1.0 - lam) * sgn / n;
+        if (SSIM) {
+            double f[3];
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) s += win.w[k] * hs[m * kLH * kLT * 3 + ((r + k) * kLT + c) * 3 + ch];
+                f[m] = s;
+            }
+            const double ds = (f[0] + 2.0 * (double)fy * f[1] + (double)fg * f[2]) / n;
+            out -= lam * ds;
+        }
+        grad[o] = (float)out;
+    }
+}
+
+__global__ void loss_pass_c(const double* __restrict__ part, int nb, double n, double lam,
+                            bool ssim_valid, double* __restrict__ out3) {
+    __shared__ double red[16];
+    double a = 0.0, b = 0.0;
+    // fixed assignment of blocks to threads and a fixed reduction tree: deterministic
+    for (int i = threadIdx.x; i < nb; i += 256) {
+        a += part[2 * i];
+        b += part[2 * i + 1];
+    }
+    block_sum2<256>(a, b, red);
+    if (threadIdx.x == 0) {
+        const double l1 = a / n;
+        const double ss = ssim_valid ? b / n : __longlong_as_double(0x7ff8000000000000ll);
+        out3[0] = l1;
+        out3[1] = ss;
+        out3[2] = lam == 0.0 ? l1 : (1.0 - lam) * l1 + lam * (1.0 - ss);
+    }
+}
+
+static Window make_window() {
+    Window w;
+    double sum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+        const double off = (double)(i - kR);
+        w.w[i] = exp(-(off * off) / (2.0 * 1.5 * 1.5));
+        sum += w.w[i];
+    }
+    for (int i = 0; i < kWin; ++i) w.w[i] /= sum;
+    return w;
+}
+
+}  // namespace rcgs
+
+using namespace rcgs;
+
+extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height,
+                              int32_t width, double lam, double* d_loss3, float* d_grad,
+                              void* stream) {
+    RCGS_CHECK_ARG(d_image && d_target && d_loss3 && d_grad, "null argument");
+    RCGS_CHECK_ARG(height > 0 && width > 0, "expected (H, W, 3) images, got (%d, %d, 3)", height, width);
+    RCGS_CHECK_ARG(lam >= 0.0 && lam <= 1.0, "lam must be in [0, 1]");
+    const bool ssim_ok = height >= kWin && width >= kWin;
+    RCGS_CHECK_ARG(ssim_ok || lam == 0.0, "images must be at least %dpx on each side for SSIM", kWin);
+    cudaStream_t s = as_stream(stream);
+    const Window win = make_window();
+    const dim3 grid(div_up(width, kLT), div_up(height, kLT));
+    const int nb = grid.x * grid.y;
+    const int64_t npix = (int64_t)height * width;
+    double *maps = nullptr, *part = nullptr;
+    int32_t* differ = nullptr;
+    RCGS_TRY(dalloc(&part, 2 * nb, s));
+    RCGS_TRY(dalloc(&differ, 1, s));
+    RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
+    const size_t smem_a = 2 * kLH * kLH * 3 * sizeof(float) + 5 * kLH * kLT * 3 * sizeof(double);
+    const size_t smem_b = 3 * kLH * kLH * 3 * sizeof(double) + 3 * kLH * kLT * 3 * sizeof(double);
+    if (ssim_ok) {
+        RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
+        static bool attr = false;
+        if (!attr) {
+            RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
+            RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+            attr = true;
+        }
+        loss_pass_a<true><<<grid, 256, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
+        RCGS_LAUNCH_CHECK();
+        if (lam > 0.0) {
+            loss_pass_b<true><<<grid, 256, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                        differ, d_grad);
+        } else {
+            loss_pass_b<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                    differ, d_grad);
+        }
+        RCGS_LAUNCH_CHECK();
+    } else {
+        loss_pass_a<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
+        loss_pass_b<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
+                                                d_grad);
+        RCGS_LAUNCH_CHECK();
+    }
+    loss_pass_c<<<1, 256, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
+    RCGS_LAUNCH_CHECK();
+    dfree(maps, s);
+    dfree(part, s);
+    dfree(differ, s);
+    return RCGS_OK;
+}

@@ -1,0 +1,568 @@
+// K1 per-gaussian preprocess + K2 tile binning (render.py:172-229 restated for
+// sm_100a).
+//
+// Everything that drives a discrete decision is evaluated in fp64 with the
+// reference's own operation order: the world->camera FMA chain (numpy/OpenBLAS
+// P @ R.T + t), the near clip, mean2d = fx*x/z + cx, the 3-sigma viewport cull,
+// and the depth keys.  The raster consumes fp32 records plus per-gaussian
+// guard bands (p_lo/p_hi/delta) that route the rare near-threshold decisions
+// back to fp64 (see raster.cu).
+//
+// Pipeline per view (one handle):
+//   k1_cull      per gaussian: fp64 projection -> kept flag + z key (+ key min/max)
+//   scan/compact stable list of kept scene indices (ascending index)
+//   radix sort   stable LSD sort of the z bit patterns over their varying bits
+//                (== np.argsort(z, kind="stable"), render.py:216)
+//   k1_record    per rank s: raster record, exact record, z, tile rect, count
+//   scan         emission offsets offs[s] (pairs emitted in rank order)
+//   k2_emit      one (tile, e) pair per overlapped tile
+//   radix sort   stable sort on tile id -> (tile, depth) order
+//   k2_ranges    per-tile [start, end) + rank/e lookup per pair
+#include <math.h>
+
+#include "common.cuh"
+#include "shmath.cuh"
+
+namespace rcgs {
+
+struct ProjF64 {
+    bool kept;
+    double z, mx, my, a, b, c, det;
+};
+
+__device__ __forceinline__ ProjF64 project_one(const double* __restrict__ pos,
+                                               const double* __restrict__ cov3d, int64_t g,
+                                               const rcgs_camera& cam,
+                                               const rcgs_raster_config& cfg) {
+    ProjF64 p;
+    const double p0 = pos[3 * g], p1 = pos[3 * g + 1], p2 = pos[3 * g + 2];
+    const double x = cam_coord(cam.R, cam.t, 0, p0, p1, p2);
+    const double y = cam_coord(cam.R, cam.t, 1, p0, p1, p2);
+    const double z = cam_coord(cam.R, cam.t, 2, p0, p1, p2);
+    p.z = z;
+    p.kept = false;
+    if (!(z > cfg.near_clip)) return p;  // render.py:176
+    // mean2d = fx * x / z + cx (render.py:182), evaluated left to right, unfused
+    p.mx = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fx, x), z), cam.cx);
+    p.my = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fy, y), z), cam.cy);
+    // EWA Jacobian and cov2d = (J W) Sigma (J W)^T + dilation (render.py:184-194)
+    const double zz = __dmul_rn(z, z);
+    const double j00 = __ddiv_rn(cam.fx, z);
+    const double j02 = __ddiv_rn(__dmul_rn(-cam.fx, x), zz);
+    const double j11 = __ddiv_rn(cam.fy, z);
+    const double j12 = __ddiv_rn(__dmul_rn(-cam.fy, y), zz);
+    const double* R = cam.R;
+    double t0[3], t1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        t0[k] = j00 * R[0 * 3 + k] + j02 * R[2 * 3 + k];
+        t1[k] = j11 * R[1 * 3 + k] + j12 * R[2 * 3 + k];
+    }
+    const double* S = cov3d + 6 * g;  // xx xy xz yy yz zz
+    const double s00 = S[0], s01 = S[1], s02 = S[2], s11 = S[3], s12 = S[4], s22 = S[5];
+    double u0[3], u1[3];  // Sigma t^T rows
+    u0[0] = s00 * t0[0] + s01 * t0[1] + s02 * t0[2];
+    u0[1] = s01 * t0[0] + s11 * t0[1] + s12 * t0[2];
+    u0[2] = s02 * t0[0] + s12 * t0[1] + s22 * t0[2];
+    u1[0] = s00 * t1[0] + s01 * t1[1] + s02 * t1[2];
+    u1[1] = s01 * t1[0] + s11 * t1[1] + s12 * t1[2];
+    u1[2] = s02 * t1[0] + s12 * t1[1] + s22 * t1[2];
+    const double a = t0[0] * u0[0] + t0[1] * u0[1] + t0[2] * u0[2] + cfg.covariance_dilation;
+    const double b = t0[0] * u1[0] + t0[1] * u1[1] + t0[2] * u1[2];
+    const double c = t1[0] * u1[0] + t1[1] * u1[1] + t1[2] * u1[2] + cfg.covariance_dilation;
+    // det, lambda_max, 3-sigma radius and viewport test (render.py:196-205), unfused
+    const double det = __dsub_rn(__dmul_rn(a, c), __dmul_rn(b, b));
+    const double mid = __dmul_rn(0.5, __dadd_rn(a, c));
+    const double lam = __dadd_rn(mid, sqrt(fmax(__dsub_rn(__dmul_rn(mid, mid), det), 0.0)));
+    const double radius = __dmul_rn(cfg.footprint_sigmas, sqrt(lam));
+    const double w1 = (double)(cam.width - 1), h1 = (double)(cam.height - 1);
+    p.kept = (det > 0) && (__dadd_rn(p.mx, radius) >= 0) && (__dsub_rn(p.mx, radius) <= w1) &&
+             (__dadd_rn(p.my, radius) >= 0) && (__dsub_rn(p.my, radius) <= h1);
+    p.a = a;
+    p.b = b;
+    p.c = c;
+    p.det = det;
+    return p;
+}
+
+// ---------------------------------------------------------------- scene
+__global__ void cov3d_kernel(const double* __restrict__ rot, const double* __restrict__ scale,
+                             int64_t n, double* __restrict__ cov) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const double w = rot[4 * g], x = rot[4 * g + 1], y = rot[4 * g + 2], z = rot[4 * g + 3];
+    // quaternion_to_rotation (scene.py:98-112)
+    double r[3][3];
+    r[0][0] = 1 - 2 * (y * y + z * z);
+    r[0][1] = 2 * (x * y - w * z);
+    r[0][2] = 2 * (x * z + w * y);
+    r[1][0] = 2 * (x * y + w * z);
+    r[1][1] = 1 - 2 * (x * x + z * z);
+    r[1][2] = 2 * (y * z - w * x);
+    r[2][0] = 2 * (x * z - w * y);
+    r[2][1] = 2 * (y * z + w * x);
+    r[2][2] = 1 - 2 * (x * x + y * y);
+    double m[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) m[i][j] = r[i][j] * scale[3 * g + j];
+    double s[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s[i][j] = m[i][0] * m[j][0] + m[i][1] * m[j][1] + m[i][2] * m[j][2];
+    double* o = cov + 6 * g;
+    o[0] = s[0][0];
+    o[1] = s[0][1];
+    o[2] = s[0][2];
+    o[3] = s[1][1];
+    o[4] = s[1][2];
+    o[5] = s[2][2];
+}
+
+// ---------------------------------------------------------------- K1a cull + keys
+__global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __restrict__ cov3d,
+                               int64_t n, rcgs_camera cam, rcgs_raster_config cfg,
+                               uint32_t* __restrict__ flag, uint64_t* __restrict__ key,
+                               unsigned long long* __restrict__ minmax) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    if (g < n) {
+        ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
+        flag[g] = p.kept ? 1u : 0u;
+        uint64_t k = (uint64_t)__double_as_longlong(p.z);  // z > near_clip > 0: bits order like values
+        key[g] = k;
+        if (p.kept) {
+            kmin = k;
+            kmax = k;
+        }
+    }
+    // block min/max -> one atomic per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && kmax != 0ull) {
+        atomicMin(&minmax[0], kmin);
+        atomicMax(&minmax[1], kmax);
+    }
+}
+
+__global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                               const uint64_t* __restrict__ key, int64_t n,
+                               uint64_t* __restrict__ kkey, uint32_t* __restrict__ kgid) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n && flag[g]) {
+        uint32_t d = pos[g];
+        kkey[d] = key[g];
+        kgid[d] = (uint32_t)g;
+    }
+}
+
+// ---------------------------------------------------------------- K1b records
+struct Rect {
+    int16_t x0, y0, x1, y1;  // inclusive tile rect; x1 < x0 => empty
+};
+
+__global__ void k1_record_kernel(const double* __restrict__ pos, const double* __restrict__ cov3d,
+                                 const double* __restrict__ opac, const uint32_t* __restrict__ sgid,
+                                 int64_t k, rcgs_camera cam, rcgs_raster_config cfg, int tiles_x,
+                                 int tiles_y, uint32_t* __restrict__ gid_out,
+                                 double* __restrict__ z_out, RasterRec* __restrict__ rec,
+                                 ExactRec* __restrict__ exact, int32_t* __restrict__ rank_of,
+                                 Rect* __restrict__ rect, uint32_t* __restrict__ count) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    const uint32_t g = sgid[s];
+    ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
+    gid_out[s] = g;
+    z_out[s] = p.z;
+    rank_of[g] = (int32_t)s;
+    const double op = opac[g];
+    // conic = inverse(cov2d) (render.py:221-223)
+    const double ca = __ddiv_rn(p.c, p.det), cb = __ddiv_rn(-p.b, p.det), cc = __ddiv_rn(p.a, p.det);
+    ExactRec ex;
+    ex.mx = p.mx;
+    ex.my = p.my;
+    ex.ca = ca;
+    ex.cb = cb;
+    ex.cc = cc;
+    ex.op = op;
+    exact[s] = ex;
+
+    RasterRec r;
+    const float mxh = (float)p.mx, myh = (float)p.my;
+    r.mean = make_float4(mxh, myh, (float)(p.mx - (double)mxh), (float)(p.my - (double)myh));
+    r.conic = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)op);
+    // alpha >= skip  <=>  power >= P := log(skip / op).  fp32 power error is bounded by
+    // |power| * 2 / (1 - |rho|) * 5.4e-7 (rho = conic correlation); a 4x safety
+    // factor gives the exact-check band [p_lo, p_hi).
+    const double P = log(cfg.alpha_skip / op);
+    const double rho = fmin(fabs(cb) / sqrt(ca * cc), 0.999999);
+    const double margin = fabs(P) * 4.4e-6 / (1.0 - rho) + 1e-6;
+    r.gate = make_float4((float)(P - margin), (float)(P + margin), (float)(margin + 1e-6), 0.f);
+    rec[s] = r;
+
+    // opacity-aware footprint: alpha >= skip inside d^T conic d <= r2 = 2 ln(op/skip);
+    // axis half widths r * sqrt(cov2d diag), padded for fp64 rounding.
+    Rect rc;
+    rc.x0 = 0;
+    rc.y0 = 0;
+    rc.x1 = -1;
+    rc.y1 = -1;
+    const double r2 = -2.0 * P;
+    if (r2 >= 0.0) {
+        const double ex_ = sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4;
+        const double ey_ = sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4;
+        const double umin = fmax(ceil(p.mx - ex_), 0.0), umax = fmin(floor(p.mx + ex_), cam.width - 1.0);
+        const double vmin = fmax(ceil(p.my - ey_), 0.0), vmax = fmin(floor(p.my + ey_), cam.height - 1.0);
+        if (umin <= umax && vmin <= vmax) {
+            rc.x0 = (int16_t)((int)umin / kTile);
+            rc.x1 = (int16_t)((int)umax / kTile);
+            rc.y0 = (int16_t)((int)vmin / kTile);
+            rc.y1 = (int16_t)((int)vmax / kTile);
+        }
+    }
+    rect[s] = rc;
+    count[s] = rc.x1 >= rc.x0 ? (uint32_t)(rc.x1 - rc.x0 + 1) * (uint32_t)(rc.y1 - rc.y0 + 1) : 0u;
+}
+
+// ---------------------------------------------------------------- K2 emission
+__global__ void k2_emit_kernel(const Rect* __restrict__ rect, const uint32_t* __restrict__ offs,
+                               int64_t k, int tiles_x, uint32_t* __restrict__ tile_key,
+                               uint32_t* __restrict__ emit_s) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    Rect rc = rect[s];
+    uint32_t e = offs[s];
+    for (int ty = rc.y0; ty <= rc.y1; ++ty)
+        for (int tx = rc.x0; tx <= rc.x1; ++tx) {
+            tile_key[e] = (uint32_t)(ty * tiles_x + tx);
+            emit_s[e] = (uint32_t)s;
+            ++e;
+        }
+}
+
+__global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key,
+                                 const uint32_t* __restrict__ pair_e,
+                                 const uint32_t* __restrict__ emit_s, int64_t pairs,
+                                 uint2* __restrict__ ranges, uint32_t* __restrict__ pair_s) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= pairs) return;
+    pair_s[j] = emit_s[pair_e[j]];
+    uint32_t t = tile_key[j];
+    if (j == 0 || tile_key[j - 1] != t) ranges[t].x = (uint32_t)j;
+    if (j == pairs - 1 || tile_key[j + 1] != t) ranges[t].y = (uint32_t)(j + 1);
+}
+
+// ---------------------------------------------------------------- colour (per step)
+__global__ void color_kernel(const double* __restrict__ pos, const float* __restrict__ sh,
+                             const uint32_t* __restrict__ gid, int64_t k, Center cen, int deg,
+                             float4* __restrict__ color) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    const uint32_t g = gid[s];
+    double x, y, z;
+    view_dir(pos, g, cen.c, x, y, z);
+    double b[16];
+    sh_basis16<double>(x, y, z, deg, b);
+    const float* c = sh + (int64_t)g * 48;
+    const int rows = (deg + 1) * (deg + 1);
+    double raw[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < rows; ++i) {
+        raw[0] += b[i] * (double)c[3 * i];
+        raw[1] += b[i] * (double)c[3 * i + 1];
+        raw[2] += b[i] * (double)c[3 * i + 2];
+    }
+    int act = 0;
+    float col[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const double v = raw[ch] + 0.5;
+        act |= (v > 0.0) << ch;
+        col[ch] = (float)fmax(0.0, v);
+    }
+    color[s] = make_float4(col[0], col[1], col[2], __int_as_float(act));
+}
+
+__global__ void basis_export_kernel(const double* __restrict__ pos, const uint32_t* __restrict__ gid,
+                                    const float4* __restrict__ color, int64_t k, Center cen, int deg,
+                                    double* __restrict__ basis, uint8_t* __restrict__ active) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    if (basis) {
+        double x, y, z;
+        view_dir(pos, gid[s], cen.c, x, y, z);
+        double b[16];
+        sh_basis16<double>(x, y, z, deg, b);
+        for (int i = 0; i < 16; ++i) basis[16 * s + i] = b[i];
+    }
+    if (active) {
+        const int a = __float_as_int(color[s].w);
+        active[3 * s] = a & 1;
+        active[3 * s + 1] = (a >> 1) & 1;
+        active[3 * s + 2] = (a >> 2) & 1;
+    }
+}
+
+__global__ void kept_export_kernel(const uint32_t* __restrict__ gid, const double* __restrict__ z,
+                                   int64_t k, int64_t* __restrict__ idx_out,
+                                   double* __restrict__ z_out) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    if (idx_out) idx_out[s] = gid[s];
+    if (z_out) z_out[s] = z[s];
+}
+
+static int validate_camera(const rcgs_camera* cam) {
+    RCGS_CHECK_ARG(cam != nullptr, "camera is null");
+    RCGS_CHECK_ARG(cam->width > 0 && cam->height > 0, "intrinsics: non-positive image dimensions");
+    RCGS_CHECK_ARG(cam->fx > 0 && cam->fy > 0, "intrinsics: non-positive focal length");
+    RCGS_CHECK_ARG((cam->width + kTile - 1) / kTile < 32768 && (cam->height + kTile - 1) / kTile < 32768,
+                   "image too large");
+    return RCGS_OK;
+}
+
+}  // namespace rcgs
+
+using namespace rcgs;
+
+extern "C" int rcgs_scene_create(const double* d_positions, const double* d_rotations,
+                                 const double* d_scales, const double* d_opacities, int64_t n,
+                                 int sh_degree, void* stream, rcgs_scene** out) {
+    RCGS_CHECK_ARG(out != nullptr, "out is null");
+    RCGS_CHECK_ARG(n >= 0 && n < (int64_t)0x7fffffff, "scene size %lld out of range", (long long)n);
+    RCGS_CHECK_ARG(sh_degree >= 0 && sh_degree <= 3, "sh_degree must be in [0, 3]");
+    cudaStream_t s = as_stream(stream);
+    rcgs_scene* sc = new rcgs_scene();
+    sc->n = n;
+    sc->sh_degree = sh_degree;
+    int st = RCGS_OK;
+    if ((st = dalloc(&sc->pos, 3 * n, s)) || (st = dalloc(&sc->cov3d, 6 * n, s)) ||
+        (st = dalloc(&sc->opac, n, s))) {
+        dfree(sc->pos, s);
+        dfree(sc->cov3d, s);
+        dfree(sc->opac, s);
+        delete sc;
+        return st;
+    }
+    if (n > 0) {
+        RCGS_CUDA(cudaMemcpyAsync(sc->pos, d_positions, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        RCGS_CUDA(cudaMemcpyAsync(sc->opac, d_opacities, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        cov3d_kernel<<<div_up(n, 256), 256, 0, s>>>(d_rotations, d_scales, n, sc->cov3d);
+        RCGS_LAUNCH_CHECK();
+    }
+    *out = sc;
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_scene_destroy(rcgs_scene* sc, void* stream) {
+    if (!sc) return RCGS_OK;
+    cudaStream_t s = as_stream(stream);
+    dfree(sc->pos, s);
+    dfree(sc->cov3d, s);
+    dfree(sc->opac, s);
+    delete sc;
+    return RCGS_OK;
+}
+
+static void view_free(rcgs_view* v, cudaStream_t s) {
+    dfree(v->gid, s);
+    dfree(v->z, s);
+    dfree(v->rec, s);
+    dfree(v->exact, s);
+    dfree(v->offs, s);
+    dfree(v->color, s);
+    dfree(v->rank_of, s);
+    dfree(v->pair_s, s);
+    dfree(v->pair_e, s);
+    dfree(v->ranges, s);
+}
+
+extern "C" int rcgs_view_destroy(rcgs_view* v, void* stream) {
+    if (!v) return RCGS_OK;
+    view_free(v, as_stream(stream));
+    delete v;
+    return RCGS_OK;
+}
+
+static int view_build(rcgs_view* v, cudaStream_t s) {
+    const rcgs_scene* sc = v->scene;
+    const int64_t n = sc->n;
+    const int ntiles = v->tiles_x * v->tiles_y;
+    RCGS_TRY(dalloc(&v->rank_of, n, s));
+    RCGS_TRY(dalloc(&v->ranges, ntiles, s));
+    if (n > 0) RCGS_CUDA(cudaMemsetAsync(v->rank_of, 0xff, n * sizeof(int32_t), s));
+    RCGS_CUDA(cudaMemsetAsync(v->ranges, 0, ntiles * sizeof(uint2), s));
+    v->k = 0;
+    v->pairs = 0;
+    v->sort_bits = 0;
+    if (n == 0) {
+        RCGS_TRY(dalloc(&v->offs, 1, s));
+        RCGS_CUDA(cudaMemsetAsync(v->offs, 0, sizeof(uint32_t), s));
+        return RCGS_OK;
+    }
+    // ---- K1a: cull + keys
+    uint32_t *flag = nullptr, *kpos = nullptr, *kgid = nullptr, *kgid_alt = nullptr;
+    uint64_t *key = nullptr, *kkey = nullptr, *kkey_alt = nullptr;
+    unsigned long long* minmax = nullptr;
+    RCGS_TRY(dalloc(&flag, n, s));
+    RCGS_TRY(dalloc(&kpos, n + 1, s));
+    RCGS_TRY(dalloc(&key, n, s));
+    RCGS_TRY(dalloc(&minmax, 2, s));
+    {
+        unsigned long long init[2] = {~0ull, 0ull};
+        RCGS_CUDA(cudaMemcpyAsync(minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    }
+    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, n, v->cam, v->cfg, flag, key, minmax);
+    RCGS_LAUNCH_CHECK();
+    RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
+    uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));
+    RCGS_CHECK_ARG(host != nullptr, "pinned scratch allocation failed");
+    uint32_t* hk = reinterpret_cast<uint32_t*>(host + 2);
+    RCGS_CUDA(cudaMemcpyAsync(host, minmax, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaMemcpyAsync(hk, kpos + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaStreamSynchronize(s));
+    const int64_t k = *hk;
+    const uint64_t kmin = host[0], kmax = host[1];
+    v->k = k;
+    RCGS_TRY(dalloc(&v->offs, k + 1, s));
+    if (k == 0) {
+        RCGS_CUDA(cudaMemsetAsync(v->offs, 0, sizeof(uint32_t), s));
+        dfree(flag, s);
+        dfree(kpos, s);
+        dfree(key, s);
+        dfree(minmax, s);
+        return RCGS_OK;
+    }
+    RCGS_TRY(dalloc(&kkey, k, s));
+    RCGS_TRY(dalloc(&kkey_alt, k, s));
+    RCGS_TRY(dalloc(&kgid, k, s));
+    RCGS_TRY(dalloc(&kgid_alt, k, s));
+    compact_kernel<<<div_up(n, 256), 256, 0, s>>>(flag, kpos, key, n, kkey, kgid);
+    RCGS_LAUNCH_CHECK();
+    dfree(flag, s);
+    dfree(kpos, s);
+    dfree(key, s);
+    dfree(minmax, s);
+    // ---- stable depth sort over the varying key bits
+    const uint64_t diff = kmin ^ kmax;
+    v->sort_bits = diff ? 64 - __builtin_clzll(diff) : 0;
+    if (v->sort_bits > 0)
+        RCGS_TRY(radix_sort_u64(&kkey, &kkey_alt, &kgid, &kgid_alt, false, k, v->sort_bits, s));
+    dfree(kkey, s);
+    dfree(kkey_alt, s);
+    dfree(kgid_alt, s);
+    // ---- K1b records
+    Rect* rect = nullptr;
+    uint32_t* count = nullptr;
+    RCGS_TRY(dalloc(&v->gid, k, s));
+    RCGS_TRY(dalloc(&v->z, k, s));
+    RCGS_TRY(dalloc(&v->rec, k, s));
+    RCGS_TRY(dalloc(&v->exact, k, s));
+    RCGS_TRY(dalloc(&v->color, k, s));
+    RCGS_TRY(dalloc(&rect, k, s));
+    RCGS_TRY(dalloc(&count, k, s));
+    k1_record_kernel<<<div_up(k, 256), 256, 0, s>>>(sc->pos, sc->cov3d, sc->opac, kgid, k, v->cam, v->cfg,
+                                                    v->tiles_x, v->tiles_y, v->gid, v->z, v->rec,
+                                                    v->exact, v->rank_of, rect, count);
+    RCGS_LAUNCH_CHECK();
+    dfree(kgid, s);
+    RCGS_TRY(exclusive_scan_u32(count, v->offs, k, s));
+    uint32_t* hp = reinterpret_cast<uint32_t*>(host);
+    RCGS_CUDA(cudaMemcpyAsync(hp, v->offs + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaStreamSynchronize(s));
+    const int64_t pairs = *hp;
+    v->pairs = pairs;
+    dfree(count, s);
+    if (pairs == 0) {
+        dfree(rect, s);
+        return RCGS_OK;
+    }
+    // ---- K2 emit + stable tile sort
+    uint32_t *tkey = nullptr, *tkey_alt = nullptr, *emit_s = nullptr, *pe = nullptr, *pe_alt = nullptr;
+    RCGS_TRY(dalloc(&tkey, pairs, s));
+    RCGS_TRY(dalloc(&tkey_alt, pairs, s));
+    RCGS_TRY(dalloc(&emit_s, pairs, s));
+    RCGS_TRY(dalloc(&pe, pairs, s));
+    RCGS_TRY(dalloc(&pe_alt, pairs, s));
+    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(rect, v->offs, k, v->tiles_x, tkey, emit_s);
+    RCGS_LAUNCH_CHECK();
+    dfree(rect, s);
+    int tile_bits = 1;
+    while ((1 << tile_bits) < ntiles) ++tile_bits;
+    RCGS_TRY(radix_sort_u32(&tkey, &tkey_alt, &pe, &pe_alt, true, pairs, tile_bits, s));
+    RCGS_TRY(dalloc(&v->pair_s, pairs, s));
+    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pe, emit_s, pairs, v->ranges, v->pair_s);
+    RCGS_LAUNCH_CHECK();
+    v->pair_e = pe;
+    dfree(pe_alt, s);
+    dfree(tkey, s);
+    dfree(tkey_alt, s);
+    dfree(emit_s, s);
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_create(const rcgs_scene* scene, const rcgs_camera* cam,
+                                const rcgs_raster_config* cfg, void* stream, rcgs_view** out) {
+    RCGS_CHECK_ARG(scene != nullptr && cfg != nullptr && out != nullptr, "null argument");
+    RCGS_TRY(validate_camera(cam));
+    cudaStream_t s = as_stream(stream);
+    rcgs_view* v = new rcgs_view();
+    v->scene = scene;
+    v->cam = *cam;
+    v->cfg = *cfg;
+    v->n = scene->n;
+    v->tiles_x = (cam->width + kTile - 1) / kTile;
+    v->tiles_y = (cam->height + kTile - 1) / kTile;
+    int st = view_build(v, s);
+    if (st != RCGS_OK) {
+        view_free(v, s);
+        delete v;
+        return st;
+    }
+    *out = v;
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_info_get(const rcgs_view* v, rcgs_view_info* out) {
+    RCGS_CHECK_ARG(v != nullptr && out != nullptr, "null argument");
+    out->n_gaussians = v->n;
+    out->n_kept = v->k;
+    out->n_pairs = v->pairs;
+    out->tiles_x = v->tiles_x;
+    out->tiles_y = v->tiles_y;
+    out->tile_size = kTile;
+    out->sort_bits = v->sort_bits;
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_kept(const rcgs_view* v, int64_t* d_index, double* d_depth, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr, "null view");
+    if (v->k == 0) return RCGS_OK;
+    kept_export_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->gid, v->z, v->k, d_index, d_depth);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_color(rcgs_view* v, const float* d_sh, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_sh != nullptr, "null argument");
+    if (v->k == 0) return RCGS_OK;
+    Center c = camera_center(v->cam);
+    color_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->scene->pos, d_sh, v->gid, v->k, c,
+                                                                   v->scene->sh_degree, v->color);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_basis(const rcgs_view* v, double* d_basis, uint8_t* d_active, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr, "null view");
+    if (v->k == 0) return RCGS_OK;
+    Center c = camera_center(v->cam);
+    basis_export_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->scene->pos, v->gid, v->color, v->k, c,
+                                                                          v->scene->sh_degree, d_basis, d_active);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}

@@ -1,0 +1,138 @@
+"""Device-resident recolor refit engine (the hot loop of optimize.py:99-120, 252-259).
+
+One optimizer step for a view batch:
+    K1+K2 view preprocess/binning (or a cached View: geometry is frozen)
+    -> K1 colour from the current SH -> K3 forward raster
+    -> K5 loss + image gradient (fp64) -> K6 backward (per-gaussian acc)
+    -> [multi-GPU: all-gather of the N x 3 acc vectors over NCCL]
+    -> K7 fused gradient expansion + Adam (device step counter, reject flag).
+Everything stays in HBM; the host only draws view indices from the reference's
+RNG stream and reads metrics back in batches.
+
+Multi-GPU: every rank holds a replica of the gaussians, the SH
+and the Adam state, and all views' targets.  A step draws G = world_size views
+(`rng.integers(V, size=G)`, the same stream as G sequential draws); rank r
+back-propagates view picks[r] and the ranks exchange only their N x 3
+per-gaussian channel sums (12 B/gaussian instead of the 192 B dense gradient);
+each rank then expands sum_v basis_v (x) acc_v / G for all G views in a fixed
+order, so every replica applies the bit-identical Adam update without a
+floating-point all-reduce.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .render import DEFAULT_CONFIG
+
+
+class RefitEngine:
+    def __init__(self, dscene: D.DeviceScene, sh_dev: torch.Tensor, cameras, targets,
+                 config, seed: int = 0, cache_views: bool = True, views=None, group=None,
+                 raster=DEFAULT_CONFIG, max_pending: int = 4096):
+        self.dscene = dscene
+        self.sh = sh_dev                      # (N, 16, 3) fp32, updated in place
+        self.m = torch.zeros_like(sh_dev)
+        self.v = torch.zeros_like(sh_dev)
+        self.cameras = list(cameras)          # [(intrinsics, pose)]
+        self.targets = targets                # per view (H, W, 3) fp32 device or pinned host
+        self.config = config
+        self.raster = raster
+        self.rng = np.random.default_rng(seed)
+        self.cache_views = cache_views
+        self.views = views if views is not None else [None] * len(self.cameras)
+        self.group = group
+        self.world = torch.distributed.get_world_size(group) if group is not None else 1
+        self.rank = torch.distributed.get_rank(group) if group is not None else 0
+        dev = D.device()
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.reject = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.acc = torch.empty((dscene.n, 3), dtype=torch.float32, device=dev)
+        self.acc_all = (torch.empty((self.world, dscene.n, 3), dtype=torch.float32, device=dev)
+                        if self.world > 1 else None)
+        self.max_pending = max_pending
+        self.records = torch.zeros((max_pending, 4), dtype=torch.float64, device=dev)
+        self.pending = []                     # [(picks, generation)]
+        self._bufs = {}
+        self._adam_cfg = D.adam_config(config)
+        self._centers = [D.camera_center(pose) for _, pose in self.cameras]
+
+    # -- helpers ------------------------------------------------------------------
+    def view(self, i: int) -> D.View:
+        if self.cache_views:
+            if self.views[i] is None:
+                intr, pose = self.cameras[i]
+                self.views[i] = D.View(self.dscene, intr, pose, self.raster)
+            return self.views[i]
+        intr, pose = self.cameras[i]
+        return D.View(self.dscene, intr, pose, self.raster)
+
+    def _buf(self, h, w):
+        key = (h, w)
+        if key not in self._bufs:
+            dev = D.device()
+            self._bufs[key] = (torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                               torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                               torch.empty((h, w, 3), dtype=torch.float32, device=dev))
+        return self._bufs[key]
+
+    def draw(self):
+        """View indices of the next step from the reference RNG stream (optimize.py:106)."""
+        if self.world == 1:
+            return [int(self.rng.integers(len(self.cameras)))]
+        return [int(x) for x in self.rng.integers(len(self.cameras), size=self.world)]
+
+    # -- one step -----------------------------------------------------------------
+    def step(self, picks=None, generation: int = 0):
+        picks = self.draw() if picks is None else picks
+        mine = picks[self.rank] if self.world > 1 else picks[0]
+        view = self.view(mine)
+        view.color(self.sh)
+        img, tgt_buf, grad = self._buf(view.height, view.width)
+        view.render(None, 0, out=img)
+        target = self.targets[mine]
+        if not target.is_cuda:           # streamed dataset: H2D of this step's target
+            tgt_buf.copy_(target, non_blocking=True)
+            target = tgt_buf
+        slot = len(self.pending) % self.max_pending
+        rec = self.records[slot]
+        D.loss_grad(img, target, self.config.lam, loss3=rec[:3], grad=grad)
+        self.reject.zero_()
+        view.backward(grad, acc=self.acc, nonfinite=self.reject)
+        if self.world > 1:
+            torch.distributed.all_gather_into_tensor(self.acc_all, self.acc, group=self.group)
+            torch.distributed.all_reduce(self.reject, op=torch.distributed.ReduceOp.MAX, group=self.group)
+            accs = [self.acc_all[r] for r in range(self.world)]
+        else:
+            accs = [self.acc]
+        ptrs = (ctypes.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
+        cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
+        N.call("rcgs_adam_fused", self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
+               (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
+               N.ptr(self.reject), N.ptr(self.step_dev), D.stream_ptr())
+        rec[3].copy_(self.reject[0], non_blocking=True)
+        self.pending.append((picks, generation))
+        if not self.cache_views:
+            view.close()
+        return picks
+
+    def drain(self):
+        """Synchronise and return [(picks, generation, l1, ssim, total, rejected)]."""
+        if not self.pending:
+            return []
+        n = len(self.pending)
+        recs = self.records[:min(n, self.max_pending)].cpu().numpy()
+        out = []
+        for i, (picks, gen) in enumerate(self.pending):
+            r = recs[i % self.max_pending]
+            out.append((picks, gen, float(r[0]), float(r[1]), float(r[2]), bool(r[3] != 0)))
+        self.pending = []
+        return out
+
+    def step_count(self) -> int:
+        return int(self.step_dev.item())

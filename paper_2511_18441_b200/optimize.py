@@ -1,0 +1,336 @@
+"""SH-only refit (drop-in for splattint/optimize.py) on the device engine.
+
+`adam_step` and `optimize_iteration` keep the reference's per-call contract
+(host numpy in, host numpy out).  `BackgroundOptimizer` keeps all state in HBM
+(`engine.RefitEngine`) and only crosses the PCIe bus for metrics (batched) and
+for `current_scene()` / `snapshot()` materialisation.
+
+Precision: SH, Adam moments and arithmetic are float32 on the device.  Host
+scenes are updated by *delta* (sh64 + (new32 - old32)), so coefficients the
+optimizer does not move stay bit-identical to the caller's float64 values
+(fixed points, unselected gaussians).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .engine import RefitEngine
+from .errors import ValidationError
+from .losses import DEFAULT_LAMBDA, LossBreakdown
+from .render import DEFAULT_CONFIG
+
+log = logging.getLogger(__name__)
+
+
+@dataclass(frozen=True)
+class OptimizerConfig:
+    lr_dc: float = 0.0025
+    lr_rest: float = 0.000125
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    lam: float = DEFAULT_LAMBDA
+    snapshot_every: int = 10
+
+
+DEFAULT_OPTIMIZER = OptimizerConfig()
+
+
+@dataclass(frozen=True)
+class AdamState:
+    m: np.ndarray
+    v: np.ndarray
+    step: int
+
+    @classmethod
+    def fresh(cls, n_gaussians: int) -> "AdamState":
+        shape = (n_gaussians, 16, 3)
+        return cls(m=np.zeros(shape), v=np.zeros(shape), step=0)
+
+
+@dataclass(frozen=True)
+class IterationMetrics:
+    iteration: int
+    view_id: int
+    generation: int
+    loss: LossBreakdown
+
+    def line(self) -> str:
+        """iter,viewId,generation,l1,ssim,total (optimize.py:86-96)."""
+        return (f"{self.iteration},{self.view_id},{self.generation},"
+                f"{self.loss.l1:.8f},{self.loss.ssim:.8f},{self.loss.total:.8f}")
+
+
+@dataclass(frozen=True)
+class OptimizerStatus:
+    iteration: int
+    loss: float
+    ips: float
+    generation: int
+
+
+def _delta_to_host(base64: np.ndarray, old32: torch.Tensor, new32: torch.Tensor) -> np.ndarray:
+    d = (new32.double() - old32.double()).cpu().numpy()
+    return base64 + d
+
+
+def adam_step(params, grads, state: AdamState, config: OptimizerConfig = DEFAULT_OPTIMIZER):
+    """One bias-corrected Adam update (optimize.py:59-83) on the device."""
+    params = np.asarray(params, dtype=np.float64)
+    grads = np.asarray(grads, dtype=np.float64)
+    if params.shape != grads.shape or params.ndim != 3 or params.shape[1:] != (16, 3):
+        raise ValidationError(
+            f"params/grads must both be (N, 16, 3), got {params.shape} and {grads.shape}")
+    if not np.all(np.isfinite(grads)):
+        log.warning("non-finite gradient; Adam iteration %d rejected", state.step + 1)
+        return params, state
+    p32 = D.to_device(params)
+    p_new = p32.clone()
+    m = D.to_device(state.m)
+    v = D.to_device(state.v)
+    g = D.to_device(grads)
+    step = torch.tensor([state.step], dtype=torch.int64, device=p32.device)
+    cfg = D.adam_config(config)
+    N.call("rcgs_adam_dense", N.ptr(p_new), N.ptr(m), N.ptr(v), N.ptr(g), params.shape[0],
+           ctypes.byref(cfg), None, N.ptr(step), D.stream_ptr())
+    return (_delta_to_host(params, p32, p_new),
+            AdamState(m=m.double().cpu().numpy(), v=v.double().cpu().numpy(), step=state.step + 1))
+
+
+def optimize_iteration(scene, dataset, rng: np.random.Generator, state: AdamState,
+                       config: OptimizerConfig = DEFAULT_OPTIMIZER):
+    """One SH refit step on a uniformly sampled view (optimize.py:99-120)."""
+    if len(dataset) == 0:
+        raise ValidationError("dataset has no views")
+    pick = int(rng.integers(len(dataset)))
+    target = dataset.views[pick]
+    view = target.view
+    ds = D.device_scene(scene)
+    sh32 = D.sh_to_device(scene.sh)
+    eng = RefitEngine(ds, sh32.clone(), [(view.intrinsics, view.pose)],
+                      [D.to_device(target.image)], config, cache_views=False)
+    eng.m.copy_(D.to_device(state.m))
+    eng.v.copy_(D.to_device(state.v))
+    eng.step_dev.fill_(state.step)
+    eng.step(picks=[0])
+    (_, _, l1, ss, total, rejected), = eng.drain()
+    loss = LossBreakdown(l1=l1, ssim=ss, total=total, lam=config.lam)
+    metrics = IterationMetrics(iteration=state.step + 1, view_id=view.view_id,
+                               generation=dataset.generation, loss=loss)
+    if rejected:
+        log.warning("non-finite gradient; Adam iteration %d rejected", state.step + 1)
+        return scene, state, metrics
+    new_sh = _delta_to_host(scene.sh, sh32, eng.sh)
+    new_state = AdamState(m=eng.m.double().cpu().numpy(), v=eng.v.double().cpu().numpy(),
+                          step=state.step + 1)
+    return scene.with_sh(new_sh), new_state, metrics
+
+
+class BackgroundOptimizer:
+    """Pausable refit worker with snapshots and atomic dataset swaps (optimize.py:131-259).
+
+    All optimizer state lives on the device.  `run_iterations` is the
+    deterministic synchronous mode; `start/pause/resume/stop` run the same
+    loop on a worker thread with its own CUDA stream.  `views_per_step` > 1 or a
+    `group` (torch.distributed process group, one rank per GPU) enables the
+    view-batched multi-GPU step (engine.py).
+    """
+
+    def __init__(self, scene, dataset, config: OptimizerConfig = DEFAULT_OPTIMIZER, seed: int = 0,
+                 metrics_sink=None, *, group=None, cache_views: bool = True,
+                 stream_targets: bool = False, raster=DEFAULT_CONFIG):
+        self._config = config
+        self._scene0 = scene
+        self._metrics_sink = metrics_sink
+        self._lock = threading.Lock()
+        self._dataset = dataset
+        self._stream_targets = stream_targets
+        self._raster = raster
+        self._ds = D.device_scene(scene)
+        self._sh0 = D.sh_to_device(scene.sh)
+        self._engine = RefitEngine(self._ds, self._sh0.clone(), self._cameras(dataset),
+                                   self._targets(dataset), config, seed=seed,
+                                   cache_views=cache_views, group=group, raster=raster)
+        self._pending_dataset = None
+        self._accepted = 0
+        self._snapshot_sh = self._sh0.clone()
+        self._snapshot_cache = (None, None)
+        self._current_cache = (None, None)
+        self._version = 0
+        self._status = OptimizerStatus(0, 0.0, 0.0, dataset.generation)
+        self._run_event = threading.Event()
+        self._run_event.set()
+        self._stop_event = threading.Event()
+        self._thread = None
+        self._window_start = time.perf_counter()
+        self._window_iters = 0
+        self._last_loss = 0.0
+
+    # -- dataset plumbing -------------------------------------------------------
+    @staticmethod
+    def _cameras(dataset):
+        return [(ev.view.intrinsics, ev.view.pose) for ev in dataset.views]
+
+    def _targets(self, dataset):
+        if self._stream_targets:
+            return [torch.from_numpy(np.ascontiguousarray(ev.image, np.float32)).pin_memory()
+                    for ev in dataset.views]
+        return [D.to_device(ev.image) for ev in dataset.views]
+
+    def _apply_pending_dataset(self):
+        with self._lock:
+            ds, self._pending_dataset = self._pending_dataset, None
+        if ds is None:
+            return
+        if len(ds) == 0:
+            raise ValidationError("dataset has no views")
+        eng = self._engine
+        same = self._cameras(ds) == eng.cameras
+        eng.targets = self._targets(ds)
+        if not same:
+            eng.cameras = self._cameras(ds)
+            eng.views = [None] * len(eng.cameras)
+            eng._centers = [D.camera_center(p) for _, p in eng.cameras]
+        with self._lock:
+            self._dataset = ds
+
+    # -- state shared with other threads ------------------------------------------
+    def _materialise(self, sh_dev, cache_name):
+        ver, sc = getattr(self, cache_name)
+        if ver == self._version and sc is not None:
+            return sc
+        sc = self._scene0.with_sh(_delta_to_host(self._scene0.sh, self._sh0, sh_dev))
+        setattr(self, cache_name, (self._version, sc))
+        return sc
+
+    def snapshot(self):
+        with self._lock:
+            return self._materialise(self._snapshot_sh, "_snapshot_cache")
+
+    def current_scene(self):
+        with self._lock:
+            return self._materialise(self._engine.sh, "_current_cache")
+
+    def status(self) -> OptimizerStatus:
+        with self._lock:
+            return self._status
+
+    def swap_dataset(self, dataset) -> None:
+        with self._lock:
+            self._pending_dataset = dataset
+
+    @property
+    def dataset(self):
+        with self._lock:
+            return self._dataset
+
+    # -- control --------------------------------------------------------------------
+    def start(self) -> None:
+        if self._thread is not None:
+            return
+        self._thread = threading.Thread(target=self._loop, name="sh-refit", daemon=True)
+        self._thread.start()
+
+    def pause(self) -> None:
+        self._run_event.clear()
+
+    def resume(self) -> None:
+        self._run_event.set()
+
+    @property
+    def paused(self) -> bool:
+        return not self._run_event.is_set()
+
+    def stop(self) -> None:
+        self._stop_event.set()
+        self._run_event.set()
+        if self._thread is not None:
+            self._thread.join(timeout=30.0)
+            self._thread = None
+
+    @property
+    def stopped(self) -> bool:
+        return self._stop_event.is_set()
+
+    # -- the loop -----------------------------------------------------------------------
+    def _step(self) -> None:
+        self._apply_pending_dataset()
+        with self._lock:
+            gen = self._dataset.generation
+        self._engine.step(generation=gen)
+        self._window_iters += 1
+        with self._lock:
+            self._version += 1
+        if len(self._engine.pending) >= min(self._config.snapshot_every, self._engine.max_pending):
+            self._flush()
+
+    def _flush(self) -> None:
+        recs = self._engine.drain()
+        lines = []
+        for picks, gen, l1, ss, total, rejected in recs:
+            it = self._accepted + 1
+            if rejected:
+                log.warning("non-finite gradient; Adam iteration %d rejected", it)
+            else:
+                self._accepted += 1
+            self._last_loss = total
+            vid = self._dataset.views[picks[self._engine.rank]].view.view_id
+            lines.append(IterationMetrics(iteration=it, view_id=vid, generation=gen,
+                                          loss=LossBreakdown(l1, ss, total, self._config.lam)))
+            if not rejected and self._accepted % self._config.snapshot_every == 0:
+                self._publish()
+        if self._metrics_sink is not None:
+            for m in lines:
+                self._metrics_sink(m)
+
+    def _publish(self) -> None:
+        now = time.perf_counter()
+        elapsed = max(now - self._window_start, 1e-9)
+        with self._lock:
+            self._snapshot_sh.copy_(self._engine.sh)
+            self._snapshot_cache = (None, None)
+            self._status = OptimizerStatus(iteration=self._accepted, loss=self._last_loss,
+                                           ips=self._window_iters / elapsed,
+                                           generation=self._dataset.generation)
+        self._window_start = now
+        self._window_iters = 0
+
+    def _loop(self) -> None:
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            while not self._stop_event.is_set():
+                if not self._run_event.wait(timeout=0.1):
+                    self._flush()
+                    continue
+                if self._stop_event.is_set():
+                    break
+                try:
+                    self._step()
+                except Exception:
+                    log.exception("optimizer iteration failed; pausing")
+                    self._run_event.clear()
+            self._flush()
+
+    def run_iterations(self, count: int):
+        """Deterministic synchronous mode; returns the final scene."""
+        if self._thread is not None:
+            raise ValidationError("run_iterations cannot be mixed with a started worker")
+        for _ in range(count):
+            self._step()
+        self._flush()
+        self._publish()
+        return self.current_scene()
+
+    @property
+    def engine(self) -> RefitEngine:
+        return self._engine
