@@ -2,10 +2,9 @@
 //
 // The per-view backward (raster.cu) leaves one fp32 3-vector per gaussian,
 // acc[i, ch] = active * sum_p g[p, ch] w_ip.  The dense (N, 16, 3) gradient is
-// basis_k(dir_i) * acc[i, ch]; it is never materialised: each CTA takes 32
-// gaussians, one warp computes their fp64 view directions and SH bases (for
-// every view of the step) into shared memory, then 384 threads run Adam on the
-// 32 x 12 float4 chunks of SH / m / v with fully coalesced 16-byte accesses.
+// basis_k(dir_i) * acc[i, ch]; it is never materialised: one thread per float4
+// of the 48 coefficients runs Adam with fully coalesced 16-byte SH / m / v
+// accesses and rebuilds the (at most two) SH basis rows it needs in fp32.
 // A device-side reject flag (non-finite gradient, optimize.py:72-74) skips the
 // update, and the device step counter feeds the bias corrections, so a
 // sequence of steps needs no host synchronisation.
@@ -17,8 +16,6 @@
 namespace rcgs {
 
 constexpr int kMaxViews = 16;
-constexpr int kGPB = 32;           // gaussians per block
-constexpr int kAdamNT = kGPB * 12; // one thread per float4 of 48 coefficients
 
 struct AccViews {
     const float* acc[kMaxViews];
@@ -53,49 +50,47 @@ __device__ __forceinline__ void bias_corr(const int64_t* step, float b1, float b
     inv2 = (float)(1.0 / (1.0 - pow(db2, t)));
 }
 
-__global__ void __launch_bounds__(kAdamNT) adam_fused_kernel(
+// One thread per float4 of a gaussian's 48 coefficients (12 per gaussian, fully
+// coalesced SH / m / v traffic).  Each thread rebuilds the few SH basis rows it
+// needs in fp32 from the fp64 view direction (cheap next to the 96 bytes it
+// moves), so there is no shared-memory staging and no block barrier.
+__global__ void __launch_bounds__(256) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float4* __restrict__ sh, float4* __restrict__ m,
     float4* __restrict__ v, AccViews views, AdamHyper h, double db1, double db2,
     const int32_t* __restrict__ reject, const int64_t* __restrict__ step) {
-    __shared__ float basis[kMaxViews][kGPB][16];
-    __shared__ float acc[kMaxViews][kGPB][3];
     if (reject && *reject) return;
-    const int t = threadIdx.x;
-    const int64_t g0 = (int64_t)blockIdx.x * kGPB;
-    if (t < kGPB) {
-        const int64_t g = g0 + t;
-        if (g < n) {
-            for (int vi = 0; vi < views.n; ++vi) {
-                double x, y, z;
-                view_dir(pos, g, views.cen[vi], x, y, z);
-                double b[16];
-                sh_basis16<double>(x, y, z, deg, b);
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n * 12) return;
+    const int64_t g = q / 12;
+    const int f0 = 4 * (int)(q - g * 12);
+    const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
+    float gr[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int vi = 0; vi < views.n; ++vi) {
+        float x = (float)(px - views.cen[vi][0]), y = (float)(py - views.cen[vi][1]),
+              z = (float)(pz - views.cen[vi][2]);
+        const float inv = rsqrtf(x * x + y * y + z * z);
+        x *= inv;
+        y *= inv;
+        z *= inv;
+        const int k0 = f0 / 3;  // the 4 coefficients span rows k0 and k0 + 1 at most
+        const float b0 = sh_row(k0, x, y, z, deg), b1 = sh_row(k0 + 1, x, y, z, deg);
+        const float* a = views.acc[vi] + 3 * g;
+        const float a0 = a[0], a1 = a[1], a2 = a[2];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) basis[vi][t][k] = (float)b[k];
-                const float* a = views.acc[vi] + 3 * g;
-                acc[vi][t][0] = a[0];
-                acc[vi][t][1] = a[1];
-                acc[vi][t][2] = a[2];
-            }
+        for (int j = 0; j < 4; ++j) {
+            const int f = f0 + j, ch = f - 3 * (f / 3);
+            const float bb = (f / 3 == k0) ? b0 : b1;
+            const float av = ch == 0 ? a0 : (ch == 1 ? a1 : a2);
+            gr[j] = fmaf(bb, av, gr[j]);
         }
     }
-    __syncthreads();
-    const int lg = t / 12, c4 = t % 12;
-    const int64_t g = g0 + lg;
-    if (g >= n) return;
-    const int f0 = 4 * c4;
-    float gr[4];
-    const float invn = 1.0f / (float)views.n;
+    if (views.n > 1) {
+        const float invn = 1.0f / (float)views.n;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int k = (f0 + j) / 3, ch = (f0 + j) % 3;
-        float s = 0.f;
-        for (int vi = 0; vi < views.n; ++vi) s = fmaf(basis[vi][lg][k], acc[vi][lg][ch], s);
-        gr[j] = views.n == 1 ? s : s * invn;
+        for (int j = 0; j < 4; ++j) gr[j] *= invn;
     }
     float inv1, inv2;
     bias_corr(step, h.b1, h.b2, db1, db2, inv1, inv2);
-    const int64_t q = g * 12 + c4;
     float4 p = sh[q], mm = m[q], vv = v[q];
     adam4(p, mm, vv, gr, f0, h, inv1, inv2);
     sh[q] = p;
@@ -179,7 +174,7 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
             av.acc[i] = h_d_accs[i];
             for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
         }
-        adam_fused_kernel<<<div_up(sc->n, kGPB), kAdamNT, 0, s>>>(
+        adam_fused_kernel<<<div_up(sc->n * 12, 256), 256, 0, s>>>(
             sc->pos, sc->n, sc->sh_degree, reinterpret_cast<float4*>(d_sh), reinterpret_cast<float4*>(d_m),
             reinterpret_cast<float4*>(d_v), av, hyper(cfg), cfg->beta1, cfg->beta2, d_reject, d_step);
         RCGS_LAUNCH_CHECK();

@@ -46,9 +46,15 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline unsigned div_up(int64_t a, int64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// Keep freed blocks in the device's default pool across stream syncs (the
+// default release threshold of 0 returns memory to the driver at every sync,
+// which turns each per-view allocation into a map/unmap).
+void retain_pool_memory();
+
 // Stream-ordered device allocation from the default memory pool.
 template <typename T>
 int dalloc(T** p, size_t count, cudaStream_t s) {
+    retain_pool_memory();
     *p = nullptr;
     if (count == 0) count = 1;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s);
@@ -103,7 +109,9 @@ struct rcgs_scene {
 struct __align__(16) RasterRec {
     float4 mean;   // mx_hi, my_hi, mx_lo, my_lo   (mean2d = hi + lo)
     float4 conic;  // -a/2, -b, -c/2, opacity      (power = nha dx^2 + nb dx dy + nhc dy^2)
-    float4 gate;   // p_lo, p_hi, delta, unused    (skip if power < p_lo; exact check below p_hi)
+    float4 gate;   // p_lo, p_hi, kappa, half2(ex, ey)  (skip if power < p_lo; exact check
+                   // below p_hi; kappa = power error coefficient; ex/ey = footprint half
+                   // extents rounded up to fp16, for sub-tile culling)
 };
 
 // Exact (fp64) record for guarded decisions: the reference's own operands.

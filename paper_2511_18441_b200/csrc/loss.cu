@@ -134,21 +134,24 @@ __global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
                 m22 += w * hs[3 * plane + base];
                 m12 += w * hs[4 * plane + base];
             }
-            const double mass = mass1d(win, gy, H) * mass1d(win, gx, W);
-            const double mu1 = m1 / mass, mu2 = m2 / mass;
-            const double var1 = m11 / mass - mu1 * mu1;
-            const double var2 = m22 / mass - mu2 * mu2;
-            const double cov = m12 / mass - mu1 * mu2;
+            // three fp64 reciprocals replace the reference's divisions (same formulas)
+            const double im = 1.0 / (mass1d(win, gy, H) * mass1d(win, gx, W));
+            const double mu1 = m1 * im, mu2 = m2 * im;
+            const double var1 = m11 * im - mu1 * mu1;
+            const double var2 = m22 * im - mu2 * mu2;
+            const double cov = m12 * im - mu1 * mu2;
             const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
             const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
-            ss += (a1 * a2) / (b1 * b2);
-            const double d_mu1 = 2.0 * (mu2 * a2) / (b1 * b2) - 2.0 * mu1 * a1 * a2 / (b1 * b1 * b2);
-            const double d_var1 = -(a1 * a2) / (b1 * b2 * b2);
-            const double d_cov = 2.0 * a1 / (b1 * b2);
+            const double ib1 = 1.0 / b1, ib2 = 1.0 / b2, ib = ib1 * ib2;
+            const double a12 = a1 * a2;
+            ss += a12 * ib;
+            const double d_mu1 = 2.0 * (mu2 * a2) * ib - 2.0 * mu1 * a12 * ib * ib1;
+            const double d_var1 = -a12 * ib * ib2;
+            const double d_cov = 2.0 * a1 * ib;
             const int64_t o = pix * 3 + ch;
-            maps[o] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) / mass;
-            maps[npix * 3 + o] = d_var1 / mass;
-            maps[2 * npix * 3 + o] = d_cov / mass;
+            maps[o] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im;
+            maps[npix * 3 + o] = d_var1 * im;
+            maps[2 * npix * 3 + o] = d_cov * im;
         }
     }
     if (__syncthreads_or(diff) && t == 0) atomicOr(differ, 1);

@@ -18,6 +18,7 @@
 //   k2_emit      one (tile, e) pair per overlapped tile
 //   radix sort   stable sort on tile id -> (tile, depth) order
 //   k2_ranges    per-tile [start, end) + rank/e lookup per pair
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -202,20 +203,25 @@ __global__ void k1_record_kernel(const double* __restrict__ pos, const double* _
     const double P = log(cfg.alpha_skip / op);
     const double rho = fmin(fabs(cb) / sqrt(ca * cc), 0.999999);
     const double margin = fabs(P) * 4.4e-6 / (1.0 - rho) + 1e-6;
-    r.gate = make_float4((float)(P - margin), (float)(P + margin), (float)(margin + 1e-6), 0.f);
-    rec[s] = r;
-
     // opacity-aware footprint: alpha >= skip inside d^T conic d <= r2 = 2 ln(op/skip);
     // axis half widths r * sqrt(cov2d diag), padded for fp64 rounding.
+    const double r2 = -2.0 * P;
+    const double ex_ = r2 >= 0.0 ? sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4 : 0.0;
+    const double ey_ = r2 >= 0.0 ? sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4 : 0.0;
+    // half extents (rounded up to fp16) ride in gate.w for the raster's sub-tile culling
+    const __half hx = __float2half_ru((float)fmin(ex_ + 0.01, 60000.0));
+    const __half hy = __float2half_ru((float)fmin(ey_ + 0.01, 60000.0));
+    const unsigned packed = (unsigned)__half_as_ushort(hx) | ((unsigned)__half_as_ushort(hy) << 16);
+    r.gate = make_float4((float)(P - margin), (float)(P + margin), (float)(margin + 1e-6),
+                         __uint_as_float(packed));
+    rec[s] = r;
+
     Rect rc;
     rc.x0 = 0;
     rc.y0 = 0;
     rc.x1 = -1;
     rc.y1 = -1;
-    const double r2 = -2.0 * P;
     if (r2 >= 0.0) {
-        const double ex_ = sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4;
-        const double ey_ = sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4;
         const double umin = fmax(ceil(p.mx - ex_), 0.0), umax = fmin(floor(p.mx + ex_), cam.width - 1.0);
         const double vmin = fmax(ceil(p.my - ey_), 0.0), vmax = fmin(floor(p.my + ey_), cam.height - 1.0);
         if (umin <= umax && vmin <= vmax) {
@@ -258,20 +264,33 @@ __global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key,
 }
 
 // ---------------------------------------------------------------- colour (per step)
-__global__ void color_kernel(const double* __restrict__ pos, const float* __restrict__ sh,
-                             const uint32_t* __restrict__ gid, int64_t k, Center cen, int deg,
+// Per-step colour (render.py:209-214), iterated in scene order so the 192-byte SH
+// rows are read fully coalesced; the 16-byte result goes to the gaussian's
+// depth-rank slot.
+__global__ void color_kernel(const double* __restrict__ pos, const float4* __restrict__ sh,
+                             const int32_t* __restrict__ rank_of, int64_t n, Center cen, int deg,
                              float4* __restrict__ color) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= k) return;
-    const uint32_t g = gid[s];
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int32_t s = rank_of[g];
+    if (s < 0) return;
     double x, y, z;
     view_dir(pos, g, cen.c, x, y, z);
     double b[16];
     sh_basis16<double>(x, y, z, deg, b);
-    const float* c = sh + (int64_t)g * 48;
-    const int rows = (deg + 1) * (deg + 1);
+    float c[48];
+    const float4* row = sh + g * 12;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+        const float4 f = row[i];
+        c[4 * i] = f.x;
+        c[4 * i + 1] = f.y;
+        c[4 * i + 2] = f.z;
+        c[4 * i + 3] = f.w;
+    }
     double raw[3] = {0.0, 0.0, 0.0};
-    for (int i = 0; i < rows; ++i) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
         raw[0] += b[i] * (double)c[3 * i];
         raw[1] += b[i] * (double)c[3 * i + 1];
         raw[2] += b[i] * (double)c[3 * i + 2];
@@ -548,11 +567,12 @@ extern "C" int rcgs_view_kept(const rcgs_view* v, int64_t* d_index, double* d_de
 }
 
 extern "C" int rcgs_view_color(rcgs_view* v, const float* d_sh, void* stream) {
-    RCGS_CHECK_ARG(v != nullptr && d_sh != nullptr, "null argument");
+    RCGS_CHECK_ARG(v != nullptr, "null view");
     if (v->k == 0) return RCGS_OK;
+    RCGS_CHECK_ARG(d_sh != nullptr, "null SH");
     Center c = camera_center(v->cam);
-    color_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->scene->pos, d_sh, v->gid, v->k, c,
-                                                                   v->scene->sh_degree, v->color);
+    color_kernel<<<div_up(v->n, 256), 256, 0, as_stream(stream)>>>(
+        v->scene->pos, reinterpret_cast<const float4*>(d_sh), v->rank_of, v->n, c, v->scene->sh_degree, v->color);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }

@@ -24,6 +24,8 @@
 // of g * w for the SH backward, deterministic: warp shuffle tree -> fixed-order
 // sum over warps -> one write per (tile, entry)), HITS (mask statistics),
 // CAPTURE (contribution lists).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace rcgs {
@@ -158,18 +160,40 @@ __device__ __forceinline__ int step(const RasterRec& r, uint32_t s, uint32_t j, 
     return COMPOSITE;
 }
 
+// Footprint box of a staged record vs the tile's eight 8x4 warp blocks (tile-local
+// coordinates): bit w set iff the box may touch warp w's pixels.  The half extents
+// are the fp64 footprint widths rounded up to fp16, so the test is conservative.
+__device__ __forceinline__ uint32_t warp_block_mask(const RasterRec& r, float x0, float y0) {
+    const unsigned packed = __float_as_uint(r.gate.w);
+    const float ex = __half2float(__ushort_as_half((unsigned short)(packed & 0xffffu)));
+    const float ey = __half2float(__ushort_as_half((unsigned short)(packed >> 16)));
+    const float mx = r.mean.x - x0, my = r.mean.y - y0;
+    const float lx = mx - ex - 0.01f, hx = mx + ex + 0.01f;
+    const float ly = my - ey - 0.01f, hy = my + ey + 0.01f;
+    const uint32_t xm = ((lx <= 7.f && hx >= 0.f) ? 1u : 0u) | ((lx <= 15.f && hx >= 8.f) ? 2u : 0u);
+    uint32_t m = 0;
+#pragma unroll
+    for (int by = 0; by < 4; ++by)
+        if (ly <= 4.f * by + 3.f && hy >= 4.f * by) m |= xm << (2 * by);
+    return m;
+}
+
 template <int M>
-__global__ void __launch_bounds__(kNT) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kNT, 3) raster_kernel(RasterArgs a) {
     __shared__ RasterRec srec[kNT];
-    __shared__ float4 scol[kNT];
+    __shared__ float4 scol[(M == FWD) ? kNT : 1];
     __shared__ uint32_t ss[kNT];
+    __shared__ uint8_t smask[kNT];
     __shared__ uint32_t se[(M == BWD) ? kNT : 1];
     __shared__ float red[(M == BWD) ? kWarps * kNT * 3 : 1];
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tile = blockIdx.x;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int u = tx * kTile + (t % kTile), v = ty * kTile + (t / kTile);
+    // warp w owns the 8x4 block (w & 1, w >> 1) of the 16x16 tile
+    const int u = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int v = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const float tile_x0 = (float)(tx * kTile), tile_y0 = (float)(ty * kTile);
     const bool inside = u < a.W && v < a.H;
     const int64_t pix = (int64_t)v * a.W + u;
 
@@ -198,8 +222,10 @@ __global__ void __launch_bounds__(kNT) raster_kernel(RasterArgs a) {
         const uint32_t cnt = min((uint32_t)kNT, range.y - start);
         if (t < cnt) {
             const uint32_t s = a.pair_s[start + t];
+            const RasterRec r = a.rec[s];
             ss[t] = s;
-            srec[t] = a.rec[s];
+            srec[t] = r;
+            smask[t] = (uint8_t)warp_block_mask(r, tile_x0, tile_y0);
             if (M == FWD) scol[t] = a.color[s];
             if (M == BWD) se[t] = a.pair_e[start + t];
         }
@@ -208,62 +234,58 @@ __global__ void __launch_bounds__(kNT) raster_kernel(RasterArgs a) {
         }
         __syncthreads();
 
-        if (M == FWD || M == DEPTH || M == CAP_COUNT || M == CAP_WRITE) {
-            // divergent per-thread loop
-            for (uint32_t k = 0; k < cnt && !done; ++k) {
-                float w;
-                const int r = step<M>(srec[k], ss[k], start + k, range.x, px, a, &w);
-                if (r == SKIP) continue;
-                if (r == STOP) {
-                    done = true;
-                    break;
-                }
-                if (r == CROSS) {
-                    cross = (int32_t)ss[k];
-                    done = true;
-                    break;
-                }
-                if (M == FWD) {
-                    const float4 c = scol[k];
-                    acc0 = fmaf(c.x, w, acc0);
-                    acc1 = fmaf(c.y, w, acc1);
-                    acc2 = fmaf(c.z, w, acc2);
-                } else if (M == CAP_COUNT) {
-                    ++ncap;
-                } else if (M == CAP_WRITE) {
-                    const uint32_t o = cap_base + ncap++;
-                    a.cap_pixel[o] = pix;
-                    a.cap_kept[o] = ss[k];
-                    a.cap_weight[o] = (double)w;
-                }
-            }
-        } else {
-            // warp-converged loop (warp reductions per entry)
-            for (uint32_t k = 0; k < cnt; ++k) {
+        // Walk this warp's entries 32 at a time: a ballot over the staged block
+        // masks yields the (warp-uniform) list of entries that can reach the block.
+        for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+            const uint32_t kl = c0 + lane;
+            unsigned bits = __ballot_sync(0xffffffffu, kl < cnt && ((smask[kl] >> warp) & 1u));
+            while (bits) {
+                const uint32_t k = c0 + (uint32_t)(__ffs(bits) - 1);
+                bits &= bits - 1;
                 float w = 0.f;
-                bool comp = false;
+                int r = SKIP;
                 if (!done) {
-                    const int r = step<M>(srec[k], ss[k], start + k, range.x, px, a, &w);
+                    r = step<M>(srec[k], ss[k], start + k, range.x, px, a, &w);
                     if (r == STOP) done = true;
-                    comp = (r == COMPOSITE);
+                    if (r == CROSS) {
+                        cross = (int32_t)ss[k];
+                        done = true;
+                    }
                 }
-                if (M == BWD) {
-                    float c0 = comp ? w * g0 : 0.f, c1 = comp ? w * g1 : 0.f, c2 = comp ? w * g2 : 0.f;
-                    if (__any_sync(0xffffffffu, c0 != 0.f || c1 != 0.f || c2 != 0.f)) {
+                const bool comp = (r == COMPOSITE);
+                if (M == FWD) {
+                    if (comp) {
+                        const float4 c = scol[k];
+                        acc0 = fmaf(c.x, w, acc0);
+                        acc1 = fmaf(c.y, w, acc1);
+                        acc2 = fmaf(c.z, w, acc2);
+                    }
+                } else if (M == CAP_COUNT) {
+                    ncap += comp;
+                } else if (M == CAP_WRITE) {
+                    if (comp) {
+                        const uint32_t o = cap_base + ncap++;
+                        a.cap_pixel[o] = pix;
+                        a.cap_kept[o] = ss[k];
+                        a.cap_weight[o] = (double)w;
+                    }
+                } else if (M == BWD) {
+                    float c0v = comp ? w * g0 : 0.f, c1v = comp ? w * g1 : 0.f, c2v = comp ? w * g2 : 0.f;
+                    if (__any_sync(0xffffffffu, c0v != 0.f || c1v != 0.f || c2v != 0.f)) {
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
-                            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-                            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-                            c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                            c0v += __shfl_xor_sync(0xffffffffu, c0v, o);
+                            c1v += __shfl_xor_sync(0xffffffffu, c1v, o);
+                            c2v += __shfl_xor_sync(0xffffffffu, c2v, o);
                         }
                         if (lane == 0) {
                             float* rp = red + (warp * kNT + k) * 3;
-                            rp[0] = c0;
-                            rp[1] = c1;
-                            rp[2] = c2;
+                            rp[0] = c0v;
+                            rp[1] = c1v;
+                            rp[2] = c2v;
                         }
                     }
-                } else {  // HITS
+                } else if (M == HITS) {
                     const unsigned bal = __ballot_sync(0xffffffffu, comp);
                     if (bal) {
                         float ws = comp ? w : 0.f;
@@ -276,8 +298,9 @@ __global__ void __launch_bounds__(kNT) raster_kernel(RasterArgs a) {
                         }
                     }
                 }
-                if (__all_sync(0xffffffffu, done)) break;
+                if (__all_sync(0xffffffffu, done)) bits = 0;
             }
+            if (__all_sync(0xffffffffu, done)) break;
         }
         if (M == BWD) {
             __syncthreads();

@@ -31,6 +31,29 @@ __device__ __forceinline__ void sh_basis16(T x, T y, T z, int deg, T* b) {
     b[15] = T(-0.5900435899266435) * x * (xx - T(3) * yy);
 }
 
+// One SH basis row (0 beyond the degree, or k > 15) without a local array.
+__device__ __forceinline__ float sh_row(int k, float x, float y, float z, int deg) {
+    if (k > 15 || (k >= 1 && deg < 1) || (k >= 4 && deg < 2) || (k >= 9 && deg < 3)) return 0.f;
+    switch (k) {
+        case 0: return 0.28209479177387814f;
+        case 1: return -0.4886025119029199f * y;
+        case 2: return 0.4886025119029199f * z;
+        case 3: return -0.4886025119029199f * x;
+        case 4: return 1.0925484305920792f * (x * y);
+        case 5: return -1.0925484305920792f * (y * z);
+        case 6: return 0.31539156525252005f * (2.f * z * z - x * x - y * y);
+        case 7: return -1.0925484305920792f * (x * z);
+        case 8: return 0.5462742152960396f * (x * x - y * y);
+        case 9: return -0.5900435899266435f * y * (3.f * x * x - y * y);
+        case 10: return 2.890611442640554f * (x * y) * z;
+        case 11: return -0.4570457994644658f * y * (4.f * z * z - x * x - y * y);
+        case 12: return 0.3731763325901154f * z * (2.f * z * z - 3.f * x * x - 3.f * y * y);
+        case 13: return -0.4570457994644658f * x * (4.f * z * z - x * x - y * y);
+        case 14: return 1.445305721320277f * z * (x * x - y * y);
+        default: return -0.5900435899266435f * x * (x * x - 3.f * y * y);
+    }
+}
+
 struct Center {
     double c[3];
 };

@@ -32,6 +32,18 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_err; }
 
+void retain_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 void* pinned_scratch(size_t bytes) {
     static thread_local void* buf = nullptr;
     static thread_local size_t cap = 0;

@@ -127,15 +127,23 @@ def make_view(scene, intrinsics, pose, config=DEFAULT_CONFIG, sh=None) -> D.View
     return view
 
 
+def _host_image(view: D.View, bg: np.ndarray) -> np.ndarray:
+    """HWC float64: the composite plus T_final * background added in float64, so a
+    pixel no gaussian reaches equals the background bit-for-bit (render.py:317-322)."""
+    if not np.any(bg):
+        return view.render(None, 0).double().cpu().numpy()
+    img, tf = view.render(None, 0, t_final=True)
+    return img.double().cpu().numpy() + tf.double().cpu().numpy()[..., None] * bg
+
+
 def render(scene, intrinsics, pose, background=None, config: RasterizerConfig = DEFAULT_CONFIG,
            layout: str = "hwc") -> np.ndarray:
     """(H, W, 3) float64, or (3, H, W) for layout="chw" (render.py:304-334)."""
     if layout not in ("hwc", "chw"):
         raise ValidationError(f"unknown layout {layout!r}")
     bg = _background(background)
-    view = make_view(scene, intrinsics, pose, config)
-    img = view.render(bg, 0 if layout == "hwc" else 1)
-    return img.double().cpu().numpy()
+    img = _host_image(make_view(scene, intrinsics, pose, config), bg)
+    return img if layout == "hwc" else to_chw(img)
 
 
 def render_forward(scene, intrinsics, pose, background=None,
@@ -143,8 +151,7 @@ def render_forward(scene, intrinsics, pose, background=None,
     """Render + device-resident contribution state (render.py:337-370)."""
     bg = _background(background)
     view = make_view(scene, intrinsics, pose, config)
-    img = view.render(bg, 0).double().cpu().numpy()
-    return ForwardCapture(view, img, len(scene))
+    return ForwardCapture(view, _host_image(view, bg), len(scene))
 
 
 def depth_from_gaussians(scene, intrinsics, pose, tau: float = DEFAULT_DEPTH_TAU,

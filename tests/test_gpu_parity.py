@@ -165,8 +165,9 @@ def test_loss_and_grad_match_oracle(two_blobs):
     for tgt in (target, _f32(two_blobs["target2"])):
         g = P.loss_grad_wrt_image(image, tgt)
         ref = OL.loss_grad(image, tgt)
+        # relative to the gradient scale; where y == gt the reference itself only
+        # leaves round-off residue (~1e-20) whose sign is arbitrary
         assert np.abs(g - ref).max() <= 1e-6 * np.abs(ref).max()
-        assert np.array_equal(np.sign(g[ref != 0]), np.sign(ref[ref != 0])) or np.abs(g - ref).max() < 1e-12
     np.testing.assert_array_equal(P.loss_grad_wrt_image(image, image), 0.0)
     small_y, small_g = np.zeros((4, 4, 3)), np.ones((4, 4, 3))
     np.testing.assert_array_equal(P.loss_grad_wrt_image(small_y, small_g, lam=0.0), -np.ones((4, 4, 3)) / 48)
