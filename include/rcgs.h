@@ -124,6 +124,11 @@ int rcgs_capture(const rcgs_view* view, int64_t* h_count, int64_t* d_pixel, int6
 int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height, int32_t width,
                    double lam, double* d_loss3, float* d_grad, void* stream);
 
+/* Float64 images and gradient (the host-facing losses API: bit-faithful sign and
+ * array_equal semantics on float64 inputs). */
+int rcgs_loss_grad_f64(const double* d_image, const double* d_target, int32_t height,
+                       int32_t width, double lam, double* d_loss3, double* d_grad, void* stream);
+
 /* ---- SH backward (backward.py:22-40) ------------------------------------------------ */
 /* Per-gaussian channel sums acc[i,ch] = active[i,ch] * sum_p g[p,ch] * w_ip over the
  * view's composited contributions, written densely as d_acc (N,3) fp32 (zero for

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "rcgs_depth": [c_void_p, c_double, c_void_p, c_void_p, c_void_p],
     "rcgs_capture": [c_void_p, P(c_i64), c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_loss_grad": [c_void_p, c_void_p, c_i32, c_i32, c_double, c_void_p, c_void_p, c_void_p],
+    "rcgs_loss_grad_f64": [c_void_p, c_void_p, c_i32, c_i32, c_double, c_void_p, c_void_p, c_void_p],
     "rcgs_backward": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_sh_grad": [c_void_p, c_void_p, P(c_double), c_void_p, c_void_p],
     "rcgs_adam_fused": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,

@@ -43,11 +43,11 @@ __device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const flo
     }
 }
 
-__device__ __forceinline__ void bias_corr(const int64_t* step, float b1, float b2, double db1, double db2,
-                                          float& inv1, float& inv2) {
+// Bias corrections 1/(1 - beta^t) for t = step + 1, once per launch (fp64 pow).
+__global__ void adam_prep_kernel(const int64_t* __restrict__ step, double db1, double db2,
+                                 float2* __restrict__ inv) {
     const double t = (double)(*step + 1);
-    inv1 = (float)(1.0 / (1.0 - pow(db1, t)));
-    inv2 = (float)(1.0 / (1.0 - pow(db2, t)));
+    *inv = make_float2((float)(1.0 / (1.0 - pow(db1, t))), (float)(1.0 / (1.0 - pow(db2, t))));
 }
 
 // One thread per float4 of a gaussian's 48 coefficients (12 per gaussian, fully
@@ -56,8 +56,8 @@ __device__ __forceinline__ void bias_corr(const int64_t* step, float b1, float b
 // moves), so there is no shared-memory staging and no block barrier.
 __global__ void __launch_bounds__(256) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float4* __restrict__ sh, float4* __restrict__ m,
-    float4* __restrict__ v, AccViews views, AdamHyper h, double db1, double db2,
-    const int32_t* __restrict__ reject, const int64_t* __restrict__ step) {
+    float4* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
+    const int32_t* __restrict__ reject) {
     if (reject && *reject) return;
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n * 12) return;
@@ -89,28 +89,25 @@ __global__ void __launch_bounds__(256) adam_fused_kernel(
 #pragma unroll
         for (int j = 0; j < 4; ++j) gr[j] *= invn;
     }
-    float inv1, inv2;
-    bias_corr(step, h.b1, h.b2, db1, db2, inv1, inv2);
+    const float2 ibc = *bc;
     float4 p = sh[q], mm = m[q], vv = v[q];
-    adam4(p, mm, vv, gr, f0, h, inv1, inv2);
+    adam4(p, mm, vv, gr, f0, h, ibc.x, ibc.y);
     sh[q] = p;
     m[q] = mm;
     v[q] = vv;
 }
 
 __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
-                                  const float4* __restrict__ grad, int64_t nq, AdamHyper h, double db1,
-                                  double db2, const int32_t* __restrict__ reject,
-                                  const int64_t* __restrict__ step) {
+                                  const float4* __restrict__ grad, int64_t nq, AdamHyper h,
+                                  const float2* __restrict__ bc, const int32_t* __restrict__ reject) {
     if (reject && *reject) return;
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    float inv1, inv2;
-    bias_corr(step, h.b1, h.b2, db1, db2, inv1, inv2);
+    const float2 ibc = *bc;
     const float4 g4 = grad[q];
     const float gr[4] = {g4.x, g4.y, g4.z, g4.w};
     float4 pp = p[q], mm = m[q], vv = v[q];
-    adam4(pp, mm, vv, gr, 4 * (int)(q % 12), h, inv1, inv2);
+    adam4(pp, mm, vv, gr, 4 * (int)(q % 12), h, ibc.x, ibc.y);
     p[q] = pp;
     m[q] = mm;
     v[q] = vv;
@@ -174,10 +171,14 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
             av.acc[i] = h_d_accs[i];
             for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
         }
+        float2* bc = nullptr;
+        RCGS_TRY(dalloc(&bc, 1, s));
+        adam_prep_kernel<<<1, 1, 0, s>>>(d_step, cfg->beta1, cfg->beta2, bc);
         adam_fused_kernel<<<div_up(sc->n * 12, 256), 256, 0, s>>>(
             sc->pos, sc->n, sc->sh_degree, reinterpret_cast<float4*>(d_sh), reinterpret_cast<float4*>(d_m),
-            reinterpret_cast<float4*>(d_v), av, hyper(cfg), cfg->beta1, cfg->beta2, d_reject, d_step);
+            reinterpret_cast<float4*>(d_v), av, hyper(cfg), bc, d_reject);
         RCGS_LAUNCH_CHECK();
+        dfree(bc, s);
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
     RCGS_LAUNCH_CHECK();
@@ -191,10 +192,14 @@ extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const fl
     cudaStream_t s = as_stream(stream);
     const int64_t nq = n * 12;
     if (nq > 0) {
+        float2* bc = nullptr;
+        RCGS_TRY(dalloc(&bc, 1, s));
+        adam_prep_kernel<<<1, 1, 0, s>>>(d_step, cfg->beta1, cfg->beta2, bc);
         adam_dense_kernel<<<div_up(nq, 256), 256, 0, s>>>(
             reinterpret_cast<float4*>(d_params), reinterpret_cast<float4*>(d_m), reinterpret_cast<float4*>(d_v),
-            reinterpret_cast<const float4*>(d_grads), nq, hyper(cfg), cfg->beta1, cfg->beta2, d_reject, d_step);
+            reinterpret_cast<const float4*>(d_grads), nq, hyper(cfg), bc, d_reject);
         RCGS_LAUNCH_CHECK();
+        dfree(bc, s);
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
     RCGS_LAUNCH_CHECK();

@@ -62,16 +62,16 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
 }
 
 // ---------------------------------------------------------------- pass A
-template <bool SSIM>
-__global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
-                                                   const float* __restrict__ g, int H, int W,
+template <bool SSIM, typename T>
+__global__ void __launch_bounds__(256) loss_pass_a(const T* __restrict__ y,
+                                                   const T* __restrict__ g, int H, int W,
                                                    Window win, double* __restrict__ maps,
                                                    double* __restrict__ block_part,
                                                    int32_t* __restrict__ differ) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* iy = reinterpret_cast<float*>(smem_raw);               // [26][26][3]
-    float* ig = iy + kLH * kLH * 3;                               // [26][26][3]
-    double* hs = reinterpret_cast<double*>(ig + kLH * kLH * 3);   // [5][26][16][3]
+    double* iy = reinterpret_cast<double*>(smem_raw);             // [26][26][3]
+    double* ig = iy + kLH * kLH * 3;                              // [26][26][3]
+    double* hs = ig + kLH * kLH * 3;                              // [5][26][16][3]
     __shared__ double red[16];
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
             const int gy = y0 - kR + r, gx = x0 - kR + c;
             const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
             const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
-            iy[i] = in ? y[gi] : 0.f;
-            ig[i] = in ? g[gi] : 0.f;
+            iy[i] = in ? (double)y[gi] : 0.0;
+            ig[i] = in ? (double)g[gi] : 0.0;
         }
         __syncthreads();
         // horizontal pass: rows 0..25, output cols 0..15
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
         const int gy = y0 + r, gx = x0 + c;
         if (gy >= H || gx >= W) continue;
         const int64_t pix = (int64_t)gy * W + gx;
-        const float fy = y[pix * 3 + ch], fg = g[pix * 3 + ch];
+        const T fy = y[pix * 3 + ch], fg = g[pix * 3 + ch];
         l1 += fabs((double)fy - (double)fg);
         diff |= (fy != fg);
         if (SSIM) {
@@ -164,13 +164,13 @@ __global__ void __launch_bounds__(256) loss_pass_a(const float* __restrict__ y,
 }
 
 // ---------------------------------------------------------------- pass B
-template <bool SSIM>
-__global__ void __launch_bounds__(256) loss_pass_b(const float* __restrict__ y,
-                                                   const float* __restrict__ g, int H, int W,
+template <bool SSIM, typename T, typename G>
+__global__ void __launch_bounds__(256) loss_pass_b(const T* __restrict__ y,
+                                                   const T* __restrict__ g, int H, int W,
                                                    Window win, double lam,
                                                    const double* __restrict__ maps,
                                                    const int32_t* __restrict__ differ,
-                                                   float* __restrict__ grad) {
+                                                   G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* im = reinterpret_cast<double*>(smem_raw);  // [3 maps][26][26][3]
     double* hs = im + 3 * kLH * kLH * 3;               // [3 maps][26][16][3]
@@ -207,10 +207,10 @@ __global__ void __launch_bounds__(256) loss_pass_b(const float* __restrict__ y,
         if (gy >= H || gx >= W) continue;
         const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
         if (!any) {
-            grad[o] = 0.f;
+            grad[o] = G(0);
             continue;
         }
-        const float fy = y[o], fg = g[o];
+        const T fy = y[o], fg = g[o];
         const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
         double out = (1.0 - lam) * sgn / n;
         if (SSIM) {
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) loss_pass_b(const float* __restrict__ y,
             const double ds = (f[0] + 2.0 * (double)fy * f[1] + (double)fg * f[2]) / n;
             out -= lam * ds;
         }
-        grad[o] = (float)out;
+        grad[o] = (G)out;
     }
 }
 
@@ -264,9 +264,9 @@ static Window make_window() {
 
 using namespace rcgs;
 
-extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height,
-                              int32_t width, double lam, double* d_loss3, float* d_grad,
-                              void* stream) {
+template <typename T, typename G>
+static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, int32_t width, double lam,
+                          double* d_loss3, G* d_grad, void* stream) {
     RCGS_CHECK_ARG(d_image && d_target && d_loss3 && d_grad, "null argument");
     RCGS_CHECK_ARG(height > 0 && width > 0, "expected (H, W, 3) images, got (%d, %d, 3)", height, width);
     RCGS_CHECK_ARG(lam >= 0.0 && lam <= 1.0, "lam must be in [0, 1]");
@@ -282,30 +282,26 @@ extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32
     RCGS_TRY(dalloc(&part, 2 * nb, s));
     RCGS_TRY(dalloc(&differ, 1, s));
     RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
-    const size_t smem_a = 2 * kLH * kLH * 3 * sizeof(float) + 5 * kLH * kLT * 3 * sizeof(double);
+    const size_t smem_a = 2 * kLH * kLH * 3 * sizeof(double) + 5 * kLH * kLT * 3 * sizeof(double);
     const size_t smem_b = 3 * kLH * kLH * 3 * sizeof(double) + 3 * kLH * kLT * 3 * sizeof(double);
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
-        static bool attr = false;
-        if (!attr) {
-            RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
-            RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-            attr = true;
-        }
-        loss_pass_a<true><<<grid, 256, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
+        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
+        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+        loss_pass_a<true, T><<<grid, 256, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
-            loss_pass_b<true><<<grid, 256, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                        differ, d_grad);
+            loss_pass_b<true, T, G><<<grid, 256, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                              differ, d_grad);
         } else {
-            loss_pass_b<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                    differ, d_grad);
+            loss_pass_b<false, T, G><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                          differ, d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
-        loss_pass_a<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
-        loss_pass_b<false><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
-                                                d_grad);
+        loss_pass_a<false, T><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
+        loss_pass_b<false, T, G><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
+                                                      d_grad);
         RCGS_LAUNCH_CHECK();
     }
     loss_pass_c<<<1, 256, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
@@ -314,4 +310,14 @@ extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32
     dfree(part, s);
     dfree(differ, s);
     return RCGS_OK;
+}
+
+extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height, int32_t width,
+                              double lam, double* d_loss3, float* d_grad, void* stream) {
+    return loss_grad_impl<float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
+}
+
+extern "C" int rcgs_loss_grad_f64(const double* d_image, const double* d_target, int32_t height,
+                                  int32_t width, double lam, double* d_loss3, double* d_grad, void* stream) {
+    return loss_grad_impl<double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
 }

@@ -2,7 +2,8 @@
 
 total = (1 - lam) L1 + lam (1 - SSIM); the loss, the SSIM map and the image
 gradient are one fp64 kernel chain (csrc/loss.cu).  Host images are
-rounded to float32 on upload, the device image format.
+kept in float64 for this host-facing API (the optimizer's device path uses the
+float32 variant on float32 renders).
 """
 
 from __future__ import annotations
@@ -46,7 +47,7 @@ def _pair(image, reference, window: bool):
         raise ValidationError(f"expected (H, W, 3) images, got {image.shape}")
     if window and min(image.shape[0], image.shape[1]) < SSIM_WINDOW:
         raise ValidationError(f"images must be at least {SSIM_WINDOW}px on each side for SSIM")
-    return D.to_device(image), D.to_device(reference)
+    return D.to_device(image, torch.float64), D.to_device(reference, torch.float64)
 
 
 def _lam(lam):
@@ -55,8 +56,13 @@ def _lam(lam):
 
 
 def _run(image, reference, lam, window):
+    """float64 images in, float64 gradient out (rcgs_loss_grad_f64)."""
+    from . import _native as N
     y, g = _pair(image, reference, window)
-    loss3, grad = D.loss_grad(y, g, lam)
+    loss3 = torch.empty(3, dtype=torch.float64, device=y.device)
+    grad = torch.empty_like(y)
+    N.call("rcgs_loss_grad_f64", N.ptr(y), N.ptr(g), int(y.shape[0]), int(y.shape[1]), float(lam),
+           N.ptr(loss3), N.ptr(grad), D.stream_ptr())
     return loss3.cpu().numpy(), grad
 
 

@@ -390,3 +390,33 @@ def test_config1_against_reference():
     for v, (intr, pose) in enumerate(cams):
         dep = P.depth_from_gaussians(scene, intr, pose)
         np.testing.assert_array_equal(P.project_cloud(cloud, intr, pose, dep), d[f"v{v}_mask"])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c1.npz")), reason="c1 golden not generated")
+def test_config1_refit_trajectory():
+    """Config 1 end to end: selection (reference cloud) + 20 refit iterations with
+    seed 7.  Ground truth is each implementation's own render (self-consistent,
+    SURVEY.md 8(c)(iv)); the view sequence must be identical, the per-step losses
+    and the final render must track the reference run."""
+    from conftest import load_golden
+    from paper_2511_18441_b200.synthetic import ring_cameras, scaled_scene
+    d = load_golden("c1.npz")
+    scene, _ = scaled_scene(10_000, 0, seed=0)
+    cams = ring_cameras(256, 256, 4)
+    views = [P.TrainingView(i, intr, pose, P.render(scene, intr, pose)) for i, (intr, pose) in enumerate(cams)]
+    ds = P.build_edited_dataset(views, P.SelectionCloud(d["cloud"]), (1.0, 0.2, 0.2), scene)
+    for v in range(4):
+        np.testing.assert_array_equal(ds.views[v].mask, d[f"v{v}_mask"])
+    lines = []
+    opt = P.BackgroundOptimizer(scene, ds, seed=7, metrics_sink=lambda m: lines.append(m.line()))
+    final = opt.run_iterations(20)
+    ref = [l.split(",") for l in d["traj_lines"]]
+    got = [l.split(",") for l in lines]
+    assert [g[:3] for g in got] == [r[:3] for r in ref]
+    worst = max(abs(float(a) - float(b)) for g, r in zip(got, ref) for a, b in zip(g[3:], r[3:]))
+    img = P.render(final, *cams[0])
+    p = psnr(img, d["final_v0_render"])
+    dc = np.abs(final.sh[:, 0, :] - d["traj_dc"]).max()
+    print(f"c1 trajectory: worst metric diff {worst:.2e}, final render PSNR {p:.1f} dB, max |dDC| {dc:.2e}")
+    assert worst < 1e-3
+    assert p > 50.0

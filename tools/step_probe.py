@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--sel-views", type=int, default=2)
+    ap.add_argument("--sel-views", type=int, default=0, help="0 = all views")
     ap.add_argument("--cache-views", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -34,8 +34,8 @@ def main():
     scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
     pts = D.to_device(cloud.points, torch.float64)
     sp = P.SelectionPass(ds, cams, gt)
-    sp.run(pts, (1.0, 0.2, 0.2), indices=list(range(a.sel_views)))
-    eng = RefitEngine(ds, sh0.clone(), cams, [sp.gt[i] for i in range(len(cams))], P.OptimizerConfig(),
+    sp.run(pts, (1.0, 0.2, 0.2), indices=list(range(a.sel_views)) if a.sel_views else None)
+    eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
                       seed=7, cache_views=a.cache_views)
     for _ in range(a.warmup + a.steps):
         eng.step()
