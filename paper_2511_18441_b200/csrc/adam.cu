@@ -39,7 +39,7 @@ __device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const flo
         mm[j] = h.b1 * mm[j] + (1.0f - h.b1) * g[j];
         vv[j] = h.b2 * vv[j] + (1.0f - h.b2) * g[j] * g[j];
         const float mh = mm[j] * inv_bc1, vh = vv[j] * inv_bc2;
-        pp[j] -= lr * mh / (sqrtf(vh) + h.eps);
+        pp[j] -= __fdividef(lr * mh, sqrtf(vh) + h.eps);
     }
 }
 
@@ -59,10 +59,11 @@ __global__ void __launch_bounds__(256) adam_fused_kernel(
     float4* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
     const int32_t* __restrict__ reject) {
     if (reject && *reject) return;
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n * 12) return;
-    const int64_t g = q / 12;
-    const int f0 = 4 * (int)(q - g * 12);
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;  // n * 12 < 2^32 (checked on host)
+    if (q >= (uint32_t)n * 12u) return;
+    const uint32_t g = q / 12u;
+    const int c4 = (int)(q - g * 12u);
+    const int k0 = (4 * c4) / 3;  // the 4 coefficients span rows k0 and k0 + 1 at most
     const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
     float gr[4] = {0.f, 0.f, 0.f, 0.f};
     for (int vi = 0; vi < views.n; ++vi) {
@@ -72,17 +73,43 @@ __global__ void __launch_bounds__(256) adam_fused_kernel(
         x *= inv;
         y *= inv;
         z *= inv;
-        const int k0 = f0 / 3;  // the 4 coefficients span rows k0 and k0 + 1 at most
-        const float b0 = sh_row(k0, x, y, z, deg), b1 = sh_row(k0 + 1, x, y, z, deg);
-        const float* a = views.acc[vi] + 3 * g;
+        // branch-free: every basis row in registers, then predicated selects of k0, k0 + 1
+        const float xx = x * x, yy = y * y, zz = z * z;
+        const float d1 = deg >= 1 ? 1.f : 0.f, d2 = deg >= 2 ? 1.f : 0.f, d3 = deg >= 3 ? 1.f : 0.f;
+        const float r0 = 0.28209479177387814f;
+        const float r1 = d1 * -0.4886025119029199f * y, r2 = d1 * 0.4886025119029199f * z;
+        const float r3 = d1 * -0.4886025119029199f * x;
+        const float r4 = d2 * 1.0925484305920792f * (x * y), r5 = d2 * -1.0925484305920792f * (y * z);
+        const float r6 = d2 * 0.31539156525252005f * (2.f * zz - xx - yy);
+        const float r7 = d2 * -1.0925484305920792f * (x * z), r8 = d2 * 0.5462742152960396f * (xx - yy);
+        const float r9 = d3 * -0.5900435899266435f * y * (3.f * xx - yy);
+        const float r10 = d3 * 2.890611442640554f * (x * y) * z;
+        const float r11 = d3 * -0.4570457994644658f * y * (4.f * zz - xx - yy);
+        const float r12 = d3 * 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+        const float r13 = d3 * -0.4570457994644658f * x * (4.f * zz - xx - yy);
+        const float r14 = d3 * 1.445305721320277f * z * (xx - yy);
+        const float r15 = d3 * -0.5900435899266435f * x * (xx - 3.f * yy);
+#define RCGS_PICK(kk)                                                                           \
+    ((kk) == 0 ? r0 : (kk) == 1 ? r1 : (kk) == 2 ? r2 : (kk) == 3 ? r3 : (kk) == 4 ? r4 :         \
+     (kk) == 5 ? r5 : (kk) == 6 ? r6 : (kk) == 7 ? r7 : (kk) == 8 ? r8 : (kk) == 9 ? r9 :         \
+     (kk) == 10 ? r10 : (kk) == 11 ? r11 : (kk) == 12 ? r12 : (kk) == 13 ? r13 : (kk) == 14 ? r14 \
+                                                                                : (kk) == 15 ? r15 : 0.f)
+        const float b0 = RCGS_PICK(k0), b1 = RCGS_PICK(k0 + 1);
+#undef RCGS_PICK
+        const float* a = views.acc[vi] + 3 * (size_t)g;
         const float a0 = a[0], a1 = a[1], a2 = a[2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int f = f0 + j, ch = f - 3 * (f / 3);
-            const float bb = (f / 3 == k0) ? b0 : b1;
-            const float av = ch == 0 ? a0 : (ch == 1 ? a1 : a2);
-            gr[j] = fmaf(bb, av, gr[j]);
-        }
+        // element 4 c4 + j has row (4 c4 + j) / 3 and channel (4 c4 + j) % 3; c4 % 3
+        // fixes the pattern: 0 -> (k0: ch 0,1,2; k0+1: ch 0), 1 -> (k0: 1,2; k0+1: 0,1),
+        // 2 -> (k0: 2; k0+1: 0,1,2)
+        const int r = c4 % 3;
+        const float e0 = r == 0 ? b0 * a0 : (r == 1 ? b0 * a1 : b0 * a2);
+        const float e1 = r == 0 ? b0 * a1 : (r == 1 ? b0 * a2 : b1 * a0);
+        const float e2 = r == 0 ? b0 * a2 : (r == 1 ? b1 * a0 : b1 * a1);
+        const float e3 = r == 0 ? b1 * a0 : (r == 1 ? b1 * a1 : b1 * a2);
+        gr[0] += e0;
+        gr[1] += e1;
+        gr[2] += e2;
+        gr[3] += e3;
     }
     if (views.n > 1) {
         const float invn = 1.0f / (float)views.n;
@@ -91,7 +118,7 @@ __global__ void __launch_bounds__(256) adam_fused_kernel(
     }
     const float2 ibc = *bc;
     float4 p = sh[q], mm = m[q], vv = v[q];
-    adam4(p, mm, vv, gr, f0, h, ibc.x, ibc.y);
+    adam4(p, mm, vv, gr, 4 * c4, h, ibc.x, ibc.y);
     sh[q] = p;
     m[q] = mm;
     v[q] = vv;
@@ -163,6 +190,7 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
                                void* stream) {
     RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
     RCGS_CHECK_ARG(n_views >= 1 && n_views <= kMaxViews, "views per step must be in [1, %d]", kMaxViews);
+    RCGS_CHECK_ARG(sc->n < (int64_t)357913941, "scene too large for 32-bit Adam indexing");
     cudaStream_t s = as_stream(stream);
     if (sc->n > 0) {
         AccViews av;

@@ -105,13 +105,14 @@ struct rcgs_scene {
     double* opac;    // (n,)
 };
 
-// Raster record of one kept gaussian (rank s), fp32, 48 bytes.
+// Raster record of one kept gaussian (rank s), fp32, 48 bytes.  `a` alone is the
+// 16-byte cull record (mean + footprint half extents) the raster tests first.
 struct __align__(16) RasterRec {
-    float4 mean;   // mx_hi, my_hi, mx_lo, my_lo   (mean2d = hi + lo)
-    float4 conic;  // -a/2, -b, -c/2, opacity      (power = nha dx^2 + nb dx dy + nhc dy^2)
-    float4 gate;   // p_lo, p_hi, kappa, half2(ex, ey)  (skip if power < p_lo; exact check
-                   // below p_hi; kappa = power error coefficient; ex/ey = footprint half
-                   // extents rounded up to fp16, for sub-tile culling)
+    float4 a;  // mx_hi, my_hi, half2(ex, ey) bits, opacity
+    float4 b;  // mx_lo, my_lo, p_lo, p_hi     (mean2d = hi + lo; skip if power < p_lo,
+               //                               exact fp64 check in [p_lo, p_hi))
+    float4 c;  // -a/2, -b, -c/2, kappa        (power = nha dx^2 + nb dx dy + nhc dy^2;
+               //                               kappa = relative power-error coefficient)
 };
 
 // Exact (fp64) record for guarded decisions: the reference's own operands.

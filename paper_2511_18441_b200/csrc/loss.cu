@@ -7,21 +7,27 @@
 //   dSSIM/dy = [F(M1) + 2 y F(M2) + g F(M3)] / n,
 //   M1 = (d_mu1 - 2 d_var1 mu1 - d_cov mu2) / mass, M2 = d_var1 / mass,
 //   M3 = d_cov / mass.
-// Pass A: moments (5 maps, separable in shared memory) -> SSIM map, |y-g|,
-//         M1..M3 (fp64), per-block partial sums, "images differ" flag.
-// Pass B: separable filter of M1..M3 -> gradient (fp32 out); exactly zero when
-//         the images are identical (losses.py:127-130).
+// Pass A: moments of y, g, y^2, g^2, y g (separable filter in shared memory)
+//         -> SSIM map, |y - g|, M1..M3 (fp64), per-block partial sums and the
+//         "images differ" flag.
+// Pass B: separable filter of M1..M3 -> gradient; exactly zero when the images
+//         are identical (losses.py:127-130).
 // Pass C: fixed-order final reduction -> {l1, ssim, total} (deterministic).
+// Both filter passes work on 32x32 output tiles (42x42 with the 5-pixel halo),
+// one channel at a time; the vertical pass is a register sliding window (each
+// thread produces 4 rows of one column from 14 shared-memory rows).
 #include <math.h>
 
 #include "common.cuh"
 
 namespace rcgs {
 
-constexpr int kR = 5;            // window half width
-constexpr int kWin = 2 * kR + 1; // 11
-constexpr int kLT = 16;          // output tile
-constexpr int kLH = kLT + 2 * kR;  // 26
+constexpr int kR = 5;              // window half width
+constexpr int kWin = 2 * kR + 1;   // 11
+constexpr int kLT = 32;            // output tile edge
+constexpr int kLH = kLT + 2 * kR;  // 42
+constexpr int kRows = 4;           // output rows per thread in the vertical pass
+constexpr int kLNT = 256;          // = kLT * kLT / kRows
 
 struct Window {
     double w[kWin];
@@ -37,7 +43,6 @@ __device__ __forceinline__ double mass1d(const Window& W, int i, int len) {
     return m;
 }
 
-template <int NT>
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -52,7 +57,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
     __syncthreads();
     if (threadIdx.x == 0) {
         double x = 0.0, y = 0.0;
-        for (int w = 0; w < NT / 32; ++w) {
+        for (int w = 0; w < kLNT / 32; ++w) {
             x += sh[2 * w];
             y += sh[2 * w + 1];
         }
@@ -61,101 +66,113 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
     }
 }
 
+// Vertical 11-tap pass for kRows consecutive output rows of one column from a
+// horizontally filtered plane h[kLH][kLT] (rows r0 .. r0 + kRows + 9).
+__device__ __forceinline__ void vfilter(const double* __restrict__ h, int r0, int c, const Window& win,
+                                        double out[kRows]) {
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) out[i] = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < kRows + kWin - 1; ++rr) {
+        const double v = h[(r0 + rr) * kLT + c];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int k = rr - i;
+            if (k >= 0 && k < kWin) out[i] = fma(win.w[k], v, out[i]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- pass A
 template <bool SSIM, typename T>
-__global__ void __launch_bounds__(256) loss_pass_a(const T* __restrict__ y,
-                                                   const T* __restrict__ g, int H, int W,
-                                                   Window win, double* __restrict__ maps,
-                                                   double* __restrict__ block_part,
-                                                   int32_t* __restrict__ differ) {
+__global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
+                                                    int W, Window win, double* __restrict__ maps,
+                                                    double* __restrict__ block_part,
+                                                    int32_t* __restrict__ differ) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* iy = reinterpret_cast<double*>(smem_raw);             // [26][26][3]
-    double* ig = iy + kLH * kLH * 3;                              // [26][26][3]
-    double* hs = ig + kLH * kLH * 3;                              // [5][26][16][3]
-    __shared__ double red[16];
+    double* iy = reinterpret_cast<double*>(smem_raw);  // [42][42]
+    double* ig = iy + kLH * kLH;                       // [42][42]
+    double* hs = ig + kLH * kLH;                       // [5][42][32]
+    __shared__ double red[2 * kLNT / 32];
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
+    const int c = t % kLT, r0 = (t / kLT) * kRows;
 
     double l1 = 0.0, ss = 0.0;
     int diff = 0;
-    if (SSIM) {
-        for (int i = t; i < kLH * kLH * 3; i += 256) {
-            const int ch = i % 3, p = i / 3, r = p / kLH, c = p % kLH;
-            const int gy = y0 - kR + r, gx = x0 - kR + c;
-            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
-            iy[i] = in ? (double)y[gi] : 0.0;
-            ig[i] = in ? (double)g[gi] : 0.0;
-        }
-        __syncthreads();
-        // horizontal pass: rows 0..25, output cols 0..15
-        for (int i = t; i < kLH * kLT * 3; i += 256) {
-            const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
-            double s1 = 0, s2 = 0, s11 = 0, s22 = 0, s12 = 0;
-#pragma unroll
-            for (int k = 0; k < kWin; ++k) {
-                const int o = (r * kLH + c + k) * 3 + ch;
-                const double a = iy[o], b = ig[o], w = win.w[k];
-                s1 += w * a;
-                s2 += w * b;
-                s11 += w * (a * a);
-                s22 += w * (b * b);
-                s12 += w * (a * b);
-            }
-            const int base = (r * kLT + c) * 3 + ch;
-            const int plane = kLH * kLT * 3;
-            hs[base] = s1;
-            hs[plane + base] = s2;
-            hs[2 * plane + base] = s11;
-            hs[3 * plane + base] = s22;
-            hs[4 * plane + base] = s12;
-        }
-        __syncthreads();
-    }
-    for (int i = t; i < kLT * kLT * 3; i += 256) {
-        const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
-        const int gy = y0 + r, gx = x0 + c;
-        if (gy >= H || gx >= W) continue;
-        const int64_t pix = (int64_t)gy * W + gx;
-        const T fy = y[pix * 3 + ch], fg = g[pix * 3 + ch];
-        l1 += fabs((double)fy - (double)fg);
-        diff |= (fy != fg);
+    for (int ch = 0; ch < 3; ++ch) {
         if (SSIM) {
-            const int plane = kLH * kLT * 3;
-            double m1 = 0, m2 = 0, m11 = 0, m22 = 0, m12 = 0;
-#pragma unroll
-            for (int k = 0; k < kWin; ++k) {
-                const int base = ((r + k) * kLT + c) * 3 + ch;
-                const double w = win.w[k];
-                m1 += w * hs[base];
-                m2 += w * hs[plane + base];
-                m11 += w * hs[2 * plane + base];
-                m22 += w * hs[3 * plane + base];
-                m12 += w * hs[4 * plane + base];
+            for (int i = t; i < kLH * kLH; i += kLNT) {
+                const int r = i / kLH, cc = i % kLH;
+                const int gy = y0 - kR + r, gx = x0 - kR + cc;
+                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+                const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
+                iy[i] = in ? (double)y[gi] : 0.0;
+                ig[i] = in ? (double)g[gi] : 0.0;
             }
-            // three fp64 reciprocals replace the reference's divisions (same formulas)
-            const double im = 1.0 / (mass1d(win, gy, H) * mass1d(win, gx, W));
-            const double mu1 = m1 * im, mu2 = m2 * im;
-            const double var1 = m11 * im - mu1 * mu1;
-            const double var2 = m22 * im - mu2 * mu2;
-            const double cov = m12 * im - mu1 * mu2;
-            const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
-            const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
-            const double ib1 = 1.0 / b1, ib2 = 1.0 / b2, ib = ib1 * ib2;
-            const double a12 = a1 * a2;
-            ss += a12 * ib;
-            const double d_mu1 = 2.0 * (mu2 * a2) * ib - 2.0 * mu1 * a12 * ib * ib1;
-            const double d_var1 = -a12 * ib * ib2;
-            const double d_cov = 2.0 * a1 * ib;
-            const int64_t o = pix * 3 + ch;
-            maps[o] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im;
-            maps[npix * 3 + o] = d_var1 * im;
-            maps[2 * npix * 3 + o] = d_cov * im;
+            __syncthreads();
+            for (int i = t; i < kLH * kLT; i += kLNT) {
+                const int r = i / kLT, cc = i % kLT;
+                double s1 = 0, s2 = 0, s11 = 0, s22 = 0, s12 = 0;
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) {
+                    const int o = r * kLH + cc + k;
+                    const double a = iy[o], b = ig[o], w = win.w[k];
+                    s1 = fma(w, a, s1);
+                    s2 = fma(w, b, s2);
+                    s11 = fma(w, a * a, s11);
+                    s22 = fma(w, b * b, s22);
+                    s12 = fma(w, a * b, s12);
+                }
+                hs[i] = s1;
+                hs[kLH * kLT + i] = s2;
+                hs[2 * kLH * kLT + i] = s11;
+                hs[3 * kLH * kLT + i] = s22;
+                hs[4 * kLH * kLT + i] = s12;
+            }
+            __syncthreads();
         }
+        double m[5][kRows];
+        if (SSIM) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) vfilter(hs + q * kLH * kLT, r0, c, win, m[q]);
+        }
+        const int gx = x0 + c;
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int gy = y0 + r0 + i;
+            if (gy >= H || gx >= W) continue;
+            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+            const T fy = y[o], fg = g[o];
+            l1 += fabs((double)fy - (double)fg);
+            diff |= (fy != fg);
+            if (SSIM) {
+                // three fp64 reciprocals replace the reference's divisions (same formulas)
+                const double im = 1.0 / (mass1d(win, gy, H) * mass1d(win, gx, W));
+                const double mu1 = m[0][i] * im, mu2 = m[1][i] * im;
+                const double var1 = m[2][i] * im - mu1 * mu1;
+                const double var2 = m[3][i] * im - mu2 * mu2;
+                const double cov = m[4][i] * im - mu1 * mu2;
+                const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
+                const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
+                const double ib1 = 1.0 / b1, ib2 = 1.0 / b2, ib = ib1 * ib2;
+                const double a12 = a1 * a2;
+                ss += a12 * ib;
+                const double d_mu1 = 2.0 * (mu2 * a2) * ib - 2.0 * mu1 * a12 * ib * ib1;
+                const double d_var1 = -a12 * ib * ib2;
+                const double d_cov = 2.0 * a1 * ib;
+                // channel-planar maps ([map][ch][pixel]) keep pass B's halo loads coalesced
+                const int64_t mo = (int64_t)ch * npix + (int64_t)gy * W + gx;
+                maps[mo] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im;
+                maps[npix * 3 + mo] = d_var1 * im;
+                maps[2 * npix * 3 + mo] = d_cov * im;
+            }
+        }
+        if (SSIM) __syncthreads();  // shared planes are reused by the next channel
     }
     if (__syncthreads_or(diff) && t == 0) atomicOr(differ, 1);
-    block_sum2<256>(l1, ss, red);
+    block_sum2(l1, ss, red);
     if (t == 0) {
         const int b = blockIdx.y * gridDim.x + blockIdx.x;
         block_part[2 * b] = l1;
@@ -165,80 +182,77 @@ __global__ void __launch_bounds__(256) loss_pass_a(const T* __restrict__ y,
 
 // ---------------------------------------------------------------- pass B
 template <bool SSIM, typename T, typename G>
-__global__ void __launch_bounds__(256) loss_pass_b(const T* __restrict__ y,
-                                                   const T* __restrict__ g, int H, int W,
-                                                   Window win, double lam,
-                                                   const double* __restrict__ maps,
-                                                   const int32_t* __restrict__ differ,
-                                                   G* __restrict__ grad) {
+__global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
+                                                    int W, Window win, double lam,
+                                                    const double* __restrict__ maps,
+                                                    const int32_t* __restrict__ differ, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* im = reinterpret_cast<double*>(smem_raw);  // [3 maps][26][26][3]
-    double* hs = im + 3 * kLH * kLH * 3;               // [3 maps][26][16][3]
+    double* im = reinterpret_cast<double*>(smem_raw);  // [3][42][42]
+    double* hs = im + 3 * kLH * kLH;                   // [3][42][32]
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
     const double n = (double)(npix * 3);
     const bool any = *differ != 0;
-    if (SSIM && any) {
-        for (int i = t; i < kLH * kLH * 3; i += 256) {
-            const int ch = i % 3, p = i / 3, r = p / kLH, c = p % kLH;
-            const int gy = y0 - kR + r, gx = x0 - kR + c;
-            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
+    const int c = t % kLT, r0 = (t / kLT) * kRows;
+    for (int ch = 0; ch < 3; ++ch) {
+        if (SSIM && any) {
+            for (int i = t; i < kLH * kLH; i += kLNT) {
+                const int r = i / kLH, cc = i % kLH;
+                const int gy = y0 - kR + r, gx = x0 - kR + cc;
+                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+                const int64_t gi = (int64_t)ch * npix + (int64_t)gy * W + gx;
 #pragma unroll
-            for (int m = 0; m < 3; ++m) im[m * kLH * kLH * 3 + i] = in ? maps[m * npix * 3 + gi] : 0.0;
-        }
-        __syncthreads();
-        for (int i = t; i < kLH * kLT * 3; i += 256) {
-            const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                double s = 0.0;
-#pragma unroll
-                for (int k = 0; k < kWin; ++k) s += win.w[k] * im[m * kLH * kLH * 3 + (r * kLH + c + k) * 3 + ch];
-                hs[m * kLH * kLT * 3 + (r * kLT + c) * 3 + ch] = s;
+                for (int q = 0; q < 3; ++q) im[q * kLH * kLH + i] = in ? maps[q * npix * 3 + gi] : 0.0;
             }
-        }
-        __syncthreads();
-    }
-    for (int i = t; i < kLT * kLT * 3; i += 256) {
-        const int ch = i % 3, p = i / 3, r = p / kLT, c = p % kLT;
-        const int gy = y0 + r, gx = x0 + c;
-        if (gy >= H || gx >= W) continue;
-        const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
-        if (!any) {
-            grad[o] = G(0);
-            continue;
-        }
-        const T fy = y[o], fg = g[o];
-        const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
-        double out = (1.0 - lam) * sgn / n;
-        if (SSIM) {
-            double f[3];
+            __syncthreads();
+            for (int i = t; i < kLH * kLT; i += kLNT) {
+                const int r = i / kLT, cc = i % kLT;
 #pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                double s = 0.0;
+                for (int q = 0; q < 3; ++q) {
+                    double s = 0.0;
 #pragma unroll
-                for (int k = 0; k < kWin; ++k) s += win.w[k] * hs[m * kLH * kLT * 3 + ((r + k) * kLT + c) * 3 + ch];
-                f[m] = s;
+                    for (int k = 0; k < kWin; ++k) s = fma(win.w[k], im[q * kLH * kLH + r * kLH + cc + k], s);
+                    hs[q * kLH * kLT + i] = s;
+                }
             }
-            const double ds = (f[0] + 2.0 * (double)fy * f[1] + (double)fg * f[2]) / n;
-            out -= lam * ds;
+            __syncthreads();
         }
-        grad[o] = (G)out;
+        double f[3][kRows];
+        if (SSIM && any) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) vfilter(hs + q * kLH * kLT, r0, c, win, f[q]);
+        }
+        const int gx = x0 + c;
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int gy = y0 + r0 + i;
+            if (gy >= H || gx >= W) continue;
+            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+            if (!any) {
+                grad[o] = G(0);
+                continue;
+            }
+            const T fy = y[o], fg = g[o];
+            const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
+            double out = (1.0 - lam) * sgn / n;
+            if (SSIM) out -= lam * ((f[0][i] + 2.0 * (double)fy * f[1][i] + (double)fg * f[2][i]) / n);
+            grad[o] = (G)out;
+        }
+        if (SSIM && any) __syncthreads();
     }
 }
 
-__global__ void loss_pass_c(const double* __restrict__ part, int nb, double n, double lam,
-                            bool ssim_valid, double* __restrict__ out3) {
-    __shared__ double red[16];
+__global__ void loss_pass_c(const double* __restrict__ part, int nb, double n, double lam, bool ssim_valid,
+                            double* __restrict__ out3) {
+    __shared__ double red[2 * kLNT / 32];
     double a = 0.0, b = 0.0;
     // fixed assignment of blocks to threads and a fixed reduction tree: deterministic
-    for (int i = threadIdx.x; i < nb; i += 256) {
+    for (int i = threadIdx.x; i < nb; i += kLNT) {
         a += part[2 * i];
         b += part[2 * i + 1];
     }
-    block_sum2<256>(a, b, red);
+    block_sum2(a, b, red);
     if (threadIdx.x == 0) {
         const double l1 = a / n;
         const double ss = ssim_valid ? b / n : __longlong_as_double(0x7ff8000000000000ll);
@@ -282,29 +296,29 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     RCGS_TRY(dalloc(&part, 2 * nb, s));
     RCGS_TRY(dalloc(&differ, 1, s));
     RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
-    const size_t smem_a = 2 * kLH * kLH * 3 * sizeof(double) + 5 * kLH * kLT * 3 * sizeof(double);
-    const size_t smem_b = 3 * kLH * kLH * 3 * sizeof(double) + 3 * kLH * kLT * 3 * sizeof(double);
+    const size_t smem_a = (2 * kLH * kLH + 5 * kLH * kLT) * sizeof(double);
+    const size_t smem_b = (3 * kLH * kLH + 3 * kLH * kLT) * sizeof(double);
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-        loss_pass_a<true, T><<<grid, 256, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
+        loss_pass_a<true, T><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
-            loss_pass_b<true, T, G><<<grid, 256, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                              differ, d_grad);
+            loss_pass_b<true, T, G><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                               differ, d_grad);
         } else {
-            loss_pass_b<false, T, G><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                          differ, d_grad);
+            loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps, differ,
+                                                           d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
-        loss_pass_a<false, T><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
-        loss_pass_b<false, T, G><<<grid, 256, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
-                                                      d_grad);
+        loss_pass_a<false, T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
+        loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
+                                                       d_grad);
         RCGS_LAUNCH_CHECK();
     }
-    loss_pass_c<<<1, 256, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
+    loss_pass_c<<<1, kLNT, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
     RCGS_LAUNCH_CHECK();
     dfree(maps, s);
     dfree(part, s);

@@ -193,27 +193,28 @@ __global__ void k1_record_kernel(const double* __restrict__ pos, const double* _
     ex.op = op;
     exact[s] = ex;
 
-    RasterRec r;
-    const float mxh = (float)p.mx, myh = (float)p.my;
-    r.mean = make_float4(mxh, myh, (float)(p.mx - (double)mxh), (float)(p.my - (double)myh));
-    r.conic = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)op);
-    // alpha >= skip  <=>  power >= P := log(skip / op).  fp32 power error is bounded by
-    // |power| * 2 / (1 - |rho|) * 5.4e-7 (rho = conic correlation); a 4x safety
-    // factor gives the exact-check band [p_lo, p_hi).
+    // alpha >= skip  <=>  power >= P := log(skip / op).  The fp32 power error is bounded
+    // by |power| * 2 / (1 - |rho|) * 5.4e-7 (rho = conic correlation); with a 4x safety
+    // factor kappa = 4.4e-6 / (1 - |rho|) and the exact-check band is P -+ |P| kappa.
     const double P = log(cfg.alpha_skip / op);
     const double rho = fmin(fabs(cb) / sqrt(ca * cc), 0.999999);
-    const double margin = fabs(P) * 4.4e-6 / (1.0 - rho) + 1e-6;
+    const double kappa = 4.4e-6 / (1.0 - rho);
+    const double margin = fabs(P) * kappa + 1e-6;
     // opacity-aware footprint: alpha >= skip inside d^T conic d <= r2 = 2 ln(op/skip);
     // axis half widths r * sqrt(cov2d diag), padded for fp64 rounding.
     const double r2 = -2.0 * P;
     const double ex_ = r2 >= 0.0 ? sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4 : 0.0;
     const double ey_ = r2 >= 0.0 ? sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4 : 0.0;
-    // half extents (rounded up to fp16) ride in gate.w for the raster's sub-tile culling
+    // half extents rounded up to fp16 (+0.01 px) for the raster's sub-tile culling
     const __half hx = __float2half_ru((float)fmin(ex_ + 0.01, 60000.0));
     const __half hy = __float2half_ru((float)fmin(ey_ + 0.01, 60000.0));
     const unsigned packed = (unsigned)__half_as_ushort(hx) | ((unsigned)__half_as_ushort(hy) << 16);
-    r.gate = make_float4((float)(P - margin), (float)(P + margin), (float)(margin + 1e-6),
-                         __uint_as_float(packed));
+    RasterRec r;
+    const float mxh = (float)p.mx, myh = (float)p.my;
+    r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
+    r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
+                      (float)(P + margin));
+    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)kappa);
     rec[s] = r;
 
     Rect rc;

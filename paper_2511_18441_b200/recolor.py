@@ -111,11 +111,12 @@ class SelectionPass:
     """
 
     def __init__(self, dscene: D.DeviceScene, cameras, gt: torch.Tensor, raster=DEFAULT_CONFIG,
-                 views=None):
+                 views=None, keep_views: bool = False):
         self.dscene = dscene
         self.cameras = list(cameras)
         self.gt = gt
         self.raster = raster
+        self.keep_views = keep_views or views is not None
         self.views = views if views is not None else [None] * len(self.cameras)
         self.masks = None
         self.edited = None
@@ -152,6 +153,9 @@ class SelectionPass:
                                      out=self.masks[i])
                 if stats:
                     view.mask_hits(self.masks[i], self.hits, self.wsum)
+                if not self.keep_views:
+                    view.close()
+                    self.views[i] = None
             apply_recolor_device(self.gt[i], self.masks[i], tint, out=self.edited[i])
         return self
 
