@@ -121,13 +121,21 @@ __global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
         st[t] = kFlagPre | total;
     } else {
         st[(int64_t)tile * 256 + t] = kFlagAgg | total;
-        for (int64_t k = (int64_t)tile - 1; k >= 0; --k) {
-            uint32_t w;
-            do {
-                w = st[k * 256 + t];
-            } while ((w >> 30) == 0);
-            excl += w & kValMask;
-            if ((w >> 30) == 2) break;
+        // walk back in batches of 16 independent loads (memory-level parallelism
+        // instead of one dependent L2 round trip per predecessor)
+        constexpr int kLB = 16;
+        bool found = false;
+        for (int64_t hi = (int64_t)tile - 1; hi >= 0 && !found; hi -= kLB) {
+            uint32_t w[kLB];
+#pragma unroll
+            for (int b = 0; b < kLB; ++b) w[b] = hi - b >= 0 ? st[(hi - b) * 256 + t] : (2u << 30);
+#pragma unroll
+            for (int b = 0; b < kLB; ++b) {
+                if (found || hi - b < 0) continue;
+                while ((w[b] >> 30) == 0) w[b] = st[(hi - b) * 256 + t];
+                excl += w[b] & kValMask;
+                if ((w[b] >> 30) == 2) found = true;
+            }
         }
         st[(int64_t)tile * 256 + t] = kFlagPre | (excl + total);
     }
