@@ -126,7 +126,7 @@ __global__ void cov3d_kernel(const double* __restrict__ rot, const double* __res
 __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __restrict__ cov3d,
                                int64_t n, rcgs_camera cam, rcgs_raster_config cfg,
                                uint32_t* __restrict__ flag, uint64_t* __restrict__ key,
-                               unsigned long long* __restrict__ minmax) {
+                               unsigned long long* __restrict__ minmax, ProjF64* __restrict__ proj) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (g < n) {
@@ -137,6 +137,7 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
         if (p.kept) {
             kmin = k;
             kmax = k;
+            proj[g] = p;  // reused by k1_record (no second fp64 projection)
         }
     }
     // block min/max -> one atomic per warp
@@ -167,17 +168,17 @@ struct Rect {
     int16_t x0, y0, x1, y1;  // inclusive tile rect; x1 < x0 => empty
 };
 
-__global__ void k1_record_kernel(const double* __restrict__ pos, const double* __restrict__ cov3d,
-                                 const double* __restrict__ opac, const uint32_t* __restrict__ sgid,
-                                 int64_t k, rcgs_camera cam, rcgs_raster_config cfg, int tiles_x,
-                                 int tiles_y, uint32_t* __restrict__ gid_out,
-                                 double* __restrict__ z_out, RasterRec* __restrict__ rec,
-                                 ExactRec* __restrict__ exact, int32_t* __restrict__ rank_of,
-                                 Rect* __restrict__ rect, uint32_t* __restrict__ count) {
+__global__ void k1_record_kernel(const ProjF64* __restrict__ proj, const double* __restrict__ opac,
+                                 const uint32_t* __restrict__ sgid, int64_t k, rcgs_camera cam,
+                                 rcgs_raster_config cfg, int tiles_x, int tiles_y,
+                                 uint32_t* __restrict__ gid_out, double* __restrict__ z_out,
+                                 RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
+                                 int32_t* __restrict__ rank_of, Rect* __restrict__ rect,
+                                 uint32_t* __restrict__ count) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
     const uint32_t g = sgid[s];
-    ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
+    const ProjF64 p = proj[g];
     gid_out[s] = g;
     z_out[s] = p.z;
     rank_of[g] = (int32_t)s;
@@ -432,11 +433,14 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&kpos, n + 1, s));
     RCGS_TRY(dalloc(&key, n, s));
     RCGS_TRY(dalloc(&minmax, 2, s));
+    ProjF64* proj = nullptr;
+    RCGS_TRY(dalloc(&proj, n, s));
     {
         unsigned long long init[2] = {~0ull, 0ull};
         RCGS_CUDA(cudaMemcpyAsync(minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
-    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, n, v->cam, v->cfg, flag, key, minmax);
+    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, n, v->cam, v->cfg, flag, key, minmax,
+                                                  proj);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
     uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));
@@ -455,6 +459,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(kpos, s);
         dfree(key, s);
         dfree(minmax, s);
+        dfree(proj, s);
         return RCGS_OK;
     }
     RCGS_TRY(dalloc(&kkey, k, s));
@@ -485,11 +490,12 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&v->color, k, s));
     RCGS_TRY(dalloc(&rect, k, s));
     RCGS_TRY(dalloc(&count, k, s));
-    k1_record_kernel<<<div_up(k, 256), 256, 0, s>>>(sc->pos, sc->cov3d, sc->opac, kgid, k, v->cam, v->cfg,
-                                                    v->tiles_x, v->tiles_y, v->gid, v->z, v->rec,
-                                                    v->exact, v->rank_of, rect, count);
+    k1_record_kernel<<<div_up(k, 256), 256, 0, s>>>(proj, sc->opac, kgid, k, v->cam, v->cfg, v->tiles_x,
+                                                    v->tiles_y, v->gid, v->z, v->rec, v->exact, v->rank_of,
+                                                    rect, count);
     RCGS_LAUNCH_CHECK();
     dfree(kgid, s);
+    dfree(proj, s);
     RCGS_TRY(exclusive_scan_u32(count, v->offs, k, s));
     uint32_t* hp = reinterpret_cast<uint32_t*>(host);
     RCGS_CUDA(cudaMemcpyAsync(hp, v->offs + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

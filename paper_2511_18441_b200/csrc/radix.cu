@@ -91,12 +91,19 @@ __global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
     K key[kRIPT];
     uint32_t val[kRIPT];
     uint32_t rank[kRIPT];
+    // all 16 coalesced loads first (independent, in flight together) ...
 #pragma unroll
     for (int r = 0; r < kRIPT; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         const bool valid = i < n;
         key[r] = valid ? kin[i] : K(0);
         val[r] = valid ? (vals_are_index ? (uint32_t)i : vin[i]) : 0u;
+    }
+    // ... then the stable warp-level ranking
+#pragma unroll
+    for (int r = 0; r < kRIPT; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        const bool valid = i < n;
         const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & mask) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t before = valid ? wcnt[warp][d] : 0u;
