@@ -155,8 +155,9 @@ def run_gpu(args):
     scene, cams, ds, sh0, gt, cloud, setup_s = build_workload(cfg, rank, dev)
 
     # ---- selection pass (views sharded statically across ranks, counts all-reduced)
+    from paper_2511_18441_b200 import parallel
     pts = D.to_device(cloud.points, torch.float64)
-    mine = list(range(rank, len(cams), world))
+    mine = parallel.shard_views(len(cams), rank, world)
     sp = P.SelectionPass(ds, cams, gt)
     sp.run(pts, (1.0, 0.2, 0.2), indices=mine[:1])  # warm-up
     sp = P.SelectionPass(ds, cams, gt)
@@ -164,9 +165,8 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sp.run(pts, (1.0, 0.2, 0.2), indices=mine)
+    parallel.reduce_counts(group, sp.hits, sp.wsum)
     if world > 1:
-        torch.distributed.all_reduce(sp.hits)
-        torch.distributed.all_reduce(sp.wsum)
         for i in range(len(cams)):  # every rank needs every edited target for the refit
             torch.distributed.broadcast(sp.edited[i], src=i % world)
     e1.record()

@@ -69,6 +69,32 @@ def view_grad(scene, intr, pose, target, lam=LAMBDA):
     return backward_sh(cap, g), (l1, ss, total)
 
 
+def view_acc(scene, intr, pose, target, lam=LAMBDA):
+    """Per-gaussian channel sums acc[i, ch] = active * sum_p g[p, ch] w_ip (N, 3)
+    of one view -- backward.py:36-39 before the basis expansion -- plus the loss."""
+    cap = raster.render_forward(scene, intr, pose)
+    loss = losses.photometric(cap["image"], target, lam)
+    g = losses.loss_grad(cap["image"], target, lam)
+    p = cap["proj"]
+    acc = np.zeros((len(scene.positions), 3))
+    if p.count and cap["contrib_weight"].size:
+        part = np.zeros((p.count, 3))
+        flat = g.reshape(-1, 3)
+        np.add.at(part, cap["contrib_kept"], flat[cap["contrib_pixel"]] * cap["contrib_weight"][:, None])
+        acc[p.index] = part * p.active
+    return acc, loss
+
+
+def expand_mean(scene, centers, accs):
+    """(1/G) sum_v basis(dir_v) (x) acc_v -> (N, 16, 3) (the multi-view gradient)."""
+    out = np.zeros((len(scene.positions), 16, 3))
+    for c, a in zip(centers, accs):
+        d = scene.positions - c
+        d = d / np.linalg.norm(d, axis=1, keepdims=True)
+        out += raster.sh_basis(d, scene.sh_degree)[:, :, None] * a[:, None, :]
+    return out / len(accs)
+
+
 def run_batched(scene, views, seed, steps, batch=1, lam=LAMBDA):
     """`steps` Adam iterations; each draws `batch` views from
     default_rng(seed).integers(len(views), size=batch) (== the reference's

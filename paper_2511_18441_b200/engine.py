@@ -28,6 +28,7 @@ import torch
 
 from . import _native as N
 from . import device as D
+from . import parallel
 from .render import DEFAULT_CONFIG
 
 
@@ -47,8 +48,7 @@ class RefitEngine:
         self.cache_views = cache_views
         self.views = views if views is not None else [None] * len(self.cameras)
         self.group = group
-        self.world = torch.distributed.get_world_size(group) if group is not None else 1
-        self.rank = torch.distributed.get_rank(group) if group is not None else 0
+        self.world, self.rank = parallel.world_of(group)
         dev = D.device()
         self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         self.reject = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -83,9 +83,7 @@ class RefitEngine:
 
     def draw(self):
         """View indices of the next step from the reference RNG stream (optimize.py:106)."""
-        if self.world == 1:
-            return [int(self.rng.integers(len(self.cameras)))]
-        return [int(x) for x in self.rng.integers(len(self.cameras), size=self.world)]
+        return parallel.draw_views(self.rng, len(self.cameras), self.world)
 
     # -- one step -----------------------------------------------------------------
     def step(self, picks=None, generation: int = 0):
@@ -104,12 +102,8 @@ class RefitEngine:
         D.loss_grad(img, target, self.config.lam, loss3=rec[:3], grad=grad)
         self.reject.zero_()
         view.backward(grad, acc=self.acc, nonfinite=self.reject)
-        if self.world > 1:
-            torch.distributed.all_gather_into_tensor(self.acc_all, self.acc, group=self.group)
-            torch.distributed.all_reduce(self.reject, op=torch.distributed.ReduceOp.MAX, group=self.group)
-            accs = [self.acc_all[r] for r in range(self.world)]
-        else:
-            accs = [self.acc]
+        accs = parallel.exchange_accs(self.acc, self.group, out=self.acc_all)
+        parallel.any_rank(self.reject, self.group)
         ptrs = (ctypes.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
         cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
         N.call("rcgs_adam_fused", self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,

@@ -1,0 +1,72 @@
+"""View sharding across ranks (one process per GPU).
+
+The recolor workload shards by camera view.  These helpers are the only
+cross-rank logic; they work with any torch.distributed backend (NCCL on the
+B200 box, gloo in the CPU tests):
+
+* `draw_views`      the step's view batch from the reference RNG stream: G
+                    views per optimizer step, `rng.integers(V, size=G)` (equal
+                    to G sequential `rng.integers(V)` draws, optimize.py:106);
+                    rank r back-propagates picks[r].
+* `exchange_accs`   all-gather of the per-gaussian channel sums (N x 3 fp32
+                    per view, 12 B/gaussian instead of the 192 B dense SH
+                    gradient).  Every rank then expands sum_v basis_v (x) acc_v
+                    / G in the same order -> bit-identical Adam on all ranks,
+                    independent of the collective's reduction order.
+* `any_rank`        logical OR of the non-finite reject flags.
+* `shard_views` / `reduce_counts`  static view blocks for the selection pass
+                    and the exact integer all-reduce of its statistics.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def world_of(group) -> tuple[int, int]:
+    if group is None or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def draw_views(rng: np.random.Generator, n_views: int, world: int) -> list[int]:
+    if world == 1:
+        return [int(rng.integers(n_views))]
+    return [int(x) for x in rng.integers(n_views, size=world)]
+
+
+def exchange_accs(acc: torch.Tensor, group, out: torch.Tensor | None = None) -> list[torch.Tensor]:
+    """All-gather the local (N, 3) channel sums; returns one tensor per rank in rank order."""
+    world, _ = world_of(group)
+    if world == 1:
+        return [acc]
+    if out is None:
+        out = torch.empty((world,) + tuple(acc.shape), dtype=acc.dtype, device=acc.device)
+    if acc.is_cuda:
+        dist.all_gather_into_tensor(out, acc.contiguous(), group=group)
+    else:  # gloo: list form
+        parts = list(out.unbind(0))
+        dist.all_gather(parts, acc.contiguous(), group=group)
+    return [out[r] for r in range(world)]
+
+
+def any_rank(flag: torch.Tensor, group) -> torch.Tensor:
+    world, _ = world_of(group)
+    if world > 1:
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    return flag
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Round-robin static view shard of this rank (selection pass)."""
+    return list(range(rank, n_views, world))
+
+
+def reduce_counts(group, *tensors: torch.Tensor) -> None:
+    """Exact SUM all-reduce of integer statistics (hit counts, fixed-point weights)."""
+    world, _ = world_of(group)
+    if world > 1:
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
