@@ -1,8 +1,8 @@
 // K3/K4/K6 tile rasteriser family (render.py:263-398, backward.py:22-40).
 //
 // Work decomposition.  Pairs are binned per 16x16 tile (preprocess.cu); the
-// unit of raster work is one 8x8 pixel block of a tile, handled by ONE warp
-// (two pixels per lane, rows y and y + 4).  Warps are persistent and independent: each grabs the
+// unit of raster work is one 8x4 pixel block of a tile, handled by ONE warp
+// (one pixel per lane).  Warps are persistent and independent: each grabs the
 // next block from a global counter, walks its tile's depth-sorted list 32
 // entries at a time, culls them against the block with the 16-byte cull record
 // (mean + fp64-derived footprint half extents, rounded up), compacts the
@@ -40,8 +40,7 @@ enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRIT
 
 constexpr int kWarpsPerCTA = 8;
 constexpr int kCTA = 32 * kWarpsPerCTA;
-constexpr int kBlocksPerTile = 4;  // 2 x 2 blocks of 8x8 pixels, one warp each
-constexpr int kPx = 2;             // pixels per lane: (x, y) and (x, y + 4)
+constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8x4 pixels
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kFixScale = 1125899906842624.0;  // 2^50
 
@@ -168,12 +167,12 @@ __device__ __forceinline__ int step(const float4 ra, const float4 rb, const floa
     return COMPOSITE;
 }
 
-// Does the cull record's footprint box touch the 8x8 block at (bx0, by0)?
+// Does the cull record's footprint box touch the 8x4 block at (bx0, by0)?
 __device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float by0) {
     const unsigned packed = __float_as_uint(ra.z);
     const float ex = __half2float(__ushort_as_half((unsigned short)(packed & 0xffffu)));
     const float ey = __half2float(__ushort_as_half((unsigned short)(packed >> 16)));
-    return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 7.f;
+    return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 3.f;
 }
 
 struct WarpStage {
@@ -182,10 +181,8 @@ struct WarpStage {
     uint32_t s[32], j[32];
 };
 
-// One warp = one 8x8 block; lane (x, y) owns pixels (x, y) and (x, y + 4), so every
-// staged entry is evaluated for 64 pixels and (BWD) reduced once per 64 pixels.
 template <int M>
-__global__ void __launch_bounds__(kCTA, 4) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
     __shared__ WarpStage stage_all[kWarpsPerCTA];
     const int lane = threadIdx.x & 31;
     WarpStage& st = stage_all[threadIdx.x >> 5];
@@ -198,43 +195,33 @@ __global__ void __launch_bounds__(kCTA, 4) raster_kernel(RasterArgs a) {
         if (item >= (unsigned)a.n_items) break;
         const int tile = (int)(item / kBlocksPerTile), blk = (int)(item % kBlocksPerTile);
         const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-        const int bx0 = tx * kTile + (blk & 1) * 8, by0 = ty * kTile + (blk >> 1) * 8;
-        const int u = bx0 + (lane & 7);
+        const int bx0 = tx * kTile + (blk & 1) * 8, by0 = ty * kTile + (blk >> 1) * 4;
+        const int u = bx0 + (lane & 7), v = by0 + (lane >> 3);
+        const bool inside = u < a.W && v < a.H;
+        const int64_t pix = (int64_t)v * a.W + u;
 
-        Pix px[kPx];
-        bool done[kPx], inside[kPx];
-        int64_t pix[kPx];
-        float acc[kPx][3], g[kPx][3];
-        int32_t cross[kPx];
-        uint32_t ncap[kPx], cap_base[kPx];
-#pragma unroll
-        for (int p = 0; p < kPx; ++p) {
-            const int v = by0 + (lane >> 3) + 4 * p;
-            inside[p] = u < a.W && v < a.H;
-            pix[p] = (int64_t)v * a.W + u;
-            px[p].uf = (float)u;
-            px[p].vf = (float)v;
-            px[p].T = 1.0f;
-            px[p].E = 0.0f;
-            done[p] = !inside[p];
-            acc[p][0] = acc[p][1] = acc[p][2] = 0.f;
-            g[p][0] = g[p][1] = g[p][2] = 0.f;
-            cross[p] = -1;
-            ncap[p] = 0;
-            cap_base[p] = 0;
-            if (M == BWD && inside[p]) {
-                g[p][0] = a.grad[3 * pix[p]];
-                g[p][1] = a.grad[3 * pix[p] + 1];
-                g[p][2] = a.grad[3 * pix[p] + 2];
-            }
-            if (M == HITS && inside[p]) done[p] = a.mask[pix[p]] == 0;
-            if (M == CAP_WRITE && inside[p]) cap_base[p] = a.cap_offs[pix[p]];
+        Pix px;
+        px.uf = (float)u;
+        px.vf = (float)v;
+        px.T = 1.0f;
+        px.E = 0.0f;
+        bool done = !inside;
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
+        int32_t cross = -1;
+        uint32_t ncap = 0, cap_base = 0;
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+        if (M == BWD && inside) {
+            g0 = a.grad[3 * pix];
+            g1 = a.grad[3 * pix + 1];
+            g2 = a.grad[3 * pix + 2];
         }
+        if (M == HITS && inside) done = a.mask[pix] == 0;
+        if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
         for (uint32_t c0 = range.x; c0 < range.y; c0 += 32) {
-            if (__all_sync(0xffffffffu, done[0] && done[1])) break;
+            if (__all_sync(0xffffffffu, done)) break;
             const uint32_t j = c0 + lane;
             bool keep = false;
             uint32_t s = 0;
@@ -257,59 +244,35 @@ __global__ void __launch_bounds__(kCTA, 4) raster_kernel(RasterArgs a) {
             __syncwarp();
             const int n = __popc(bal);
             for (int k = 0; k < n; ++k) {
-                const float4 ea = st.a[k], eb = st.b[k], ec = st.c[k];
-                const uint32_t es = st.s[k], ej = st.j[k];
-                float w[kPx];
-                bool comp[kPx];
-#pragma unroll
-                for (int p = 0; p < kPx; ++p) {
-                    w[p] = 0.f;
-                    int r = SKIP;
-                    if (!done[p]) {
-                        r = step<M>(ea, eb, ec, es, ej, range.x, px[p], a, &w[p]);
-                        if (r == STOP) done[p] = true;
-                        if (r == CROSS) {
-                            cross[p] = (int32_t)es;
-                            done[p] = true;
-                        }
+                float w = 0.f;
+                int r = SKIP;
+                if (!done) {
+                    r = step<M>(st.a[k], st.b[k], st.c[k], st.s[k], st.j[k], range.x, px, a, &w);
+                    if (r == STOP) done = true;
+                    if (r == CROSS) {
+                        cross = (int32_t)st.s[k];
+                        done = true;
                     }
-                    comp[p] = (r == COMPOSITE);
                 }
+                const bool comp = (r == COMPOSITE);
                 if (M == FWD) {
-                    if (comp[0] || comp[1]) {
+                    if (comp) {
                         const float4 c = st.col[k];
-#pragma unroll
-                        for (int p = 0; p < kPx; ++p) {
-                            if (comp[p]) {
-                                acc[p][0] = fmaf(c.x, w[p], acc[p][0]);
-                                acc[p][1] = fmaf(c.y, w[p], acc[p][1]);
-                                acc[p][2] = fmaf(c.z, w[p], acc[p][2]);
-                            }
-                        }
+                        acc0 = fmaf(c.x, w, acc0);
+                        acc1 = fmaf(c.y, w, acc1);
+                        acc2 = fmaf(c.z, w, acc2);
                     }
                 } else if (M == CAP_COUNT) {
-#pragma unroll
-                    for (int p = 0; p < kPx; ++p) ncap[p] += comp[p];
+                    ncap += comp;
                 } else if (M == CAP_WRITE) {
-#pragma unroll
-                    for (int p = 0; p < kPx; ++p) {
-                        if (comp[p]) {
-                            const uint32_t o = cap_base[p] + ncap[p]++;
-                            a.cap_pixel[o] = pix[p];
-                            a.cap_kept[o] = es;
-                            a.cap_weight[o] = (double)w[p];
-                        }
+                    if (comp) {
+                        const uint32_t o = cap_base + ncap++;
+                        a.cap_pixel[o] = pix;
+                        a.cap_kept[o] = st.s[k];
+                        a.cap_weight[o] = (double)w;
                     }
                 } else if (M == BWD) {
-                    float v0 = 0.f, v1 = 0.f, v2 = 0.f;
-#pragma unroll
-                    for (int p = 0; p < kPx; ++p) {
-                        if (comp[p]) {
-                            v0 = fmaf(w[p], g[p][0], v0);
-                            v1 = fmaf(w[p], g[p][1], v1);
-                            v2 = fmaf(w[p], g[p][2], v2);
-                        }
-                    }
+                    float v0 = comp ? w * g0 : 0.f, v1 = comp ? w * g1 : 0.f, v2 = comp ? w * g2 : 0.f;
                     if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
@@ -321,56 +284,50 @@ __global__ void __launch_bounds__(kCTA, 4) raster_kernel(RasterArgs a) {
                             const float val = lane == 0 ? v0 : (lane == 1 ? v1 : v2);
                             if (isfinite(val)) {
                                 const long long q = llrint((double)val * kFixScale);
-                                atomicAdd(&a.acc_fx[3 * (int64_t)es + lane], (unsigned long long)q);
+                                atomicAdd(&a.acc_fx[3 * (int64_t)st.s[k] + lane], (unsigned long long)q);
                             } else if (a.nonfinite) {
                                 atomicOr(a.nonfinite, 1);
                             }
                         }
                     }
                 } else if (M == HITS) {
-                    const unsigned hb0 = __ballot_sync(0xffffffffu, comp[0]);
-                    const unsigned hb1 = __ballot_sync(0xffffffffu, comp[1]);
-                    if (hb0 | hb1) {
-                        float ws = (comp[0] ? w[0] : 0.f) + (comp[1] ? w[1] : 0.f);
+                    const unsigned hb = __ballot_sync(0xffffffffu, comp);
+                    if (hb) {
+                        float ws = comp ? w : 0.f;
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
                         if (lane == 0) {
-                            const uint32_t gg = a.gid[es];
-                            atomicAdd(&a.hits[gg], __popc(hb0) + __popc(hb1));
-                            atomicAdd(&a.wsum[gg], (unsigned long long)llrint((double)ws * 4294967296.0));
+                            const uint32_t g = a.gid[st.s[k]];
+                            atomicAdd(&a.hits[g], __popc(hb));
+                            atomicAdd(&a.wsum[g], (unsigned long long)llrint((double)ws * 4294967296.0));
                         }
                     }
                 }
-                if ((k & 7) == 7 && __all_sync(0xffffffffu, done[0] && done[1])) break;
+                if ((k & 7) == 7 && __all_sync(0xffffffffu, done)) break;
             }
             __syncwarp();
         }
 
-#pragma unroll
-        for (int p = 0; p < kPx; ++p) {
-            if (!inside[p]) continue;
-            if (M == FWD) {
-                const float T = px[p].T;
-                const float o0 = fmaf(T, a.bg0, acc[p][0]), o1 = fmaf(T, a.bg1, acc[p][1]),
-                            o2 = fmaf(T, a.bg2, acc[p][2]);
-                if (a.layout == 0) {
-                    a.image[3 * pix[p]] = o0;
-                    a.image[3 * pix[p] + 1] = o1;
-                    a.image[3 * pix[p] + 2] = o2;
-                } else {
-                    const int64_t plane = (int64_t)a.W * a.H;
-                    a.image[pix[p]] = o0;
-                    a.image[plane + pix[p]] = o1;
-                    a.image[2 * plane + pix[p]] = o2;
-                }
-                if (a.t_final) a.t_final[pix[p]] = T;
-            } else if (M == DEPTH) {
-                if (a.cross) a.cross[pix[p]] = cross[p];
-                if (a.depth)
-                    a.depth[pix[p]] = cross[p] >= 0 ? a.z[cross[p]] : __longlong_as_double(0x7ff0000000000000ll);
-            } else if (M == CAP_COUNT) {
-                a.cap_count[pix[p]] = ncap[p];
+        if (!inside) continue;
+        if (M == FWD) {
+            const float T = px.T;
+            const float o0 = fmaf(T, a.bg0, acc0), o1 = fmaf(T, a.bg1, acc1), o2 = fmaf(T, a.bg2, acc2);
+            if (a.layout == 0) {
+                a.image[3 * pix] = o0;
+                a.image[3 * pix + 1] = o1;
+                a.image[3 * pix + 2] = o2;
+            } else {
+                const int64_t plane = (int64_t)a.W * a.H;
+                a.image[pix] = o0;
+                a.image[plane + pix] = o1;
+                a.image[2 * plane + pix] = o2;
             }
+            if (a.t_final) a.t_final[pix] = T;
+        } else if (M == DEPTH) {
+            if (a.cross) a.cross[pix] = cross;
+            if (a.depth) a.depth[pix] = cross >= 0 ? a.z[cross] : __longlong_as_double(0x7ff0000000000000ll);
+        } else if (M == CAP_COUNT) {
+            a.cap_count[pix] = ncap;
         }
     }
 }
