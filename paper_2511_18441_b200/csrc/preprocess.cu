@@ -215,14 +215,7 @@ __global__ void k1_record_kernel(const ProjF64* __restrict__ proj, const double*
     r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
     r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
                       (float)(P + margin));
-    // Per-composite increment of the raster's relative error bound on fp32 T:
-    // |d(1 - alpha)| / (1 - alpha) <= q_max * delta_max + rounding, with
-    // q_max = a_max / (1 - a_max) (a_max = min(clamp, op) bounds alpha) and
-    // delta_max the relative alpha error at |power| <= |P| (composited entries
-    // have P <= power <= 0): |P| (kappa + 2e-7) + 6e-7 (exp2 + argument rounding).
-    const double amax = fmin(cfg.alpha_clamp, op);
-    const double e_inc = amax / (1.0 - amax) * (fabs(P) * (kappa + 2e-7) + 6e-7) + 2.4e-7;
-    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)(e_inc * 1.01));
+    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)kappa);
     rec[s] = r;
 
     Rect rc;

@@ -140,15 +140,16 @@ __device__ __forceinline__ int step(const float4 ra, const float4 rb, const floa
     } else {
         alpha = fminf(a.f_alpha_clamp, ra.w * ex2_approx(power * kLog2e));
     }
-    float Tkeep = px.T * (1.0f - alpha);
-    float Ekeep = px.E + rc.w;  // precomputed per-gaussian bound increment (preprocess.cu)
+    const float oma = 1.0f - alpha;
+    const float delta = fmaf(fabsf(power), rc.w + 2e-7f, 6e-7f);
+    float Tkeep = px.T * oma;
+    float Ekeep = fmaf(__fdividef(alpha, oma), delta, px.E + 2.4e-7f);
     double T64 = 0.0;
     bool resynced = false;
     // is the exact inclusive T below the threshold?  (fp32 test, fp64 when ambiguous)
     auto below = [&](float thr_f, double thr_d) -> bool {
-        const float band = 2.0f * Ekeep * Tkeep;
-        if (Tkeep - band >= thr_f) return false;  // common case first
-        if (Tkeep + band < thr_f) return true;
+        if (Tkeep * (1.0f + 2.0f * Ekeep) < thr_f) return true;
+        if (Tkeep * (1.0f - 2.0f * Ekeep) >= thr_f) return false;
         if (!resynced) {
             T64 = exact_T(a.exact, a.pair_s, j0, j, (double)px.uf, (double)px.vf, a.alpha_clamp,
                           a.alpha_skip);
