@@ -86,6 +86,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Reference alpha in fp64 with numpy's operation order (render.py:265-271).
 __device__ __forceinline__ double exact_alpha(const ExactRec& r, double u, double v, double clamp,
                                               double skip) {
@@ -140,16 +146,19 @@ __device__ __forceinline__ int step(const float4 ra, const float4 rb, const floa
     } else {
         alpha = fminf(a.f_alpha_clamp, ra.w * ex2_approx(power * kLog2e));
     }
-    const float oma = 1.0f - alpha;
+    const float oma = 1.0f - alpha;  // >= 0.01 (alpha clamp)
     const float delta = fmaf(fabsf(power), rc.w + 2e-7f, 6e-7f);
     float Tkeep = px.T * oma;
-    float Ekeep = fmaf(__fdividef(alpha, oma), delta, px.E + 2.4e-7f);
+    // q = alpha / (1 - alpha) via one MUFU reciprocal (relative error ~1e-7, absorbed
+    // by the 2x safety factor of the band below)
+    float Ekeep = fmaf(alpha * rcp_approx(oma), delta, px.E + 2.4e-7f);
     double T64 = 0.0;
     bool resynced = false;
     // is the exact inclusive T below the threshold?  (fp32 test, fp64 when ambiguous)
     auto below = [&](float thr_f, double thr_d) -> bool {
-        if (Tkeep * (1.0f + 2.0f * Ekeep) < thr_f) return true;
-        if (Tkeep * (1.0f - 2.0f * Ekeep) >= thr_f) return false;
+        const float band = 2.0f * Ekeep * Tkeep;
+        if (Tkeep - band >= thr_f) return false;  // the common case first
+        if (Tkeep + band < thr_f) return true;
         if (!resynced) {
             T64 = exact_T(a.exact, a.pair_s, j0, j, (double)px.uf, (double)px.vf, a.alpha_clamp,
                           a.alpha_skip);
