@@ -180,7 +180,8 @@ def run_gpu(args):
     # ---- recolor refit: K timed steps
     opt_cfg = P.OptimizerConfig()
     targets = [sp.edited[i] for i in range(len(cams))]
-    eng = RefitEngine(ds, sh0.clone(), cams, targets, opt_cfg, seed=7, cache_views=False, group=group)
+    eng = RefitEngine(ds, sh0.clone(), cams, targets, opt_cfg, seed=7, cache_views=False, group=group,
+                      prefetch=2)
     for _ in range(args.warmup):
         eng.step()
     eng.drain()
@@ -215,6 +216,7 @@ def run_gpu(args):
     frame_ms = sync_max(e0.elapsed_time(e1), world) / frames
 
     # ---- e2e through the public API, host (pinned) targets streamed each step
+    eng.close()
     e2e = run_e2e(args, scene, cams, sp, group, world) if rank == 0 or world > 1 else None
 
     gpu_launches = launches_per_step(eng) * args.steps
@@ -348,7 +350,8 @@ def run_e2e(args, scene, cams, sp, group, world):
                                mask=masks[i], image=edited[i].numpy()) for i in range(len(cams)))
     ds = P.EditedDataset(views=views, generation=0, tint=np.array([1.0, 0.2, 0.2]))
     cfg = P.OptimizerConfig(snapshot_every=1)
-    opt = P.BackgroundOptimizer(scene, ds, cfg, seed=7, group=group, cache_views=False, stream_targets=True)
+    opt = P.BackgroundOptimizer(scene, ds, cfg, seed=7, group=group, cache_views=False, stream_targets=True,
+                                prefetch=2)
     opt.run_iterations(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
@@ -360,6 +363,7 @@ def run_e2e(args, scene, cams, sp, group, world):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     dt = sync_max(dt, world)
+    opt.stop()
     h, w = edited.shape[1], edited.shape[2]
     return {"value": round(world * args.steps / dt, 3), "unit": "view-steps/s",
             "h2d_bytes_per_step": int(h * w * 3 * 4), "d2h_bytes_per_step": 32,

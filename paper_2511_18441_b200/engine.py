@@ -21,7 +21,9 @@ floating-point all-reduce.
 
 from __future__ import annotations
 
+import collections
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -32,10 +34,78 @@ from . import parallel
 from .render import DEFAULT_CONFIG
 
 
+class ViewPrefetcher:
+    """Builds the views of upcoming steps on a side stream from a worker thread.
+
+    A view build (K1 + depth sort + K2) synchronises its stream twice to size
+    its buffers; running it one or two steps ahead on its own stream and host
+    thread (ctypes releases the GIL) overlaps those syncs and the build kernels
+    with the current step's raster / loss / backward / Adam.  Every step still
+    builds its own view from scratch; only the timing moves.
+    """
+
+    def __init__(self, dscene, cameras, raster, device):
+        self.dscene, self.cameras, self.raster, self.device = dscene, cameras, raster, device
+        self.stream = torch.cuda.Stream(device=device)
+        self.jobs = collections.deque()
+        self.ready = {}
+        self.cv = threading.Condition()
+        self.stop = False
+        self.error = None
+        self.thread = threading.Thread(target=self._run, name="view-prefetch", daemon=True)
+        self.thread.start()
+
+    def submit(self, key, index):
+        with self.cv:
+            self.jobs.append((key, index))
+            self.cv.notify_all()
+
+    def take(self, key):
+        with self.cv:
+            while key not in self.ready and self.error is None:
+                self.cv.wait(timeout=1.0)
+            if self.error is not None:
+                raise self.error
+            return self.ready.pop(key)
+
+    def _run(self):
+        torch.cuda.set_device(self.device)
+        with torch.cuda.stream(self.stream):
+            while True:
+                with self.cv:
+                    while not self.jobs and not self.stop:
+                        self.cv.wait(timeout=1.0)
+                    if self.stop:
+                        return
+                    key, index = self.jobs.popleft()
+                try:
+                    intr, pose = self.cameras[index]
+                    view = D.View(self.dscene, intr, pose, self.raster)
+                    ev = torch.cuda.Event()
+                    ev.record(self.stream)
+                    with self.cv:
+                        self.ready[key] = (view, ev)
+                        self.cv.notify_all()
+                except Exception as e:  # surfaced to the consumer
+                    with self.cv:
+                        self.error = e
+                        self.cv.notify_all()
+                    return
+
+    def close(self):
+        with self.cv:
+            self.stop = True
+            self.cv.notify_all()
+        self.thread.join(timeout=30)
+        for view, _ in self.ready.values():
+            view.close()
+        self.ready.clear()
+
+
 class RefitEngine:
     def __init__(self, dscene: D.DeviceScene, sh_dev: torch.Tensor, cameras, targets,
                  config, seed: int = 0, cache_views: bool = True, views=None, group=None,
-                 raster=DEFAULT_CONFIG, max_pending: int = 4096):
+                 raster=DEFAULT_CONFIG, max_pending: int = 4096, prefetch: int = 0):
         self.dscene = dscene
         self.sh = sh_dev                      # (N, 16, 3) fp32, updated in place
         self.m = torch.zeros_like(sh_dev)
@@ -61,6 +131,19 @@ class RefitEngine:
         self._bufs = {}
         self._adam_cfg = D.adam_config(config)
         self._centers = [D.camera_center(pose) for _, pose in self.cameras]
+        # prefetch > 0: draw picks `prefetch` steps ahead and build their views on a
+        # side stream (only without view caching; see ViewPrefetcher)
+        self.prefetch = prefetch if not cache_views else 0
+        self._future = collections.deque()
+        self._seq = 0
+        self._pf = ViewPrefetcher(dscene, self.cameras, raster, dev) if self.prefetch else None
+
+    def close(self):
+        if self._pf is not None:
+            self._pf.close()
+            while self._future:
+                self._future.popleft()
+            self._pf = None
 
     # -- helpers ------------------------------------------------------------------
     def view(self, i: int) -> D.View:
@@ -86,10 +169,26 @@ class RefitEngine:
         return parallel.draw_views(self.rng, len(self.cameras), self.world)
 
     # -- one step -----------------------------------------------------------------
+    def _next_prefetched(self):
+        while len(self._future) < self.prefetch:
+            picks = self.draw()
+            key = self._seq
+            self._seq += 1
+            self._pf.submit(key, picks[self.rank] if self.world > 1 else picks[0])
+            self._future.append((key, picks))
+        key, picks = self._future.popleft()
+        view, ev = self._pf.take(key)
+        torch.cuda.current_stream().wait_event(ev)
+        return picks, view
+
     def step(self, picks=None, generation: int = 0):
-        picks = self.draw() if picks is None else picks
-        mine = picks[self.rank] if self.world > 1 else picks[0]
-        view = self.view(mine)
+        if picks is None and self._pf is not None:
+            picks, view = self._next_prefetched()
+            mine = picks[self.rank] if self.world > 1 else picks[0]
+        else:
+            picks = self.draw() if picks is None else picks
+            mine = picks[self.rank] if self.world > 1 else picks[0]
+            view = self.view(mine)
         view.color(self.sh)
         img, tgt_buf, grad = self._buf(view.height, view.width)
         view.render(None, 0, out=img)

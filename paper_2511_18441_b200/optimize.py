@@ -148,7 +148,7 @@ class BackgroundOptimizer:
 
     def __init__(self, scene, dataset, config: OptimizerConfig = DEFAULT_OPTIMIZER, seed: int = 0,
                  metrics_sink=None, *, group=None, cache_views: bool = True,
-                 stream_targets: bool = False, raster=DEFAULT_CONFIG):
+                 stream_targets: bool = False, raster=DEFAULT_CONFIG, prefetch: int = 0):
         self._config = config
         self._scene0 = scene
         self._metrics_sink = metrics_sink
@@ -158,9 +158,13 @@ class BackgroundOptimizer:
         self._raster = raster
         self._ds = D.device_scene(scene)
         self._sh0 = D.sh_to_device(scene.sh)
+        # prefetch > 0 (only with cache_views=False) builds upcoming views on a side
+        # stream; the view indices are then drawn `prefetch` steps ahead, so a
+        # dataset swap takes effect after the already-drawn steps.
         self._engine = RefitEngine(self._ds, self._sh0.clone(), self._cameras(dataset),
                                    self._targets(dataset), config, seed=seed,
-                                   cache_views=cache_views, group=group, raster=raster)
+                                   cache_views=cache_views, group=group, raster=raster,
+                                   prefetch=prefetch)
         self._pending_dataset = None
         self._accepted = 0
         self._snapshot_sh = self._sh0.clone()
@@ -198,6 +202,8 @@ class BackgroundOptimizer:
         same = self._cameras(ds) == eng.cameras
         eng.targets = self._targets(ds)
         if not same:
+            if eng._pf is not None:
+                raise ValidationError("swap_dataset with different cameras needs prefetch=0")
             eng.cameras = self._cameras(ds)
             eng.views = [None] * len(eng.cameras)
             eng._centers = [D.camera_center(p) for _, p in eng.cameras]
@@ -257,6 +263,7 @@ class BackgroundOptimizer:
         if self._thread is not None:
             self._thread.join(timeout=30.0)
             self._thread = None
+        self._engine.close()
 
     @property
     def stopped(self) -> bool:
