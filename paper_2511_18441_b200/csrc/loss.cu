@@ -7,11 +7,13 @@
 //   dSSIM/dy = [F(M1) + 2 y F(M2) + g F(M3)] / n,
 //   M1 = (d_mu1 - 2 d_var1 mu1 - d_cov mu2) / mass, M2 = d_var1 / mass,
 //   M3 = d_cov / mass.
+// Dirty: per 32x32 block, do image and target differ anywhere?  (+ global flag)
 // Pass A: moments of y, g, y^2, g^2, y g (separable filter in shared memory)
-//         -> SSIM map, |y - g|, M1..M3 (fp64), per-block partial sums and the
-//         "images differ" flag.
-// Pass B: separable filter of M1..M3 -> gradient; exactly zero when the images
-//         are identical (losses.py:127-130).
+//         -> SSIM map, |y - g|, M1..M3 (fp64) and per-block partial sums, for
+//         blocks within two blocks of a difference (elsewhere SSIM == 1, L1 == 0).
+// Pass B: separable filter of M1..M3 -> gradient within one block of a
+//         difference; exact zeros elsewhere and when the images are identical
+//         (losses.py:127-130).
 // Pass C: fixed-order final reduction -> {l1, ssim, total} (deterministic).
 // Both filter passes work on 32x32 output tiles (42x42 with the 5-pixel halo),
 // one channel at a time; the vertical pass is a register sliding window (each
@@ -83,12 +85,46 @@ __device__ __forceinline__ void vfilter(const double* __restrict__ h, int r0, in
     }
 }
 
+// ---------------------------------------------------------------- dirty blocks
+// dirty[b] = 1 iff image and target differ anywhere in 32x32 block b.  The
+// gradient at a pixel depends on images within 10 px (two 5-px windows), the SSIM
+// map within 5 px: blocks farther than one block from every dirty block have an
+// exactly-1 SSIM map, zero L1 and a mathematically zero gradient.
+template <typename T>
+__global__ void __launch_bounds__(kLNT) loss_dirty_kernel(const T* __restrict__ y, const T* __restrict__ g,
+                                                          int H, int W, uint8_t* __restrict__ dirty,
+                                                          int32_t* __restrict__ differ) {
+    const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
+    int d = 0;
+    for (int i = threadIdx.x; i < kLT * kLT * 3; i += kLNT) {
+        const int p = i / 3, ch = i % 3;
+        const int gy = y0 + p / kLT, gx = x0 + p % kLT;
+        if (gy < H && gx < W) {
+            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+            d |= y[o] != g[o];
+        }
+    }
+    d = __syncthreads_or(d);
+    if (threadIdx.x == 0) {
+        dirty[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)d;
+        if (d) atomicOr(differ, 1);
+    }
+}
+
+__device__ __forceinline__ bool near_dirty(const uint8_t* __restrict__ dirty, int r) {
+    const int bx = blockIdx.x, by = blockIdx.y;
+    for (int yy = max(0, by - r); yy <= min((int)gridDim.y - 1, by + r); ++yy)
+        for (int xx = max(0, bx - r); xx <= min((int)gridDim.x - 1, bx + r); ++xx)
+            if (dirty[yy * gridDim.x + xx]) return true;
+    return false;
+}
+
 // ---------------------------------------------------------------- pass A
 template <bool SSIM, typename T>
 __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
                                                     int W, Window win, double* __restrict__ maps,
                                                     double* __restrict__ block_part,
-                                                    int32_t* __restrict__ differ) {
+                                                    const uint8_t* __restrict__ dirty) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* iy = reinterpret_cast<double*>(smem_raw);  // [42][42]
     double* ig = iy + kLH * kLH;                       // [42][42]
@@ -99,8 +135,21 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
     const int64_t npix = (int64_t)H * W;
     const int c = t % kLT, r0 = (t / kLT) * kRows;
 
+    // Blocks more than two blocks from any difference: L1 = 0 and the SSIM map is
+    // exactly 1 (a1 == b1, a2 == b2 bitwise when y == g over the window); their
+    // maps are never read by pass B (which only runs within one block of a
+    // difference, reading a 5-px halo).
+    if (!near_dirty(dirty, SSIM ? 2 : 0)) {
+        if (t == 0) {
+            const int vw = min(kLT, W - x0), vh = min(kLT, H - y0);
+            const int b = blockIdx.y * gridDim.x + blockIdx.x;
+            block_part[2 * b] = 0.0;
+            block_part[2 * b + 1] = SSIM ? (double)(vw * vh * 3) : 0.0;
+        }
+        return;
+    }
+
     double l1 = 0.0, ss = 0.0;
-    int diff = 0;
     for (int ch = 0; ch < 3; ++ch) {
         if (SSIM) {
             for (int i = t; i < kLH * kLH; i += kLNT) {
@@ -146,7 +195,6 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
             const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
             const T fy = y[o], fg = g[o];
             l1 += fabs((double)fy - (double)fg);
-            diff |= (fy != fg);
             if (SSIM) {
                 // three fp64 reciprocals replace the reference's divisions (same formulas)
                 const double im = 1.0 / (mass1d(win, gy, H) * mass1d(win, gx, W));
@@ -171,7 +219,6 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
         }
         if (SSIM) __syncthreads();  // shared planes are reused by the next channel
     }
-    if (__syncthreads_or(diff) && t == 0) atomicOr(differ, 1);
     block_sum2(l1, ss, red);
     if (t == 0) {
         const int b = blockIdx.y * gridDim.x + blockIdx.x;
@@ -185,7 +232,8 @@ template <bool SSIM, typename T, typename G>
 __global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
                                                     int W, Window win, double lam,
                                                     const double* __restrict__ maps,
-                                                    const int32_t* __restrict__ differ, G* __restrict__ grad) {
+                                                    const int32_t* __restrict__ differ,
+                                                    const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* im = reinterpret_cast<double*>(smem_raw);  // [3][42][42]
     double* hs = im + 3 * kLH * kLH;                   // [3][42][32]
@@ -193,7 +241,9 @@ __global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, 
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
     const double n = (double)(npix * 3);
-    const bool any = *differ != 0;
+    // exact zeros where the gradient is mathematically zero: everywhere when the
+    // images are identical (losses.py:127-130), else outside one block of a difference
+    const bool any = *differ != 0 && near_dirty(dirty, SSIM ? 1 : 0);
     const int c = t % kLT, r0 = (t / kLT) * kRows;
     for (int ch = 0; ch < 3; ++ch) {
         if (SSIM && any) {
@@ -293,29 +343,32 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     const int64_t npix = (int64_t)height * width;
     double *maps = nullptr, *part = nullptr;
     int32_t* differ = nullptr;
+    uint8_t* dirty = nullptr;
     RCGS_TRY(dalloc(&part, 2 * nb, s));
     RCGS_TRY(dalloc(&differ, 1, s));
+    RCGS_TRY(dalloc(&dirty, nb, s));
     RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
+    loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty, differ);
     const size_t smem_a = (2 * kLH * kLH + 5 * kLH * kLT) * sizeof(double);
     const size_t smem_b = (3 * kLH * kLH + 3 * kLH * kLT) * sizeof(double);
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-        loss_pass_a<true, T><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, differ);
+        loss_pass_a<true, T><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, dirty);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
             loss_pass_b<true, T, G><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                               differ, d_grad);
+                                                               differ, dirty, d_grad);
         } else {
             loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps, differ,
-                                                           d_grad);
+                                                           dirty, d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
-        loss_pass_a<false, T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, differ);
+        loss_pass_a<false, T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, dirty);
         loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
-                                                       d_grad);
+                                                       dirty, d_grad);
         RCGS_LAUNCH_CHECK();
     }
     loss_pass_c<<<1, kLNT, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
@@ -323,6 +376,7 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     dfree(maps, s);
     dfree(part, s);
     dfree(differ, s);
+    dfree(dirty, s);
     return RCGS_OK;
 }
 

@@ -219,10 +219,15 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
         int32_t cross = -1;
         uint32_t ncap = 0, cap_base = 0;
         float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-        if (M == BWD && inside) {
-            g0 = a.grad[3 * pix];
-            g1 = a.grad[3 * pix + 1];
-            g2 = a.grad[3 * pix + 2];
+        if (M == BWD) {
+            if (inside) {
+                g0 = a.grad[3 * pix];
+                g1 = a.grad[3 * pix + 1];
+                g2 = a.grad[3 * pix + 2];
+            }
+            // sum_p g_p w_ip has no term from this block when all its gradients are 0
+            // (the recolor gradient is local to the edited region): skip the block
+            if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) continue;
         }
         if (M == HITS && inside) done = a.mask[pix] == 0;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];

@@ -175,6 +175,27 @@ def test_loss_and_grad_match_oracle(two_blobs):
         P.loss_grad_wrt_image(small_y, small_g, lam=0.2)
 
 
+def test_loss_grad_local_differences_match_oracle():
+    """Differences confined to small patches (one straddling a 32-px block corner):
+    the block-sparse loss kernels must equal the dense oracle everywhere."""
+    rng = np.random.default_rng(21)
+    img = rng.uniform(0.1, 0.9, (150, 170, 3))
+    tgt = img.copy()
+    tgt[28:35, 29:36] = np.clip(tgt[28:35, 29:36] * [1.0, 0.3, 0.3], 0, 1)   # block corner (32, 32)
+    tgt[120:124, 140:150, 1] += 0.05
+    for lam in (0.2, 0.0):
+        g = P.loss_grad_wrt_image(img, tgt, lam=lam)
+        ref = OL.loss_grad(img, tgt, lam=lam)
+        assert np.abs(g - ref).max() <= 1e-9 * np.abs(ref).max()
+        far = np.ones(img.shape[:2], bool)
+        far[18:46, 19:47] = False
+        far[110:135, 130:161] = False
+        assert np.all(g[far] == 0.0)
+    lb = P.photometric_loss(img, tgt)
+    l1, ss, total = OL.photometric(img, tgt)
+    assert abs(lb.l1 - l1) < 1e-13 and abs(lb.ssim - ss) < 1e-12 and abs(lb.total - total) < 1e-12
+
+
 def test_backward_matches_oracle(two_blobs):
     scene = p_scene(two_blobs)
     intr, pose = p_cam(two_blobs, "v0_")
