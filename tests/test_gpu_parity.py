@@ -187,9 +187,11 @@ def test_loss_grad_local_differences_match_oracle():
         g = P.loss_grad_wrt_image(img, tgt, lam=lam)
         ref = OL.loss_grad(img, tgt, lam=lam)
         assert np.abs(g - ref).max() <= 1e-9 * np.abs(ref).max()
+        # beyond one 32-px block of any difference the gradient is an exact zero
+        # (the dense formula leaves ~1e-20 round-off there)
         far = np.ones(img.shape[:2], bool)
-        far[18:46, 19:47] = False
-        far[110:135, 130:161] = False
+        far[:96, :96] = False
+        far[64:, 96:] = False
         assert np.all(g[far] == 0.0)
     lb = P.photometric_loss(img, tgt)
     l1, ss, total = OL.photometric(img, tgt)
