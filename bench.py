@@ -189,11 +189,15 @@ def run_gpu(args):
     # ---- recolor refit: K timed steps
     opt_cfg = P.OptimizerConfig()
     targets = [sp.edited[i] for i in range(len(cams))]
+    from paper_2511_18441_b200 import _native as N
     eng = RefitEngine(ds, sh0.clone(), cams, targets, opt_cfg, seed=7, cache_views=False, group=group,
-                      prefetch=2)
+                      prefetch=2, profile=True)
     for _ in range(args.warmup):
         eng.step()
     eng.drain()
+    eng.stage_report(reset=True)
+    counters = torch.zeros(30, dtype=torch.int64, device=dev)
+    N.call("rcgs_raster_counters", N.ptr(counters))  # work counters over the timed steps
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -205,11 +209,14 @@ def run_gpu(args):
         torch.cuda.synchronize()
     step_ms = sync_max(e0.elapsed_time(e1), world) / args.steps
     recs = eng.drain()
+    N.call("rcgs_raster_counters", None)
+    live = eng.stage_report(reset=True)
+    cnt = counters.view(6, 5).cpu().numpy() / float(args.steps)  # per launch (one per step)
     if world > 1:
         torch.distributed.barrier()
 
-    # ---- stage breakdown + per-kernel roofline (one view, CUDA events on this stream)
-    stages = stage_times(eng, cams, args.config, npix, cfg)
+    # ---- per-kernel algorithmic work (live stage times above) + view statistics
+    stages = stage_model(eng, cams, npix, cfg, live, cnt)
     # ---- rendered Mpix/s: full forward (preprocess + bin + colour + raster) per frame
     frames = max(8, args.steps)
     torch.cuda.synchronize()
@@ -232,12 +239,23 @@ def run_gpu(args):
     if rank != 0:
         return
     hbm, peak_kind = peaks()
+    fp32_peak = ctypes_fp32_peak()
+    rooflines = {}
+    for name, kk in stages["kernels"].items():
+        if kk.get("flops"):
+            ach = kk["flops"] / (kk["ms"] / 1000.0) / 1e12
+            rooflines[name] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32_peak / 1e12, 1),
+                               "unit": "TFLOP/s", "frac": round(ach / (fp32_peak / 1e12), 4),
+                               "ms_per_launch": round(kk["ms"], 4), "note": kk.get("note", "")}
+        else:
+            ach = kk["bytes"] / (kk["ms"] / 1000.0) / 1e9
+            rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                               "frac": round(ach / hbm, 4), "ms_per_launch": round(kk["ms"], 4),
+                               "note": kk.get("note", "")}
     dom = max(stages["kernels"], key=lambda k: stages["kernels"][k]["ms"])
-    dk = stages["kernels"][dom]
-    roof = {"kernel": dom, "bound": "hbm", "achieved": round(dk["gbs"], 1), "peak": hbm,
-            "unit": "GB/s", "frac": round(dk["gbs"] / hbm, 4), "traffic": None,
-            "peak_kind": peak_kind, "bytes_per_launch": dk["bytes"], "ms_per_launch": dk["ms"],
-            "note": dk.get("note", "")}
+    roof = dict(rooflines[dom], kernel=dom, traffic=None,
+                peak_kind=(peak_kind if rooflines[dom]["bound"] == "hbm" else "measured (rcgs_fp32_peak FFMA probe)"),
+                work_per_launch=stages["kernels"][dom].get("work"))
     cpu = cpu_baseline_sample(args, cfg) if args.cpu_baseline else None
     value = world / (step_ms / 1000.0)
     line = {
@@ -258,7 +276,8 @@ def run_gpu(args):
         "interactive_job_s": round((sel_ms + 100 * step_ms) / 1000.0, 4),
         "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items()},
         "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
-        "roofline": roof, "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
+        "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"],
+        "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
     }
@@ -274,75 +293,49 @@ def launches_per_step(eng):
     return 1 + 3 + 1 + ((bits + 7) // 8) * 5 + 1 + 3 + 1 + 2 * 5 + 1 + 1 + 1 + 3 + 2 + 2
 
 
-def stage_times(eng, cams, config, npix, cfg, reps=5):
-    import torch
-    import paper_2511_18441_b200 as P
+def ctypes_fp32_peak():
+    import ctypes
     from paper_2511_18441_b200 import _native as N
+    from paper_2511_18441_b200 import device as D
+    out = ctypes.c_double(0.0)
+    N.call("rcgs_fp32_peak", 20000, ctypes.byref(out), D.stream_ptr())
+    return out.value
+
+
+def stage_model(eng, cams, npix, cfg, live, cnt):
+    """Per-stage live times (CUDA events inside the timed steps) paired with the
+    algorithmic work of one launch.  Raster kernels are FP32-issue bound: their
+    work is FLOPs from the live counters -- 11 per evaluated (pixel, entry) pair
+    (dx, dy, quadratic form) + 13 per composite (exp argument, exp, alpha, clamp,
+    1 - alpha, T, weight, 3 colour FMAs), +6 per composite in the backward (g * w).
+    The rest are HBM bound: algorithmic bytes per launch."""
+    import paper_2511_18441_b200 as P
     from paper_2511_18441_b200 import device as D
 
     intr, pose = cams[1]
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-
-    def timed(fn):
-        fn()
-        torch.cuda.synchronize()
-        ev[0].record()
-        for _ in range(reps):
-            fn()
-        ev[1].record()
-        torch.cuda.synchronize()
-        return ev[0].elapsed_time(ev[1]) / reps
-
-    ds = eng.dscene
-    holder = {}
-
-    def build():
-        if "v" in holder:
-            holder["v"].close()
-        holder["v"] = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
-
-    t_build = timed(build)
-    v = holder["v"]
-    t_color = timed(lambda: v.color(eng.sh))
-    img, tgt, grad = eng._buf(intr.height, intr.width)
-    t_render = timed(lambda: v.render(None, 0, out=img))
-    loss3 = torch.empty(3, dtype=torch.float64, device="cuda")
-    target = eng.targets[1]
-    t_loss = timed(lambda: D.loss_grad(img, target, 0.2, loss3=loss3, grad=grad))
-    acc = torch.empty((ds.n, 3), dtype=torch.float32, device="cuda")
-    t_bwd = timed(lambda: v.backward(grad, acc=acc))
-    m = torch.zeros_like(eng.sh)
-    vv = torch.zeros_like(eng.sh)
-    sh = eng.sh.clone()
-    step = torch.zeros(1, dtype=torch.int64, device="cuda")
-    import ctypes
-    cfgc = D.adam_config(P.OptimizerConfig())
-    ptrs = (ctypes.c_void_p * 1)(acc.data_ptr())
-    cen = (ctypes.c_double * 3)(*D.camera_center(pose))
-
-    def adam():
-        N.call("rcgs_adam_fused", ds.handle, N.ptr(sh), N.ptr(m), N.ptr(vv), ptrs, cen, 1,
-               ctypes.byref(cfgc), None, N.ptr(step), D.stream_ptr())
-
-    t_adam = timed(adam)
-    n, k, pairs = ds.n, v.n_kept, v.n_pairs
+    v = D.View(eng.dscene, intr, pose, P.DEFAULT_CONFIG)
+    n, k, pairs = eng.dscene.n, v.n_kept, v.n_pairs
     passes = (v.sort_bits + 7) // 8
-    kern = {
-        # K1+K2: geometry read + depth sort passes on K keys + pair sort (2 passes)
-        "view_build": dict(ms=t_build, bytes=n * (24 + 48 + 8) + k * (24 + 48 + 8)
-                           + passes * k * 24 + pairs * (8 + 2 * 16), note="K1+K2"),
-        "color": dict(ms=t_color, bytes=k * (192 + 24 + 4 + 16)),
-        "raster_fwd": dict(ms=t_render, bytes=pairs * (4 + 48 + 16) + npix * 12,
-                           note="FP32/MUFU-issue bound; HBM bytes shown"),
-        "loss_grad": dict(ms=t_loss, bytes=npix * 36),
-        "raster_bwd": dict(ms=t_bwd, bytes=pairs * (4 + 4 + 48 + 16 + 12) + npix * 12 + k * 28 + n * 12,
-                           note="FP32-issue + shuffle bound; HBM bytes shown"),
-        "adam": dict(ms=t_adam, bytes=n * (6 * 192 + 12 + 24)),
-    }
-    for kk in kern.values():
-        kk["gbs"] = kk["bytes"] / (kk["ms"] / 1000.0) / 1e9
     v.close()
-    return {"kernels": kern, "pairs": pairs, "kept": k}
+    fwd, bwd = cnt[0], cnt[2]  # rows: 0 render, 2 backward (per launch)
+    kern = {
+        "view_build": dict(ms=live.get("view_build", 0.0), note="K1+K2 on the prefetch stream",
+                           bytes=n * (24 + 48 + 8 + 12) + k * (64 + 8 + 200) + passes * k * 24
+                           + pairs * (8 + 2 * 16)),
+        "color": dict(ms=live["color"], bytes=n * (192 + 24 + 4) + k * 16),
+        "raster_fwd": dict(ms=live["raster_fwd"], flops=11 * fwd[0] + 13 * fwd[1],
+                           work={"evals": int(fwd[0]), "composites": int(fwd[1]), "blocks": int(fwd[2])}),
+        "loss_grad": dict(ms=live["loss_grad"], bytes=npix * 36, note="fp64 SSIM; fused-minimum bytes"),
+        "raster_bwd": dict(ms=live["raster_bwd"], flops=11 * bwd[0] + 19 * bwd[1],
+                           work={"evals": int(bwd[0]), "composites": int(bwd[1]), "blocks": int(bwd[2]),
+                                 "blocks_skipped_zero_grad": int(bwd[3])}),
+        "adam": dict(ms=live["adam"], bytes=n * (6 * 192 + 12 + 24)),
+    }
+    work = {"fwd": {"evals_per_px": float(fwd[0]) / npix, "composites_per_px": float(fwd[1]) / npix,
+                    "warp_iterations": int(fwd[4])},
+            "bwd": {"evals_per_px": float(bwd[0]) / npix, "composites_per_px": float(bwd[1]) / npix,
+                    "warp_iterations": int(bwd[4]), "blocks_skipped": int(bwd[3])}}
+    return {"kernels": kern, "pairs": pairs, "kept": k, "raster_work": work}
 
 
 def run_e2e(args, scene, cams, sp, group, world):

@@ -117,6 +117,18 @@ int rcgs_depth(const rcgs_view* view, double tau, double* d_depth, int32_t* d_cr
 int rcgs_capture(const rcgs_view* view, int64_t* h_count, int64_t* d_pixel, int64_t* d_kept,
                  double* d_weight, void* stream);
 
+/* Instrumentation: while d_counters30 != NULL every raster launch of the process
+ * accumulates, at row `mode` (0 render, 1 depth, 2 backward, 3 mask hits, 4/5
+ * capture), {evaluated pixel-entry pairs, composited pairs, warp blocks processed,
+ * warp blocks skipped, warp-level entry iterations} into the (6, 5) uint64 array;
+ * pass NULL to switch off.  Feeds the benchmark's compute roofline (one atomic
+ * per warp block, <1% overhead). */
+int rcgs_raster_counters(uint64_t* d_counters30);
+
+/* Measured FP32 FFMA throughput of this device in FLOP/s (2 per FFMA): the
+ * denominator of the rasteriser's compute roofline. */
+int rcgs_fp32_peak(int32_t iters, double* h_flops, void* stream);
+
 /* ---- loss + image gradient (losses.py:68-134), fp64 arithmetic ---------------------- */
 /* d_loss3 (device, fp64) receives {l1, ssim, total}.  d_grad (H,W,3) fp32 gets
  * d total / d image, exactly zero when image == target (losses.py:127-130).

@@ -74,6 +74,8 @@ _SIGNATURES = {
     "rcgs_view_basis": [c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_apply_recolor_f64": [c_void_p, c_void_p, c_i64, P(c_double), c_void_p, c_void_p],
     "rcgs_mask_hits": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_raster_counters": [c_void_p],
+    "rcgs_fp32_peak": [c_i32, P(c_double), c_void_p],
 }
 EXPORTED = tuple(_SIGNATURES) + ("rcgs_version", "rcgs_last_error")
 

@@ -68,6 +68,10 @@ struct RasterArgs {
     const float* grad;
     unsigned long long* acc_fx;  // (k, 3) fixed point
     int32_t* nonfinite;
+    // optional work counters (instrumented launches only): evaluated pixel-entry
+    // pairs, composited pairs, warp blocks processed, warp blocks skipped,
+    // warp-level entry iterations
+    unsigned long long* counters;
     // HITS
     const uint8_t* mask;
     int32_t* hits;
@@ -79,6 +83,9 @@ struct RasterArgs {
     int64_t* cap_kept;
     double* cap_weight;
 };
+
+// Instrumentation: when set, raster launches accumulate work counters here.
+static unsigned long long* g_counters = nullptr;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -227,13 +234,17 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
             }
             // sum_p g_p w_ip has no term from this block when all its gradients are 0
             // (the recolor gradient is local to the edited region): skip the block
-            if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) continue;
+            if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) {
+                if (a.counters && lane == 0) atomicAdd(&a.counters[5 * M + 3], 1ull);
+                continue;
+            }
         }
         if (M == HITS && inside) done = a.mask[pix] == 0;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
+        uint32_t n_eval = 0, n_comp = 0, n_iter = 0;
         for (uint32_t c0 = range.x; c0 < range.y; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const uint32_t j = c0 + lane;
@@ -260,6 +271,10 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
             for (int k = 0; k < n; ++k) {
                 float w = 0.f;
                 int r = SKIP;
+                if (a.counters) {
+                    n_eval += !done;
+                    ++n_iter;
+                }
                 if (!done) {
                     r = step<M>(st.a[k], st.b[k], st.c[k], st.s[k], st.j[k], range.x, px, a, &w);
                     if (r == STOP) done = true;
@@ -269,6 +284,7 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
                     }
                 }
                 const bool comp = (r == COMPOSITE);
+                if (a.counters) n_comp += comp;
                 if (M == FWD) {
                     if (comp) {
                         const float4 c = st.col[k];
@@ -322,6 +338,19 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
             __syncwarp();
         }
 
+        if (a.counters) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
+                n_comp += __shfl_xor_sync(0xffffffffu, n_comp, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.counters[5 * M + 0], (unsigned long long)n_eval);
+                atomicAdd(&a.counters[5 * M + 1], (unsigned long long)n_comp);
+                atomicAdd(&a.counters[5 * M + 2], 1ull);
+                atomicAdd(&a.counters[5 * M + 4], (unsigned long long)n_iter);
+            }
+        }
         if (!inside) continue;
         if (M == FWD) {
             const float T = px.T;
@@ -386,6 +415,7 @@ static int launch(RasterArgs a, cudaStream_t s) {
     RCGS_TRY(dalloc(&counter, 1, s));
     RCGS_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
     a.counter = counter;
+    a.counters = g_counters;
     const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
     if (blocks > 0) raster_kernel<M><<<blocks, kCTA, 0, s>>>(a);
     dfree(counter, s);
@@ -396,6 +426,11 @@ static int launch(RasterArgs a, cudaStream_t s) {
 }  // namespace rcgs
 
 using namespace rcgs;
+
+extern "C" int rcgs_raster_counters(uint64_t* d_counters30) {
+    g_counters = reinterpret_cast<unsigned long long*>(d_counters30);
+    return RCGS_OK;
+}
 
 extern "C" int rcgs_render(const rcgs_view* v, const float* h_bg, int layout, float* d_image,
                            float* d_t_final, void* stream) {

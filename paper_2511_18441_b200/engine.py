@@ -44,8 +44,10 @@ class ViewPrefetcher:
     builds its own view from scratch; only the timing moves.
     """
 
-    def __init__(self, dscene, cameras, raster, device):
+    def __init__(self, dscene, cameras, raster, device, profile=False):
         self.dscene, self.cameras, self.raster, self.device = dscene, cameras, raster, device
+        self.profile = profile
+        self.events = []  # (start, end) of each view build on the side stream
         self.stream = torch.cuda.Stream(device=device)
         self.jobs = collections.deque()
         self.ready = {}
@@ -80,9 +82,14 @@ class ViewPrefetcher:
                     key, index = self.jobs.popleft()
                 try:
                     intr, pose = self.cameras[index]
+                    if self.profile:
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e0.record(self.stream)
                     view = D.View(self.dscene, intr, pose, self.raster)
-                    ev = torch.cuda.Event()
+                    ev = torch.cuda.Event(enable_timing=self.profile)
                     ev.record(self.stream)
+                    if self.profile:
+                        self.events.append((e0, ev))
                     with self.cv:
                         self.ready[key] = (view, ev)
                         self.cv.notify_all()
@@ -105,7 +112,8 @@ class ViewPrefetcher:
 class RefitEngine:
     def __init__(self, dscene: D.DeviceScene, sh_dev: torch.Tensor, cameras, targets,
                  config, seed: int = 0, cache_views: bool = True, views=None, group=None,
-                 raster=DEFAULT_CONFIG, max_pending: int = 4096, prefetch: int = 0):
+                 raster=DEFAULT_CONFIG, max_pending: int = 4096, prefetch: int = 0,
+                 profile: bool = False):
         self.dscene = dscene
         self.sh = sh_dev                      # (N, 16, 3) fp32, updated in place
         self.m = torch.zeros_like(sh_dev)
@@ -136,7 +144,10 @@ class RefitEngine:
         self.prefetch = prefetch if not cache_views else 0
         self._future = collections.deque()
         self._seq = 0
-        self._pf = ViewPrefetcher(dscene, self.cameras, raster, dev) if self.prefetch else None
+        self._pf = ViewPrefetcher(dscene, self.cameras, raster, dev, profile) if self.prefetch else None
+        # profile: CUDA events around every stage of every step (negligible cost)
+        self.profile = profile
+        self._prof = []
 
     def close(self):
         if self._pf is not None:
@@ -189,8 +200,13 @@ class RefitEngine:
             picks = self.draw() if picks is None else picks
             mine = picks[self.rank] if self.world > 1 else picks[0]
             view = self.view(mine)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if self.profile else None
+        if ev:
+            ev[0].record()
         view.color(self.sh)
         img, tgt_buf, grad = self._buf(view.height, view.width)
+        if ev:
+            ev[1].record()
         view.render(None, 0, out=img)
         target = self.targets[mine]
         if not target.is_cuda:           # streamed dataset: H2D of this step's target
@@ -198,16 +214,25 @@ class RefitEngine:
             target = tgt_buf
         slot = len(self.pending) % self.max_pending
         rec = self.records[slot]
+        if ev:
+            ev[2].record()
         D.loss_grad(img, target, self.config.lam, loss3=rec[:3], grad=grad)
         self.reject.zero_()
+        if ev:
+            ev[3].record()
         view.backward(grad, acc=self.acc, nonfinite=self.reject)
         accs = parallel.exchange_accs(self.acc, self.group, out=self.acc_all)
         parallel.any_rank(self.reject, self.group)
         ptrs = (ctypes.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
         cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
+        if ev:
+            ev[4].record()
         N.call("rcgs_adam_fused", self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
                (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
                N.ptr(self.reject), N.ptr(self.step_dev), D.stream_ptr())
+        if ev:
+            ev[5].record()
+            self._prof.append(ev)
         rec[3].copy_(self.reject[0], non_blocking=True)
         self.pending.append((picks, generation))
         if not self.cache_views:
@@ -225,6 +250,24 @@ class RefitEngine:
             r = recs[i % self.max_pending]
             out.append((picks, gen, float(r[0]), float(r[1]), float(r[2]), bool(r[3] != 0)))
         self.pending = []
+        return out
+
+    def stage_report(self, reset: bool = True) -> dict:
+        """Mean device ms per stage over the profiled steps (CUDA events on the
+        launching streams; view builds on the prefetch stream)."""
+        torch.cuda.synchronize()
+        names = ["color", "raster_fwd", "loss_grad", "raster_bwd", "adam"]
+        out = {}
+        if self._prof:
+            for i, nme in enumerate(names):
+                out[nme] = float(np.mean([e[i].elapsed_time(e[i + 1]) for e in self._prof]))
+            out["step_events"] = len(self._prof)
+        if self._pf is not None and self._pf.events:
+            out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._pf.events]))
+        if reset:
+            self._prof = []
+            if self._pf is not None:
+                self._pf.events = []
         return out
 
     def step_count(self) -> int:
