@@ -191,7 +191,7 @@ def run_gpu(args):
     targets = [sp.edited[i] for i in range(len(cams))]
     from paper_2511_18441_b200 import _native as N
     eng = RefitEngine(ds, sh0.clone(), cams, targets, opt_cfg, seed=7, cache_views=False, group=group,
-                      prefetch=2, profile=True)
+                      prefetch=args.prefetch, profile=args.profile)
     for _ in range(args.warmup):
         eng.step()
     eng.drain()
@@ -201,13 +201,21 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region
     with ClockSampler(local) as clk:
         e0.record()
-        for _ in range(args.steps):
+        marks[0].record()
+        for i in range(args.steps):
             eng.step()
+            marks[i + 1].record()
         e1.record()
         torch.cuda.synchronize()
+    gc.enable()
     step_ms = sync_max(e0.elapsed_time(e1), world) / args.steps
+    per_step = np.array([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)])
     recs = eng.drain()
     N.call("rcgs_raster_counters", None)
     live = eng.stage_report(reset=True)
@@ -242,6 +250,8 @@ def run_gpu(args):
     fp32_peak = ctypes_fp32_peak()
     rooflines = {}
     for name, kk in stages["kernels"].items():
+        if not kk.get("ms"):
+            continue
         if kk.get("flops"):
             ach = kk["flops"] / (kk["ms"] / 1000.0) / 1e12
             rooflines[name] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32_peak / 1e12, 1),
@@ -252,8 +262,8 @@ def run_gpu(args):
             rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                                "frac": round(ach / hbm, 4), "ms_per_launch": round(kk["ms"], 4),
                                "note": kk.get("note", "")}
-    dom = max(stages["kernels"], key=lambda k: stages["kernels"][k]["ms"])
-    roof = dict(rooflines[dom], kernel=dom, traffic=None,
+    dom = max(rooflines, key=lambda k: rooflines[k]["ms_per_launch"]) if rooflines else None
+    roof = None if dom is None else dict(rooflines[dom], kernel=dom, traffic=None,
                 peak_kind=(peak_kind if rooflines[dom]["bound"] == "hbm" else "measured (rcgs_fp32_peak FFMA probe)"),
                 work_per_launch=stages["kernels"][dom].get("work"))
     cpu = cpu_baseline_sample(args, cfg) if args.cpu_baseline else None
@@ -262,6 +272,7 @@ def run_gpu(args):
         "metric": METRIC, "value": round(value, 3), "unit": "view-steps/s (opt steps/s x views per step)",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "step_ms_p10_p50_p90_max": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90, 100)],
         "vs_baseline": None, "dtype": "f32 (fp64 decisions/keys/loss)", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg['n']} gaussians SH deg {cfg['deg']}, "
                                f"{cfg['views']} views {cfg['width']}x{cfg['height']}, selection + recolor",
@@ -274,7 +285,7 @@ def run_gpu(args):
                       "views_per_s": round(len(cams) / (sel_ms / 1000.0), 1),
                       "masked_px": masked_px, "cloud_points": len(cloud)},
         "interactive_job_s": round((sel_ms + 100 * step_ms) / 1000.0, 4),
-        "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items()},
+        "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items() if v.get("ms")},
         "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
         "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"],
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
@@ -318,8 +329,11 @@ def stage_model(eng, cams, npix, cfg, live, cnt):
     passes = (v.sort_bits + 7) // 8
     v.close()
     fwd, bwd = cnt[0], cnt[2]  # rows: 0 render, 2 backward (per launch)
+    live = dict(live)
+    for key in ("color", "raster_fwd", "loss_grad", "raster_bwd", "adam", "view_build"):
+        live.setdefault(key, None)
     kern = {
-        "view_build": dict(ms=live.get("view_build", 0.0), note="K1+K2 on the prefetch stream",
+        "view_build": dict(ms=live["view_build"], note="K1+K2 (prefetch stream when prefetching)",
                            bytes=n * (24 + 48 + 8 + 12) + k * (64 + 8 + 200) + passes * k * 24
                            + pairs * (8 + 2 * 16)),
         "color": dict(ms=live["color"], bytes=n * (192 + 24 + 4) + k * 16),
@@ -462,6 +476,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--prefetch", type=int, default=2, help="views built ahead on a side stream (0 = inline)")
+    ap.add_argument("--no-profile", dest="profile", action="store_false",
+                    help="skip the per-stage CUDA events inside the timed steps")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -71,6 +71,9 @@ typedef struct {
 
 int rcgs_version(void);
 const char* rcgs_last_error(void);
+/* Pre-grow the device's stream-ordered memory pool (used for the per-view and
+ * temporary buffers) to `bytes`, so steady-state steps never map new memory. */
+int rcgs_pool_reserve(int64_t bytes, void* stream);
 
 /* ---- scene (replaces the geometry half of splattint.Scene, scene.py:126-186) -------- */
 /* Copies fp64 positions (N,3), opacities (N,) and derives the view-independent 3D

@@ -76,6 +76,7 @@ _SIGNATURES = {
     "rcgs_mask_hits": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_raster_counters": [c_void_p],
     "rcgs_fp32_peak": [c_i32, P(c_double), c_void_p],
+    "rcgs_pool_reserve": [c_i64, c_void_p],
 }
 EXPORTED = tuple(_SIGNATURES) + ("rcgs_version", "rcgs_last_error")
 

@@ -71,6 +71,10 @@ void dfree(T*& p, cudaStream_t s) {
     p = nullptr;
 }
 
+// Grow the stream-ordered pool to hold `bytes` (allocate + free) so later
+// allocations do not map new physical memory on the timed path.
+int pool_reserve(int64_t bytes, cudaStream_t s);
+
 // Pinned scratch for small device->host readbacks (per thread).
 void* pinned_scratch(size_t bytes);
 

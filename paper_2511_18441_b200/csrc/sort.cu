@@ -32,6 +32,24 @@ void retain_pool_memory() {
     done_dev = dev;
 }
 
+int pool_reserve(int64_t bytes, cudaStream_t s) {
+    retain_pool_memory();
+    // several moderate blocks (the pool sub-allocates from freed blocks)
+    const int64_t chunk = (int64_t)256 << 20;
+    const int64_t n = (bytes + chunk - 1) / chunk;
+    void* ptrs[4096];
+    int64_t got = 0;
+    for (; got < n && got < 4096; ++got) {
+        if (cudaMallocAsync(&ptrs[got], chunk, s) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+        }
+    }
+    for (int64_t i = 0; i < got; ++i) cudaFreeAsync(ptrs[i], s);
+    RCGS_CUDA(cudaStreamSynchronize(s));
+    return RCGS_OK;
+}
+
 void* pinned_scratch(size_t bytes) {
     static thread_local void* buf = nullptr;
     static thread_local size_t cap = 0;
@@ -148,3 +166,8 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_
 
 extern "C" const char* rcgs_last_error(void) { return rcgs::last_error(); }
 extern "C" int rcgs_version(void) { return RCGS_VERSION; }
+
+extern "C" int rcgs_pool_reserve(int64_t bytes, void* stream) {
+    RCGS_CHECK_ARG(bytes >= 0, "negative size");
+    return rcgs::pool_reserve(bytes, rcgs::as_stream(stream));
+}

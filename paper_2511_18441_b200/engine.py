@@ -144,10 +144,15 @@ class RefitEngine:
         self.prefetch = prefetch if not cache_views else 0
         self._future = collections.deque()
         self._seq = 0
+        if self.prefetch:
+            # up to prefetch + 1 views alive at once, ~170 B per gaussian each plus
+            # build temporaries: grow the pool once, outside any timed region
+            N.call("rcgs_pool_reserve", int((self.prefetch + 2) * dscene.n * 400), D.stream_ptr())
         self._pf = ViewPrefetcher(dscene, self.cameras, raster, dev, profile) if self.prefetch else None
         # profile: CUDA events around every stage of every step (negligible cost)
         self.profile = profile
         self._prof = []
+        self._build_ev = []  # inline view builds (no prefetcher)
 
     def close(self):
         if self._pf is not None:
@@ -199,7 +204,14 @@ class RefitEngine:
         else:
             picks = self.draw() if picks is None else picks
             mine = picks[self.rank] if self.world > 1 else picks[0]
+            if self.profile:
+                b0 = torch.cuda.Event(enable_timing=True)
+                b0.record()
             view = self.view(mine)
+            if self.profile:
+                b1 = torch.cuda.Event(enable_timing=True)
+                b1.record()
+                self._build_ev.append((b0, b1))
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if self.profile else None
         if ev:
             ev[0].record()
@@ -264,8 +276,11 @@ class RefitEngine:
             out["step_events"] = len(self._prof)
         if self._pf is not None and self._pf.events:
             out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._pf.events]))
+        elif self._build_ev:
+            out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._build_ev]))
         if reset:
             self._prof = []
+            self._build_ev = []
             if self._pf is not None:
                 self._pf.events = []
         return out
