@@ -273,6 +273,7 @@ def run_gpu(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
         "step_ms_p10_p50_p90_max": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90, 100)],
+        "slowest_steps": [[int(i), round(float(per_step[i]), 3)] for i in np.argsort(per_step)[-3:][::-1]],
         "vs_baseline": None, "dtype": "f32 (fp64 decisions/keys/loss)", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg['n']} gaussians SH deg {cfg['deg']}, "
                                f"{cfg['views']} views {cfg['width']}x{cfg['height']}, selection + recolor",
