@@ -242,6 +242,11 @@ def run_gpu(args):
     # ---- e2e through the public API, host (pinned) targets streamed each step
     eng.close()
     e2e = run_e2e(args, scene, cams, sp, group, world) if rank == 0 or world > 1 else None
+    interactive = run_interactive(args, scene, cams, ds, sh0, sp, cloud) if args.extras and rank == 0 else None
+    if args.extras:
+        del sp, targets, gt
+        torch.cuda.empty_cache()
+    sweep = run_selection_sweep(group, world, rank, dev) if args.extras else None
 
     gpu_launches = launches_per_step(eng) * args.steps
     if rank != 0:
@@ -292,6 +297,7 @@ def run_gpu(args):
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        "interactive_c5": interactive, "selection_sweep_c4": sweep,
     }
     print(json.dumps(line))
 
@@ -351,6 +357,88 @@ def stage_model(eng, cams, npix, cfg, live, cnt):
             "bwd": {"evals_per_px": float(bwd[0]) / npix, "composites_per_px": float(bwd[1]) / npix,
                     "warp_iterations": int(bwd[4]), "blocks_skipped": int(bwd[3])}}
     return {"kernels": kern, "pairs": pairs, "kept": k, "raster_work": work}
+
+
+def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
+    """Config 5 (BASELINE.json): 1M gaussians, one 1080p viewer.  Per frame: one
+    optimizer step (on the sampled training view), the viewer's render of an orbit
+    camera (preprocess + bin + colour + raster), the selection overlay (depth +
+    cloud projection, blended 0.45 as session.py:381-402) and RGBA8 quantisation;
+    latency = host wall time per frame including the device sync."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import device as D
+    from paper_2511_18441_b200.engine import RefitEngine
+    from paper_2511_18441_b200.selection import project_cloud_device
+    from paper_2511_18441_b200.synthetic import ring_cameras
+
+    eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
+                      seed=11, cache_views=False)
+    intr = cams[0][0]
+    orbit = ring_cameras(intr.width, intr.height, frames)
+    pts = D.to_device(cloud.points, torch.float64)
+    tint = torch.tensor([1.0, 0.2, 0.2], device="cuda")
+    lat = []
+    for f in range(frames + 5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.step()
+        ci, cp = orbit[f % frames]
+        v = D.View(ds, ci, cp, P.DEFAULT_CONFIG)
+        v.color(eng.sh)
+        img = v.render(None, 0)
+        depth = v.depth(0.5)
+        mask = project_cloud_device(pts, ci, cp, depth, 5, 0.02)
+        m = mask.unsqueeze(-1).float()
+        img = img * (1 - 0.45 * m) + (0.45 * m) * tint
+        rgba = torch.empty((ci.height, ci.width, 4), dtype=torch.uint8, device="cuda")
+        rgba[..., :3] = (img.clamp(0, 1) * 255.0 + 0.5).to(torch.uint8)
+        rgba[..., 3] = 255
+        frame = rgba.cpu()
+        v.close()
+        torch.cuda.synchronize()
+        if f >= 5:
+            lat.append((time.perf_counter() - t0) * 1000.0)
+    eng.drain()
+    eng.close()
+    lat = np.array(lat)
+    return {"frames": len(lat), "p50_ms": round(float(np.percentile(lat, 50)), 3),
+            "p99_ms": round(float(np.percentile(lat, 99)), 3), "fps_p50": round(1000.0 / float(np.percentile(lat, 50)), 1),
+            "frame_bytes_d2h": int(frame.numel()),
+            "note": "1 optimizer step + viewer render + depth/cloud overlay + RGBA8 readback per frame"}
+
+
+def run_selection_sweep(group, world, rank, dev):
+    """Config 4 (BASELINE.json): 3M gaussians, 128 views at 1080p, selection-only
+    pass (depth + cloud projection + recolour + per-gaussian mask statistics),
+    views sharded statically across ranks, integer statistics all-reduced."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import device as D
+    from paper_2511_18441_b200 import parallel
+
+    cfg = {"n": 3_000_000, "deg": 3, "views": 128, "width": 1920, "height": 1080}
+    scene, cams, ds, sh0, gt, cloud, setup_s = build_workload(cfg, rank, dev)
+    pts = D.to_device(cloud.points, torch.float64)
+    mine = parallel.shard_views(len(cams), rank, world)
+    P.SelectionPass(ds, cams, gt).run(pts, (1.0, 0.2, 0.2), indices=mine[:2])  # warm-up
+    sp = P.SelectionPass(ds, cams, gt)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sp.run(pts, (1.0, 0.2, 0.2), indices=mine)
+    parallel.reduce_counts(group, sp.hits, sp.wsum)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = sync_max(e0.elapsed_time(e1), world)
+    out = {"config": "c4: 3M gaussians, 128 views 1920x1080, selection only", "n_gpus": world,
+           "ms": round(ms, 2), "views_per_s": round(len(cams) / (ms / 1000.0), 1),
+           "mpix_per_s": round(len(cams) * cfg["width"] * cfg["height"] / (ms / 1000.0) / 1e6, 1),
+           "gaussians_hit": int((sp.hits > 0).sum().item()), "cloud_points": len(cloud)}
+    del sp, gt, ds
+    return out
 
 
 def run_e2e(args, scene, cams, sp, group, world):
@@ -477,6 +565,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-extras", dest="extras", action="store_false",
+                    help="skip config 4 (3M selection sweep) and config 5 (interactive latency)")
     ap.add_argument("--prefetch", type=int, default=2, help="views built ahead on a side stream (0 = inline)")
     ap.add_argument("--no-profile", dest="profile", action="store_false",
                     help="skip the per-stage CUDA events inside the timed steps")
