@@ -74,11 +74,16 @@ class ClockSampler:
             masks = {k: getattr(nv, v) for k, v in self.REASONS.items()}
         except Exception:
             return
+        me = os.getpid()
+        self.foreign = set()
         while not self._stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append((sm, [k for k, m in masks.items() if r & m]))
+                for p in nv.nvmlDeviceGetComputeRunningProcesses(h):
+                    if p.pid != me:
+                        self.foreign.add(p.pid)
             except Exception:
                 pass
             self._stop.wait(self.period)
@@ -98,7 +103,8 @@ class ClockSampler:
         sm = [s[0] for s in self.samples]
         reasons = sorted({r for s in self.samples for r in s[1]})
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.samples), "source": "nvml"}
+                "samples": len(self.samples), "source": "nvml",
+                "other_compute_pids": sorted(getattr(self, "foreign", set()))}
 
 
 # ----------------------------------------------------------------------------- GPU arm
