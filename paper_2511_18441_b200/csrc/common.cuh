@@ -130,6 +130,7 @@ struct rcgs_view {
     rcgs_raster_config cfg;
     int64_t n, k, pairs;
     int tiles_x, tiles_y, sort_bits;
+    bool full_sort;       // depth order from the full 64-bit keys (fallback path)
     // per kept rank s (front to back)
     uint32_t* gid;        // (k,) scene index
     double* z;            // (k,) view-space z (bit-exact reference depth)

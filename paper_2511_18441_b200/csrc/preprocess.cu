@@ -163,6 +163,64 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
     }
 }
 
+// ---------------------------------------------------------------- depth order, 32-bit keys
+constexpr int kRetryFullSort = 100;
+
+__global__ void key32_kernel(const uint64_t* __restrict__ key, int64_t k, uint64_t kmin, int shift,
+                             uint32_t* __restrict__ k32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) k32[i] = (uint32_t)((key[i] - kmin) >> shift);
+}
+
+__global__ void key_rebase_kernel(uint64_t* __restrict__ key, int64_t k, uint64_t kmin) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) key[i] -= kmin;
+}
+
+// Runs of equal top-32-bit keys (at most 32 long) are re-sorted by the full fp64
+// key, ties by scene index (the stable input order of np.argsort, render.py:216).
+__global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ gid,
+                                   const uint64_t* __restrict__ key_of, int64_t k) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const uint32_t h = k32[i];
+    if ((i > 0 && k32[i - 1] == h) || i + 1 >= k || k32[i + 1] != h) return;  // run starts only
+    int64_t e = i + 1;
+    while (e < k && k32[e] == h && e - i <= 32) ++e;
+    const int len = (int)(e - i);
+    if (len > 32) return;  // long runs: verified by depth_check_kernel
+    uint64_t kk[32];
+    uint32_t gg[32];
+    for (int a = 0; a < len; ++a) {
+        gg[a] = gid[i + a];
+        kk[a] = key_of[gg[a]];
+    }
+    for (int a = 1; a < len; ++a) {  // insertion sort, stable, by (key, index)
+        const uint64_t ck = kk[a];
+        const uint32_t cg = gg[a];
+        int b = a - 1;
+        while (b >= 0 && (kk[b] > ck || (kk[b] == ck && gg[b] > cg))) {
+            kk[b + 1] = kk[b];
+            gg[b + 1] = gg[b];
+            --b;
+        }
+        kk[b + 1] = ck;
+        gg[b + 1] = cg;
+    }
+    for (int a = 0; a < len; ++a) gid[i + a] = gg[a];
+}
+
+// Flags any adjacent pair out of (fp64 key, index) order (only possible inside a
+// tie run longer than 32 with differing low bits).
+__global__ void depth_check_kernel(const uint32_t* __restrict__ k32, const uint32_t* __restrict__ gid,
+                                   const uint64_t* __restrict__ key_of, int64_t k, int32_t* __restrict__ bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + 1 >= k || k32[i] != k32[i + 1]) return;
+    const uint32_t g0 = gid[i], g1 = gid[i + 1];
+    const uint64_t a = key_of[g0], b = key_of[g1];
+    if (a > b || (a == b && g0 > g1)) atomicOr(bad, 1);
+}
+
 // ---------------------------------------------------------------- K1b records
 struct Rect {
     int16_t x0, y0, x1, y1;  // inclusive tile rect; x1 < x0 => empty
@@ -470,13 +528,39 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_LAUNCH_CHECK();
     dfree(flag, s);
     dfree(kpos, s);
-    dfree(key, s);
     dfree(minmax, s);
     // ---- stable depth sort over the varying key bits
-    const uint64_t diff = kmin ^ kmax;
-    v->sort_bits = diff ? 64 - __builtin_clzll(diff) : 0;
-    if (v->sort_bits > 0)
-        RCGS_TRY(radix_sort_u64(&kkey, &kkey_alt, &kgid, &kgid_alt, false, k, v->sort_bits, s));
+    // keys relative to the smallest kept key (order preserving): the exponent
+    // carry between e.g. [1, 2) and [2, 4) no longer widens the sorted range
+    const uint64_t span = kmax - kmin;
+    v->sort_bits = span ? 64 - __builtin_clzll(span) : 0;
+    int32_t* fix_flag = nullptr;
+    RCGS_TRY(dalloc(&fix_flag, 1, s));
+    RCGS_CUDA(cudaMemsetAsync(fix_flag, 0, sizeof(int32_t), s));
+    if (v->sort_bits > 0) {
+        if (v->sort_bits <= 32 || !v->full_sort) {
+            // 4-byte keys: the varying bits themselves (exact when <= 32 of them), else
+            // their top 32 bits followed by the tie-run repair and the order check
+            const int shift = v->sort_bits > 32 ? v->sort_bits - 32 : 0;
+            uint32_t *k32 = nullptr, *k32_alt = nullptr;
+            RCGS_TRY(dalloc(&k32, k, s));
+            RCGS_TRY(dalloc(&k32_alt, k, s));
+            key32_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin, shift, k32);
+            RCGS_TRY(radix_sort_u32(&k32, &k32_alt, &kgid, &kgid_alt, false, k,
+                                    v->sort_bits < 32 ? v->sort_bits : 32, s));
+            if (shift > 0) {
+                depth_fixup_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k);
+                depth_check_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k, fix_flag);
+            }
+            RCGS_LAUNCH_CHECK();
+            dfree(k32, s);
+            dfree(k32_alt, s);
+        } else {
+            key_rebase_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin);
+            RCGS_TRY(radix_sort_u64(&kkey, &kkey_alt, &kgid, &kgid_alt, false, k, v->sort_bits, s));
+        }
+    }
+    dfree(key, s);
     dfree(kkey, s);
     dfree(kkey_alt, s);
     dfree(kgid_alt, s);
@@ -499,8 +583,15 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(exclusive_scan_u32(count, v->offs, k, s));
     uint32_t* hp = reinterpret_cast<uint32_t*>(host);
     RCGS_CUDA(cudaMemcpyAsync(hp, v->offs + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaMemcpyAsync(hp + 1, fix_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RCGS_CUDA(cudaStreamSynchronize(s));
-    const int64_t pairs = *hp;
+    const int64_t pairs = hp[0];
+    dfree(fix_flag, s);
+    if (hp[1] != 0) {  // a long tie run needs the full 64-bit key sort: rebuild
+        dfree(count, s);
+        dfree(rect, s);
+        return kRetryFullSort;
+    }
     v->pairs = pairs;
     dfree(count, s);
     if (pairs == 0) {
@@ -544,6 +635,11 @@ extern "C" int rcgs_view_create(const rcgs_scene* scene, const rcgs_camera* cam,
     v->tiles_x = (cam->width + kTile - 1) / kTile;
     v->tiles_y = (cam->height + kTile - 1) / kTile;
     int st = view_build(v, s);
+    if (st == kRetryFullSort) {
+        view_free(v, s);
+        v->full_sort = true;
+        st = view_build(v, s);
+    }
     if (st != RCGS_OK) {
         view_free(v, s);
         delete v;

@@ -73,6 +73,26 @@ def test_kept_order_bit_exact(fixture, views, request):
         np.testing.assert_array_equal(z.cpu().numpy(), OR.project(scene, intr, pose).depth)
 
 
+@pytest.mark.parametrize("run", [6, 40])
+def test_depth_order_near_ties_bit_exact(run):
+    """Depths equal in their top 32 varying key bits but decreasing with scene
+    index: a short run is repaired in place, a run longer than 32 takes the
+    full 64-bit sort path; both must give np.argsort(z, kind="stable")."""
+    from paper_2511_18441_b200 import device as D
+    rng = np.random.default_rng(run)
+    spread = [dict(position=(rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), rng.uniform(1.0, 7.0)), scale=0.05)
+              for _ in range(200)]
+    ties = [dict(position=(rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), 3.0 + 1e-13 * (run - i)), scale=0.05)
+            for i in range(run)]
+    exact = [dict(position=(0.1 * i - 0.2, 0.05, 2.5), scale=0.05) for i in range(5)]  # identical z
+    ns = make_scene(spread[:100] + ties + exact + spread[100:])
+    scene = p_from_ns(ns)
+    intr, pose = p_cam_ns(*identity_camera(64, 64, fx=64.0))
+    view = D.View(D.device_scene(scene), intr, pose, P.DEFAULT_CONFIG)
+    idx, z = view.kept()
+    np.testing.assert_array_equal(idx.cpu().numpy(), OR.project(ns, intr, pose).index)
+
+
 # ---------------------------------------------------------------- raster + depth
 @pytest.mark.parametrize("fixture,views", [("two_blobs", (0, 1)), ("orbit_room", (0, 3)),
                                             ("scaled_small", (0,))])
