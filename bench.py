@@ -57,7 +57,8 @@ class ClockSampler:
                "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.05, enabled=True):
+        self.enabled = enabled
         self.samples = []
         self.index = index
         self.period = period
@@ -89,7 +90,7 @@ class ClockSampler:
             self._stop.wait(self.period)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t = threading.Thread(target=self._run if self.enabled else (lambda: None), daemon=True)
         self._t.start()
         return self
 
@@ -211,15 +212,26 @@ def run_gpu(args):
     import gc
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, enabled=args.clocks) as clk:
+        if args.call_profile:
+            N.profile_calls(True)
+        host_t = [time.perf_counter()]
         e0.record()
         marks[0].record()
         for i in range(args.steps):
             eng.step()
             marks[i + 1].record()
+            host_t.append(time.perf_counter())
         e1.record()
         torch.cuda.synchronize()
     gc.enable()
+    if args.call_profile:
+        ct = N.call_times()
+        N.profile_calls(False)
+        hs = np.diff(host_t) * 1000.0
+        print("host step ms max", round(float(hs.max()), 2), "at", int(hs.argmax()), file=sys.stderr)
+        for k, (mx, c, tot) in sorted(ct.items(), key=lambda kv: -kv[1][0])[:12]:
+            print(f"  call {k[0]:>12s} {k[1]:28s} max {mx:9.3f} ms  n {c:5d}  mean {tot / c:7.3f}", file=sys.stderr)
     step_ms = sync_max(e0.elapsed_time(e1), world) / args.steps
     per_step = np.array([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)])
     recs = eng.drain()
@@ -298,6 +310,8 @@ def run_gpu(args):
                       "masked_px": masked_px, "cloud_points": len(cloud)},
         "interactive_job_s": round((sel_ms + 100 * step_ms) / 1000.0, 4),
         "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items() if v.get("ms")},
+        "prefetch_host_ms_max": {k: round(live[k], 3) for k in ("prefetch_host_build_ms_max", "prefetch_wait_ms_max")
+                                 if k in live},
         "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
         "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"],
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
@@ -571,9 +585,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-clocks", dest="clocks", action="store_false", help="skip NVML clock sampling")
     ap.add_argument("--no-extras", dest="extras", action="store_false",
                     help="skip config 4 (3M selection sweep) and config 5 (interactive latency)")
     ap.add_argument("--prefetch", type=int, default=2, help="views built ahead on a side stream (0 = inline)")
+    ap.add_argument("--call-profile", action="store_true",
+                    help="diagnostics: host time of every C-ABI call in the timed loop (stderr)")
     ap.add_argument("--no-profile", dest="profile", action="store_false",
                     help="skip the per-stage CUDA events inside the timed steps")
     args = ap.parse_args()

@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import time
 
 from .errors import SplattintError, ValidationError
 
@@ -119,9 +120,33 @@ def check(status: int) -> None:
     raise SplattintError(f"rcgs error {status}: {msg}")
 
 
+_CALL_TIMES = None  # {(thread name, fn): [max ms, count, total ms]} when profiling
+
+
+def profile_calls(enable: bool = True) -> None:
+    """Record host-side duration of every C-ABI call (diagnostics only)."""
+    global _CALL_TIMES
+    _CALL_TIMES = {} if enable else None
+
+
+def call_times() -> dict:
+    return dict(_CALL_TIMES or {})
+
+
 def call(name: str, *args) -> None:
     lib = load_library()
-    check(getattr(lib, name)(*args))
+    if _CALL_TIMES is None:
+        check(getattr(lib, name)(*args))
+        return
+    t0 = time.perf_counter()
+    rc = getattr(lib, name)(*args)
+    ms = (time.perf_counter() - t0) * 1000.0
+    key = (threading.current_thread().name, name)
+    rec = _CALL_TIMES.setdefault(key, [0.0, 0, 0.0])
+    rec[0] = max(rec[0], ms)
+    rec[1] += 1
+    rec[2] += ms
+    check(rc)
 
 
 def ptr(t) -> int | None:

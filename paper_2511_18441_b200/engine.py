@@ -24,6 +24,7 @@ from __future__ import annotations
 import collections
 import ctypes
 import threading
+import time
 
 import numpy as np
 import torch
@@ -42,14 +43,24 @@ class ViewPrefetcher:
     thread (ctypes releases the GIL) overlaps those syncs and the build kernels
     with the current step's raster / loss / backward / Adam.  Every step still
     builds its own view from scratch; only the timing moves.
+
+    Used views come back through `retire`: the worker frees them on ITS stream
+    after an event recorded on the consumer's stream.  Allocation and release of
+    view memory then happen on one stream, so the stream-ordered pool reuses
+    blocks without cross-stream dependencies and never grows in steady state.
+    Growing it (a driver-locked physical allocation) stalled both host threads
+    for 30-800 ms when views were freed on the consumer stream instead.
     """
 
     def __init__(self, dscene, cameras, raster, device, profile=False):
         self.dscene, self.cameras, self.raster, self.device = dscene, cameras, raster, device
         self.profile = profile
         self.events = []  # (start, end) of each view build on the side stream
+        self.host_build_ms = []
+        self.host_wait_ms = []
         self.stream = torch.cuda.Stream(device=device)
         self.jobs = collections.deque()
+        self.retired = collections.deque()
         self.ready = {}
         self.cv = threading.Condition()
         self.stop = False
@@ -62,10 +73,30 @@ class ViewPrefetcher:
             self.jobs.append((key, index))
             self.cv.notify_all()
 
+    def retire(self, view):
+        """Hand a used view back; it is freed on the side stream once the current
+        stream's work queued so far (which reads the view) has completed."""
+        ev = torch.cuda.Event()
+        ev.record()
+        with self.cv:
+            self.retired.append((view, ev))
+            self.cv.notify_all()
+
+    def _free_retired(self):
+        with self.cv:
+            items = list(self.retired)
+            self.retired.clear()
+        for view, ev in items:
+            self.stream.wait_event(ev)
+            view.close()
+
     def take(self, key):
+        t0 = time.perf_counter()
         with self.cv:
             while key not in self.ready and self.error is None:
                 self.cv.wait(timeout=1.0)
+            if self.profile:
+                self.host_wait_ms.append((time.perf_counter() - t0) * 1000.0)
             if self.error is not None:
                 raise self.error
             return self.ready.pop(key)
@@ -75,17 +106,24 @@ class ViewPrefetcher:
         with torch.cuda.stream(self.stream):
             while True:
                 with self.cv:
-                    while not self.jobs and not self.stop:
+                    while not self.jobs and not self.retired and not self.stop:
                         self.cv.wait(timeout=1.0)
                     if self.stop:
                         return
-                    key, index = self.jobs.popleft()
+                    job = self.jobs.popleft() if self.jobs else None
+                if job is None:
+                    self._free_retired()
+                    continue
+                key, index = job
                 try:
                     intr, pose = self.cameras[index]
+                    t0 = time.perf_counter()
                     if self.profile:
                         e0 = torch.cuda.Event(enable_timing=True)
                         e0.record(self.stream)
                     view = D.View(self.dscene, intr, pose, self.raster)
+                    if self.profile:
+                        self.host_build_ms.append((time.perf_counter() - t0) * 1000.0)
                     ev = torch.cuda.Event(enable_timing=self.profile)
                     ev.record(self.stream)
                     if self.profile:
@@ -93,6 +131,7 @@ class ViewPrefetcher:
                     with self.cv:
                         self.ready[key] = (view, ev)
                         self.cv.notify_all()
+                    self._free_retired()
                 except Exception as e:  # surfaced to the consumer
                     with self.cv:
                         self.error = e
@@ -104,8 +143,10 @@ class ViewPrefetcher:
             self.stop = True
             self.cv.notify_all()
         self.thread.join(timeout=30)
-        for view, _ in self.ready.values():
-            view.close()
+        with torch.cuda.stream(self.stream):
+            self._free_retired()
+            for view, _ in self.ready.values():
+                view.close()
         self.ready.clear()
 
 
@@ -201,7 +242,9 @@ class RefitEngine:
         if picks is None and self._pf is not None:
             picks, view = self._next_prefetched()
             mine = picks[self.rank] if self.world > 1 else picks[0]
+            prefetched = True
         else:
+            prefetched = False
             picks = self.draw() if picks is None else picks
             mine = picks[self.rank] if self.world > 1 else picks[0]
             if self.profile:
@@ -247,7 +290,9 @@ class RefitEngine:
             self._prof.append(ev)
         rec[3].copy_(self.reject[0], non_blocking=True)
         self.pending.append((picks, generation))
-        if not self.cache_views:
+        if prefetched:
+            self._pf.retire(view)
+        elif not self.cache_views:
             view.close()
         return picks
 
@@ -276,6 +321,9 @@ class RefitEngine:
             out["step_events"] = len(self._prof)
         if self._pf is not None and self._pf.events:
             out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._pf.events]))
+            if self._pf.host_build_ms:
+                out["prefetch_host_build_ms_max"] = float(np.max(self._pf.host_build_ms))
+                out["prefetch_wait_ms_max"] = float(np.max(self._pf.host_wait_ms or [0.0]))
         elif self._build_ev:
             out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._build_ev]))
         if reset:
@@ -283,6 +331,8 @@ class RefitEngine:
             self._build_ev = []
             if self._pf is not None:
                 self._pf.events = []
+                self._pf.host_build_ms = []
+                self._pf.host_wait_ms = []
         return out
 
     def step_count(self) -> int:
