@@ -94,6 +94,9 @@ int rcgs_view_info_get(const rcgs_view* view, rcgs_view_info* out);
 int rcgs_view_destroy(rcgs_view* view, void* stream);
 /* Kept gaussians front to back: scene index (K,) int64 and view-space z (K,) fp64. */
 int rcgs_view_kept(const rcgs_view* view, int64_t* d_index, double* d_depth, void* stream);
+/* Tile bins: [start, end) into the pair list per 16x16 tile, row-major (tiles_y,
+ * tiles_x, 2) uint32 (the reference's per-tile index lists, render.py binning). */
+int rcgs_view_ranges(const rcgs_view* view, uint32_t* d_ranges, void* stream);
 
 /* SH basis (K,16) fp64 along each kept gaussian's view direction and the channel
  * activation flags (K,3) uint8 from the last rcgs_view_color (ForwardCapture.basis /
@@ -127,6 +130,13 @@ int rcgs_capture(const rcgs_view* view, int64_t* h_count, int64_t* d_pixel, int6
  * pass NULL to switch off.  Feeds the benchmark's compute roofline (one atomic
  * per warp block, <1% overhead). */
 int rcgs_raster_counters(uint64_t* d_counters30);
+
+/* Diagnostics: while d_trace != NULL every raster launch with at most max_items
+ * work items (8x4 pixel blocks) overwrites, per item, 8 uint32 {start ns, end ns
+ * (globaltimer low word), SM id, warp entry iterations, evaluated pixel-entry
+ * pairs, fp64 gate-band alpha evaluations, exact transmittance re-walks, tile};
+ * the load-balance probe (tools/raster_trace.py) reads it. */
+int rcgs_raster_trace(uint32_t* d_trace, int64_t max_items);
 
 /* Measured FP32 FFMA throughput of this device in FLOP/s (2 per FFMA): the
  * denominator of the rasteriser's compute roofline. */

@@ -56,6 +56,7 @@ _SIGNATURES = {
     "rcgs_view_info_get": [c_void_p, P(ViewInfo)],
     "rcgs_view_destroy": [c_void_p, c_void_p],
     "rcgs_view_kept": [c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_view_ranges": [c_void_p, c_void_p, c_void_p],
     "rcgs_view_color": [c_void_p, c_void_p, c_void_p],
     "rcgs_render": [c_void_p, P(ctypes.c_float), c_int, c_void_p, c_void_p, c_void_p],
     "rcgs_depth": [c_void_p, c_double, c_void_p, c_void_p, c_void_p],
@@ -76,6 +77,7 @@ _SIGNATURES = {
     "rcgs_apply_recolor_f64": [c_void_p, c_void_p, c_i64, P(c_double), c_void_p, c_void_p],
     "rcgs_mask_hits": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_raster_counters": [c_void_p],
+    "rcgs_raster_trace": [c_void_p, c_i64],
     "rcgs_fp32_peak": [c_i32, P(c_double), c_void_p],
     "rcgs_pool_reserve": [c_i64, c_void_p],
 }

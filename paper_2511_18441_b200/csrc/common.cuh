@@ -143,4 +143,5 @@ struct rcgs_view {
     uint32_t* pair_s;     // (pairs,) rank s
     uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
     uint2* ranges;        // (tiles,) [start, end)
+    uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
 };

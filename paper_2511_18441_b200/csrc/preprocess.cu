@@ -323,6 +323,47 @@ __global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key,
     if (j == pairs - 1 || tile_key[j + 1] != t) ranges[t].y = (uint32_t)(j + 1);
 }
 
+// Raster work order: tiles by descending entry count (longest-processing-time
+// first).  The persistent raster warps pull items in this order, so the heavy
+// tiles start early and the tail of the launch is light tiles; in row-major order
+// a few dense tiles taken last kept one SM busy for the second half of the
+// launch.  Any order gives identical results (items are independent), so a
+// single-CTA bucket scatter on count / max * 255 is enough.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int ntiles,
+                                                          uint32_t* __restrict__ order) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_max;
+    const int t = threadIdx.x;
+    if (t < 256) hist[t] = 0;
+    if (t == 0) s_max = 1;
+    __syncthreads();
+    uint32_t mx = 0;
+    for (int i = t; i < ntiles; i += blockDim.x) {
+        const uint2 r = ranges[i];
+        mx = max(mx, r.y - r.x);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0) atomicMax(&s_max, mx);
+    __syncthreads();
+    const uint64_t m = s_max;
+    auto bucket = [&](int i) -> int {  // 0 = heaviest
+        const uint2 r = ranges[i];
+        return 255 - (int)(((uint64_t)(r.y - r.x) * 255u) / m);
+    };
+    for (int i = t; i < ntiles; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
+    __syncthreads();
+    if (t == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < 256; ++b) {
+            const uint32_t c = hist[b];
+            hist[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int i = t; i < ntiles; i += blockDim.x) order[atomicAdd(&hist[bucket(i)], 1u)] = (uint32_t)i;
+}
+
 // ---------------------------------------------------------------- colour (per step)
 // Per-step colour (render.py:209-214), iterated in scene order so the 192-byte SH
 // rows are read fully coalesced; the 16-byte result goes to the gaussian's
@@ -458,6 +499,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->pair_s, s);
     dfree(v->pair_e, s);
     dfree(v->ranges, s);
+    dfree(v->tile_order, s);
 }
 
 extern "C" int rcgs_view_destroy(rcgs_view* v, void* stream) {
@@ -614,6 +656,9 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&v->pair_s, pairs, s));
     k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pe, emit_s, pairs, v->ranges, v->pair_s);
     RCGS_LAUNCH_CHECK();
+    RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
+    tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order);
+    RCGS_LAUNCH_CHECK();
     v->pair_e = pe;
     dfree(pe_alt, s);
     dfree(tkey, s);
@@ -666,6 +711,13 @@ extern "C" int rcgs_view_kept(const rcgs_view* v, int64_t* d_index, double* d_de
     if (v->k == 0) return RCGS_OK;
     kept_export_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->gid, v->z, v->k, d_index, d_depth);
     RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_ranges(const rcgs_view* v, uint32_t* d_ranges, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_ranges != nullptr, "null argument");
+    RCGS_CUDA(cudaMemcpyAsync(d_ranges, v->ranges, sizeof(uint2) * (size_t)v->tiles_x * v->tiles_y,
+                              cudaMemcpyDeviceToDevice, as_stream(stream)));
     return RCGS_OK;
 }
 

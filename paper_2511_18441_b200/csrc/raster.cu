@@ -46,6 +46,7 @@ constexpr double kFixScale = 1125899906842624.0;  // 2^50
 
 struct RasterArgs {
     const uint2* ranges;
+    const uint32_t* tile_order;  // work order (nullptr: row-major)
     const uint32_t* pair_s;
     const RasterRec* rec;
     const ExactRec* exact;
@@ -72,6 +73,7 @@ struct RasterArgs {
     // pairs, composited pairs, warp blocks processed, warp blocks skipped,
     // warp-level entry iterations
     unsigned long long* counters;
+    uint32_t* trace;  // diagnostics: per work item {t0, t1, smid, iters, evals, exact, resync, tile}
     // HITS
     const uint8_t* mask;
     int32_t* hits;
@@ -86,6 +88,20 @@ struct RasterArgs {
 
 // Instrumentation: when set, raster launches accumulate work counters here.
 static unsigned long long* g_counters = nullptr;
+static uint32_t* g_trace = nullptr;
+static int64_t g_trace_items = 0;
+
+__device__ __forceinline__ uint32_t globaltimer_lo() {
+    uint32_t t;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
+    return t;
+}
+
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -116,14 +132,56 @@ __device__ __forceinline__ double exact_alpha_at(const ExactRec* __restrict__ ex
     return exact_alpha(exact[s], u, v, clamp, skip);
 }
 
-// Exact inclusive transmittance after list entries [j0, j1] (np.cumprod, render.py:278).
-__device__ __forceinline__ double exact_T(const ExactRec* __restrict__ exact,
-                                       const uint32_t* __restrict__ pair_s, uint32_t j0, uint32_t j1,
-                                       double u, double v, double clamp, double skip) {
+// fp32 cull power of a record at pixel (uf, vf) -- one expression shared by the
+// per-entry step and the exact re-walk, so both make the same gate decision.
+__device__ __forceinline__ float cull_power(const float4 ra, const float4 rb, const float4 rc, float uf, float vf) {
+    const float dx = (uf - ra.x) - rb.x;
+    const float dy = (vf - ra.y) - rb.y;
+    return fmaf(rc.x * dx, dx, fmaf(rc.z * dy, dy, rc.y * dx * dy));
+}
+
+// Exact inclusive transmittance of pixel (uf, vf) after list entries [j0, j1]
+// (np.cumprod, render.py:278), computed by the whole warp.  Entries below the
+// gate (power < p_lo: alpha is exactly 0 in fp64, the same test the per-entry
+// step trusts) contribute an exact factor 1 and are skipped; the remaining
+// (1 - alpha) factors are multiplied in list order, so every fp64 rounding is
+// the reference's.  32 lanes x 4 entries in flight per round instead of one
+// lane walking up to a few thousand entries with a dependent fp64 exp each
+// (those serial re-walks were the launch tail: one warp busy for 0.7 ms).
+__device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair_s,
+                                            const RasterRec* __restrict__ rec,
+                                            const ExactRec* __restrict__ exact, double clamp, double skip,
+                                            uint32_t j0, uint32_t j1, float uf, float vf, int lane) {
+    constexpr int kU = 2;
+    const double u = (double)uf, v = (double)vf;
     double T = 1.0;
-    for (uint32_t j = j0; j <= j1; ++j) {
-        const double al = exact_alpha(exact[pair_s[j]], u, v, clamp, skip);
-        T = __dmul_rn(T, __dsub_rn(1.0, al));
+    for (uint32_t c = j0; c <= j1; c += 32 * kU) {
+        uint32_t sv[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t j = c + q * 32 + lane;
+            sv[q] = j <= j1 ? pair_s[j] : 0xffffffffu;
+        }
+        bool live[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            live[q] = false;
+            if (sv[q] != 0xffffffffu) {
+                const RasterRec rr = rec[sv[q]];
+                live[q] = !(cull_power(rr.a, rr.b, rr.c, uf, vf) < rr.b.z);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            double om = 1.0;
+            if (live[q]) om = __dsub_rn(1.0, exact_alpha(exact[sv[q]], u, v, clamp, skip));
+            unsigned m = __ballot_sync(0xffffffffu, om != 1.0);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                T = __dmul_rn(T, __shfl_sync(0xffffffffu, om, b));
+                m &= m - 1;
+            }
+        }
     }
     return T;
 }
@@ -133,17 +191,17 @@ struct Pix {
     float T, E;  // fp32 transmittance and its relative error bound vs fp64
 };
 
-enum StepKind { SKIP = 0, COMPOSITE = 1, STOP = 2, CROSS = 3 };
+enum StepKind { SKIP = 0, COMPOSITE = 1, STOP = 2, CROSS = 3, AMBIG = 4 };
 
 // One (pixel, entry) step.  On COMPOSITE *w = alpha * T_before and the pixel
 // advances.  DEPTH returns CROSS at the first composited entry with T_inc < tau
-// (which is never after the stop entry, render.py:389-397).
+// (which is never after the stop entry, render.py:389-397).  When the fp32
+// transmittance and its error band straddle a threshold the step returns AMBIG
+// with *w set; the warp then resolves it with the exact transmittance (resolve).
 template <int M>
 __device__ __forceinline__ int step(const float4 ra, const float4 rb, const float4 rc, uint32_t s,
-                                    uint32_t j, uint32_t j0, Pix& px, const RasterArgs& a, float* w) {
-    const float dx = (px.uf - ra.x) - rb.x;
-    const float dy = (px.vf - ra.y) - rb.y;
-    const float power = fmaf(rc.x * dx, dx, fmaf(rc.z * dy, dy, rc.y * dx * dy));
+                                    Pix& px, const RasterArgs& a, float* w) {
+    const float power = cull_power(ra, rb, rc, px.uf, px.vf);
     if (power < rb.z) return SKIP;
     float alpha;
     if (power < rb.w) {
@@ -155,31 +213,34 @@ __device__ __forceinline__ int step(const float4 ra, const float4 rb, const floa
     }
     const float oma = 1.0f - alpha;  // >= 0.01 (alpha clamp)
     const float delta = fmaf(fabsf(power), rc.w + 2e-7f, 6e-7f);
-    float Tkeep = px.T * oma;
+    const float Tkeep = px.T * oma;
     // q = alpha / (1 - alpha) via one MUFU reciprocal (relative error ~1e-7, absorbed
     // by the 2x safety factor of the band below)
-    float Ekeep = fmaf(alpha * rcp_approx(oma), delta, px.E + 2.4e-7f);
-    double T64 = 0.0;
-    bool resynced = false;
-    // is the exact inclusive T below the threshold?  (fp32 test, fp64 when ambiguous)
-    auto below = [&](float thr_f, double thr_d) -> bool {
-        const float band = 2.0f * Ekeep * Tkeep;
-        if (Tkeep - band >= thr_f) return false;  // the common case first
-        if (Tkeep + band < thr_f) return true;
-        if (!resynced) {
-            T64 = exact_T(a.exact, a.pair_s, j0, j, (double)px.uf, (double)px.vf, a.alpha_clamp,
-                          a.alpha_skip);
-            Tkeep = (float)T64;
-            Ekeep = 1.2e-7f;
-            resynced = true;
-        }
-        return T64 < thr_d;
-    };
-    if (M == DEPTH && below(a.f_tau, a.tau)) return CROSS;
-    if (below(a.f_floor, a.t_floor)) return STOP;
+    const float Ekeep = fmaf(alpha * rcp_approx(oma), delta, px.E + 2.4e-7f);
+    // is the exact inclusive T below a threshold?  fp32 with its error band; the
+    // common case (clearly above) first
+    const float band = 2.0f * Ekeep * Tkeep;
     *w = alpha * px.T;
-    px.T = Tkeep;
-    px.E = Ekeep;
+    if (M == DEPTH) {
+        if (Tkeep + band < a.f_tau) return CROSS;
+        if (!(Tkeep - band >= a.f_tau)) return AMBIG;
+    }
+    if (Tkeep - band >= a.f_floor) {
+        px.T = Tkeep;
+        px.E = Ekeep;
+        return COMPOSITE;
+    }
+    if (Tkeep + band < a.f_floor) return STOP;
+    return AMBIG;
+}
+
+// Exact decision for an AMBIG step given the exact inclusive transmittance.
+template <int M>
+__device__ __forceinline__ int resolve(double T64, Pix& px, const RasterArgs& a) {
+    if (M == DEPTH && T64 < a.tau) return CROSS;
+    if (T64 < a.t_floor) return STOP;
+    px.T = (float)T64;
+    px.E = 1.2e-7f;
     return COMPOSITE;
 }
 
@@ -209,7 +270,8 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
         if (lane == 0) item = atomicAdd(a.counter, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (unsigned)a.n_items) break;
-        const int tile = (int)(item / kBlocksPerTile), blk = (int)(item % kBlocksPerTile);
+        const int tile = a.tile_order ? (int)a.tile_order[item / kBlocksPerTile] : (int)(item / kBlocksPerTile);
+        const int blk = (int)(item % kBlocksPerTile);
         const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
         const int bx0 = tx * kTile + (blk & 1) * 8, by0 = ty * kTile + (blk >> 1) * 4;
         const int u = bx0 + (lane & 7), v = by0 + (lane >> 3);
@@ -221,6 +283,7 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
         px.vf = (float)v;
         px.T = 1.0f;
         px.E = 0.0f;
+        uint32_t n_resync = 0;  // warp-uniform (trace launches)
         bool done = !inside;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
         int32_t cross = -1;
@@ -239,6 +302,7 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
                 continue;
             }
         }
+        if (a.trace && lane == 0) a.trace[8 * (int64_t)item] = globaltimer_lo();
         if (M == HITS && inside) done = a.mask[pix] == 0;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
@@ -271,12 +335,21 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
             for (int k = 0; k < n; ++k) {
                 float w = 0.f;
                 int r = SKIP;
-                if (a.counters) {
+                if (a.counters || a.trace) {
                     n_eval += !done;
                     ++n_iter;
                 }
+                if (!done) r = step<M>(st.a[k], st.b[k], st.c[k], st.s[k], px, a, &w);
+                // ambiguous threshold tests: exact transmittance, one pixel at a time, by the warp
+                for (unsigned amb = __ballot_sync(0xffffffffu, r == AMBIG); amb; amb &= amb - 1) {
+                    const int L = __ffs(amb) - 1;
+                    const float lu = __shfl_sync(0xffffffffu, px.uf, L), lv = __shfl_sync(0xffffffffu, px.vf, L);
+                    const double T64 = warp_exact_T(a.pair_s, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, range.x,
+                                                    st.j[k], lu, lv, lane);
+                    if (lane == L) r = resolve<M>(T64, px, a);
+                    ++n_resync;
+                }
                 if (!done) {
-                    r = step<M>(st.a[k], st.b[k], st.c[k], st.s[k], st.j[k], range.x, px, a, &w);
                     if (r == STOP) done = true;
                     if (r == CROSS) {
                         cross = (int32_t)st.s[k];
@@ -351,6 +424,21 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
                 atomicAdd(&a.counters[5 * M + 4], (unsigned long long)n_iter);
             }
         }
+        if (a.trace) {
+            uint32_t nv = n_eval;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+            if (lane == 0) {
+                uint32_t* tr = a.trace + 8 * (int64_t)item;
+                tr[1] = globaltimer_lo();
+                tr[2] = smid();
+                tr[3] = n_iter;
+                tr[4] = nv;
+                tr[5] = 0;
+                tr[6] = n_resync;
+                tr[7] = (uint32_t)tile;
+            }
+        }
         if (!inside) continue;
         if (M == FWD) {
             const float T = px.T;
@@ -379,6 +467,7 @@ static RasterArgs base_args(const rcgs_view* v) {
     RasterArgs a;
     memset(&a, 0, sizeof(a));
     a.ranges = v->ranges;
+    a.tile_order = v->tile_order;
     a.pair_s = v->pair_s;
     a.rec = v->rec;
     a.exact = v->exact;
@@ -416,6 +505,7 @@ static int launch(RasterArgs a, cudaStream_t s) {
     RCGS_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
     a.counter = counter;
     a.counters = g_counters;
+    a.trace = (g_trace && g_trace_items >= a.n_items) ? g_trace : nullptr;
     const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
     if (blocks > 0) raster_kernel<M><<<blocks, kCTA, 0, s>>>(a);
     dfree(counter, s);
@@ -426,6 +516,12 @@ static int launch(RasterArgs a, cudaStream_t s) {
 }  // namespace rcgs
 
 using namespace rcgs;
+
+extern "C" int rcgs_raster_trace(uint32_t* d_trace, int64_t max_items) {
+    g_trace = d_trace;
+    g_trace_items = d_trace ? max_items : 0;
+    return RCGS_OK;
+}
 
 extern "C" int rcgs_raster_counters(uint64_t* d_counters30) {
     g_counters = reinterpret_cast<unsigned long long*>(d_counters30);

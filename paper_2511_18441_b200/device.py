@@ -197,6 +197,13 @@ class View:
         N.call("rcgs_view_kept", self.handle, N.ptr(idx), N.ptr(z), stream_ptr())
         return idx[:self.n_kept], z[:self.n_kept]
 
+    def ranges(self) -> torch.Tensor:
+        """Per-tile [start, end) into the depth-ordered pair list, (tiles_y, tiles_x, 2)."""
+        out = torch.zeros((self.tiles[1], self.tiles[0], 2), dtype=torch.int32, device=device())
+        if self.n_pairs:
+            N.call("rcgs_view_ranges", self.handle, N.ptr(out), stream_ptr())
+        return out
+
     def backward(self, grad_image: torch.Tensor, acc=None, nonfinite=None) -> torch.Tensor:
         self._need_color()
         if tuple(grad_image.shape) != (self.height, self.width, 3):
