@@ -40,6 +40,10 @@ enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRIT
 
 constexpr int kWarpsPerCTA = 8;
 constexpr int kCTA = 32 * kWarpsPerCTA;
+#ifndef RCGS_RASTER_MIN_CTAS
+#define RCGS_RASTER_MIN_CTAS 4
+#endif
+constexpr int kMinCTAs = RCGS_RASTER_MIN_CTAS;  // resident CTAs per SM the register budget targets
 constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8x4 pixels
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kFixScale = 1125899906842624.0;  // 2^50
@@ -252,6 +256,33 @@ __device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float 
     return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 3.f;
 }
 
+// Can the footprint {power >= p_lo} reach any point of the rectangle
+// [x0, x1] x [y0, y1]?  Q = -power is a PSD quadratic of the offset from the mean;
+// its minimum over the box is 0 when the mean is inside, else it lies on an edge,
+// where the 1-D minimiser is a clamp.  The candidates' fp32 values are lowered by
+// their evaluation error bound (2e-6 of the absolute term sum, plus 1e-4), so the
+// test only drops entries whose power stays below the gate at every pixel of the
+// rectangle -- exactly those the per-pixel step would SKIP (alpha exactly 0 in
+// fp64) -- and the results do not change.  NaN keeps the entry.
+__device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const float4 rb, const float4 rc, float x0,
+                                                     float y0, float x1, float y1) {
+    const float X0 = (x0 - ra.x) - rb.x, X1 = (x1 - ra.x) - rb.x;
+    const float Y0 = (y0 - ra.y) - rb.y, Y1 = (y1 - ra.y) - rb.y;
+    if (X0 <= 0.f && X1 >= 0.f && Y0 <= 0.f && Y1 >= 0.f) return true;
+    const float A = -rc.x, B = -rc.y, C = -rc.z;
+    const float hA = __fdividef(-0.5f * B, A), hC = __fdividef(-0.5f * B, C);
+    auto lower = [&](float dx, float dy) {  // lower bound of Q(dx, dy)
+        const float xx = A * dx * dx, yy = C * dy * dy, xy = B * dx * dy;
+        return (xx + yy + xy) - fmaf(2e-6f, xx + yy + fabsf(xy), 1e-4f);
+    };
+    auto clampf = [](float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); };
+    float m = lower(X0, clampf(hC * X0, Y0, Y1));
+    m = fminf(m, lower(X1, clampf(hC * X1, Y0, Y1)));
+    m = fminf(m, lower(clampf(hA * Y0, X0, X1), Y0));
+    m = fminf(m, lower(clampf(hA * Y1, X0, X1), Y1));
+    return !(m > -rb.z);
+}
+
 struct WarpStage {
     float4 a[32], b[32], c[32];
     float4 col[32];
@@ -259,7 +290,7 @@ struct WarpStage {
 };
 
 template <int M>
-__global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
     __shared__ WarpStage stage_all[kWarpsPerCTA];
     const int lane = threadIdx.x & 31;
     WarpStage& st = stage_all[threadIdx.x >> 5];
@@ -314,18 +345,23 @@ __global__ void __launch_bounds__(kCTA, 5) raster_kernel(RasterArgs a) {
             const uint32_t j = c0 + lane;
             bool keep = false;
             uint32_t s = 0;
-            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
             if (j < range.y) {
                 s = a.pair_s[j];
                 ra = a.rec[s].a;
                 keep = touches_block(ra, fbx0, fby0);
+                if (keep) {
+                    rb = a.rec[s].b;
+                    rc = a.rec[s].c;
+                    keep = ellipse_touches_rect(ra, rb, rc, fbx0, fby0, fbx0 + 7.f, fby0 + 3.f);
+                }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = __popc(bal & lt_mask);
                 st.a[slot] = ra;
-                st.b[slot] = a.rec[s].b;
-                st.c[slot] = a.rec[s].c;
+                st.b[slot] = rb;
+                st.c[slot] = rc;
                 st.s[slot] = s;
                 st.j[slot] = j;
                 if (M == FWD) st.col[slot] = a.color[s];

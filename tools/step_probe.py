@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--sel-views", type=int, default=0, help="0 = all views")
     ap.add_argument("--cache-views", action="store_true")
+    ap.add_argument("--prefetch", type=int, default=0)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     cfg = bench.CONFIGS[a.config]
@@ -36,9 +37,17 @@ def main():
     sp = P.SelectionPass(ds, cams, gt)
     sp.run(pts, (1.0, 0.2, 0.2), indices=list(range(a.sel_views)) if a.sel_views else None)
     eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
-                      seed=7, cache_views=a.cache_views)
-    for _ in range(a.warmup + a.steps):
+                      seed=7, cache_views=a.cache_views, prefetch=a.prefetch)
+    for _ in range(a.warmup):
         eng.step()
+    torch.cuda.synchronize()
+    # the timed steps are bracketed by cudaProfilerStart/Stop: run ncu with
+    # --profile-from-start off to capture only them
+    torch.cuda.profiler.start()
+    for _ in range(a.steps):
+        eng.step()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     eng.drain()
     torch.cuda.synchronize()
     print("probe ok", eng.step_count())
