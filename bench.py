@@ -203,8 +203,6 @@ def run_gpu(args):
         eng.step()
     eng.drain()
     eng.stage_report(reset=True)
-    counters = torch.zeros(30, dtype=torch.int64, device=dev)
-    N.call("rcgs_raster_counters", N.ptr(counters))  # work counters over the timed steps
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -235,9 +233,18 @@ def run_gpu(args):
     step_ms = sync_max(e0.elapsed_time(e1), world) / args.steps
     per_step = np.array([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)])
     recs = eng.drain()
-    N.call("rcgs_raster_counters", None)
     live = eng.stage_report(reset=True)
-    cnt = counters.view(6, 5).cpu().numpy() / float(args.steps)  # per launch (one per step)
+    # raster work counters (instrumented kernel variant) over a few extra, untimed
+    # steps of the same trajectory: the timed steps run the uninstrumented kernels
+    ncnt = max(1, min(args.steps, 16))
+    counters = torch.zeros(30, dtype=torch.int64, device=dev)
+    N.call("rcgs_raster_counters", N.ptr(counters))
+    for _ in range(ncnt):
+        eng.step()
+    eng.drain()
+    N.call("rcgs_raster_counters", None)
+    eng.stage_report(reset=True)
+    cnt = counters.view(6, 5).cpu().numpy() / float(ncnt)  # per launch (one per step)
     if world > 1:
         torch.distributed.barrier()
 

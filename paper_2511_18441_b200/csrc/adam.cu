@@ -50,80 +50,175 @@ __global__ void adam_prep_kernel(const int64_t* __restrict__ step, double db1, d
     *inv = make_float2((float)(1.0 / (1.0 - pow(db1, t))), (float)(1.0 / (1.0 - pow(db2, t))));
 }
 
-// One thread per float4 of a gaussian's 48 coefficients (12 per gaussian, fully
-// coalesced SH / m / v traffic).  Each thread rebuilds the few SH basis rows it
-// needs in fp32 from the fp64 view direction (cheap next to the 96 bytes it
-// moves), so there is no shared-memory staging and no block barrier.
-__global__ void __launch_bounds__(256) adam_fused_kernel(
-    const double* __restrict__ pos, int64_t n, int deg, float4* __restrict__ sh, float4* __restrict__ m,
-    float4* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
+// SH basis rows 0..15 in fp32 along the unit direction (x, y, z) (render.py SH
+// constants; rows above `deg` are 0), written out branch-free.
+__device__ __forceinline__ void basis16_f32(float x, float y, float z, int deg, float r[16]) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float d1 = deg >= 1 ? 1.f : 0.f, d2 = deg >= 2 ? 1.f : 0.f, d3 = deg >= 3 ? 1.f : 0.f;
+    r[0] = 0.28209479177387814f;
+    r[1] = d1 * -0.4886025119029199f * y;
+    r[2] = d1 * 0.4886025119029199f * z;
+    r[3] = d1 * -0.4886025119029199f * x;
+    r[4] = d2 * 1.0925484305920792f * (x * y);
+    r[5] = d2 * -1.0925484305920792f * (y * z);
+    r[6] = d2 * 0.31539156525252005f * (2.f * zz - xx - yy);
+    r[7] = d2 * -1.0925484305920792f * (x * z);
+    r[8] = d2 * 0.5462742152960396f * (xx - yy);
+    r[9] = d3 * -0.5900435899266435f * y * (3.f * xx - yy);
+    r[10] = d3 * 2.890611442640554f * (x * y) * z;
+    r[11] = d3 * -0.4570457994644658f * y * (4.f * zz - xx - yy);
+    r[12] = d3 * 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    r[13] = d3 * -0.4570457994644658f * x * (4.f * zz - xx - yy);
+    r[14] = d3 * 1.445305721320277f * z * (xx - yy);
+    r[15] = d3 * -0.5900435899266435f * x * (xx - 3.f * yy);
+}
+
+// ---- bulk-copy (TMA) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RCGS_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra RCGS_WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+
+constexpr int kAG = 64;                     // gaussians per tile
+constexpr int kAThreads = 4 * kAG;          // 4 threads per gaussian, 12 coefficients each
+constexpr int kAStages = 2;                 // tiles in flight per CTA
+constexpr uint32_t kARow = 48 * 4;          // bytes of one gaussian's SH (or m, or v)
+constexpr uint32_t kATileBytes = kAG * kARow;
+constexpr size_t kASmem = (size_t)kAStages * 3 * kATileBytes + kAStages * sizeof(uint64_t);
+
+// Fused SH-gradient expansion + Adam over all N x 48 coefficients (optimize.py
+// Adam; recolor.py SH-only refit).  The step streams SH, m and v once each way
+// (1152 B per gaussian), so it is HBM bound: persistent CTAs pull 64-gaussian
+// tiles of all three arrays with bulk async copies (TMA) into a 2-stage shared
+// ring completed by mbarrier transaction counts, update them in shared memory
+// (4 threads per gaussian: the view direction and SH basis once per thread
+// instead of once per float4) and write them back with bulk stores, which read
+// the stage before it is refilled.  Element order, products and Adam formulas
+// are the per-element ones of adam4, so results are bit-identical to an
+// elementwise update.
+__global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
+    const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
+    float* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
     const int32_t* __restrict__ reject) {
     if (reject && *reject) return;
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;  // n * 12 < 2^32 (checked on host)
-    if (q >= (uint32_t)n * 12u) return;
-    const uint32_t g = q / 12u;
-    const int c4 = (int)(q - g * 12u);
-    const int k0 = (4 * c4) / 3;  // the 4 coefficients span rows k0 and k0 + 1 at most
-    // the 48 bytes of state this thread updates, loaded first (in flight during the
-    // basis math) with streaming hints: touched once per step, keep L2 for the raster
-    float4 p = __ldcs(sh + q), mm = __ldcs(m + q), vv = __ldcs(v + q);
-    const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
-    float gr[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int vi = 0; vi < views.n; ++vi) {
-        float x = (float)(px - views.cen[vi][0]), y = (float)(py - views.cen[vi][1]),
-              z = (float)(pz - views.cen[vi][2]);
-        const float inv = rsqrtf(x * x + y * y + z * z);
-        x *= inv;
-        y *= inv;
-        z *= inv;
-        // branch-free: every basis row in registers, then predicated selects of k0, k0 + 1
-        const float xx = x * x, yy = y * y, zz = z * z;
-        const float d1 = deg >= 1 ? 1.f : 0.f, d2 = deg >= 2 ? 1.f : 0.f, d3 = deg >= 3 ? 1.f : 0.f;
-        const float r0 = 0.28209479177387814f;
-        const float r1 = d1 * -0.4886025119029199f * y, r2 = d1 * 0.4886025119029199f * z;
-        const float r3 = d1 * -0.4886025119029199f * x;
-        const float r4 = d2 * 1.0925484305920792f * (x * y), r5 = d2 * -1.0925484305920792f * (y * z);
-        const float r6 = d2 * 0.31539156525252005f * (2.f * zz - xx - yy);
-        const float r7 = d2 * -1.0925484305920792f * (x * z), r8 = d2 * 0.5462742152960396f * (xx - yy);
-        const float r9 = d3 * -0.5900435899266435f * y * (3.f * xx - yy);
-        const float r10 = d3 * 2.890611442640554f * (x * y) * z;
-        const float r11 = d3 * -0.4570457994644658f * y * (4.f * zz - xx - yy);
-        const float r12 = d3 * 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
-        const float r13 = d3 * -0.4570457994644658f * x * (4.f * zz - xx - yy);
-        const float r14 = d3 * 1.445305721320277f * z * (xx - yy);
-        const float r15 = d3 * -0.5900435899266435f * x * (xx - 3.f * yy);
-#define RCGS_PICK(kk)                                                                           \
-    ((kk) == 0 ? r0 : (kk) == 1 ? r1 : (kk) == 2 ? r2 : (kk) == 3 ? r3 : (kk) == 4 ? r4 :         \
-     (kk) == 5 ? r5 : (kk) == 6 ? r6 : (kk) == 7 ? r7 : (kk) == 8 ? r8 : (kk) == 9 ? r9 :         \
-     (kk) == 10 ? r10 : (kk) == 11 ? r11 : (kk) == 12 ? r12 : (kk) == 13 ? r13 : (kk) == 14 ? r14 \
-                                                                                : (kk) == 15 ? r15 : 0.f)
-        const float b0 = RCGS_PICK(k0), b1 = RCGS_PICK(k0 + 1);
-#undef RCGS_PICK
-        const float* a = views.acc[vi] + 3 * (size_t)g;
-        const float a0 = a[0], a1 = a[1], a2 = a[2];
-        // element 4 c4 + j has row (4 c4 + j) / 3 and channel (4 c4 + j) % 3; c4 % 3
-        // fixes the pattern: 0 -> (k0: ch 0,1,2; k0+1: ch 0), 1 -> (k0: 1,2; k0+1: 0,1),
-        // 2 -> (k0: 2; k0+1: 0,1,2)
-        const int r = c4 % 3;
-        const float e0 = r == 0 ? b0 * a0 : (r == 1 ? b0 * a1 : b0 * a2);
-        const float e1 = r == 0 ? b0 * a1 : (r == 1 ? b0 * a2 : b1 * a0);
-        const float e2 = r == 0 ? b0 * a2 : (r == 1 ? b1 * a0 : b1 * a1);
-        const float e3 = r == 0 ? b1 * a0 : (r == 1 ? b1 * a1 : b1 * a2);
-        gr[0] += e0;
-        gr[1] += e1;
-        gr[2] += e2;
-        gr[3] += e3;
-    }
-    if (views.n > 1) {
-        const float invn = 1.0f / (float)views.n;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kAStages * 3 * kATileBytes);
+    const int t = threadIdx.x;
+    const int64_t ntiles = (n + kAG - 1) / kAG;
+    float* const arrays[3] = {sh, m, v};
+    auto stage_buf = [&](int s, int arr) -> float4* {
+        return reinterpret_cast<float4*>(smem + ((size_t)s * 3 + arr) * kATileBytes);
+    };
+    auto issue = [&](int64_t tile, int s) {  // one thread
+        const int64_t g0 = tile * kAG;
+        const uint32_t bytes = (uint32_t)(n - g0 < kAG ? n - g0 : kAG) * kARow;
+        const uint32_t bar = smem_addr(&bars[s]);
+        mbar_expect_tx(bar, 3 * bytes);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) gr[j] *= invn;
+        for (int arr = 0; arr < 3; ++arr)
+            bulk_load(smem_addr(stage_buf(s, arr)), arrays[arr] + g0 * 48, bytes, bar);
+    };
+    if (t == 0) {
+        for (int s = 0; s < kAStages; ++s) mbar_init(smem_addr(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        for (int s = 0; s < kAStages; ++s)
+            if ((int64_t)blockIdx.x + (int64_t)s * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
     }
     const float2 ibc = *bc;
-    adam4(p, mm, vv, gr, 4 * c4, h, ibc.x, ibc.y);
-    __stcs(sh + q, p);
-    __stcs(m + q, mm);
-    __stcs(v + q, vv);
+    const int gi = t >> 2, part = t & 3;  // gaussian in the tile, 12-coefficient quarter
+    const float invn = 1.0f / (float)views.n;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % kAStages;
+        const int64_t g0 = tile * kAG;
+        const int ng = (int)(n - g0 < kAG ? n - g0 : kAG);
+        mbar_wait(smem_addr(&bars[s]), (uint32_t)((it / kAStages) & 1));
+        if (gi < ng) {
+            const int64_t g = g0 + gi;
+            const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
+            float gr[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) gr[e] = 0.f;
+            for (int vi = 0; vi < views.n; ++vi) {
+                float x = (float)(px - views.cen[vi][0]), y = (float)(py - views.cen[vi][1]),
+                      z = (float)(pz - views.cen[vi][2]);
+                const float inv = rsqrtf(x * x + y * y + z * z);
+                x *= inv;
+                y *= inv;
+                z *= inv;
+                float r[16];
+                basis16_f32(x, y, z, deg, r);
+                // this thread's rows 4 part .. 4 part + 3 (branch-free selects)
+                float b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    b[q] = part == 0 ? r[q] : (part == 1 ? r[4 + q] : (part == 2 ? r[8 + q] : r[12 + q]));
+                const float* acc = views.acc[vi] + 3 * (size_t)g;
+                const float a3[3] = {acc[0], acc[1], acc[2]};
+#pragma unroll
+                for (int e = 0; e < 12; ++e) gr[e] += b[e / 3] * a3[e % 3];
+            }
+            if (views.n > 1) {
+#pragma unroll
+                for (int e = 0; e < 12; ++e) gr[e] *= invn;
+            }
+            float4* P = stage_buf(s, 0) + gi * 12 + part * 3;
+            float4* Mm = stage_buf(s, 1) + gi * 12 + part * 3;
+            float4* V = stage_buf(s, 2) + gi * 12 + part * 3;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                float4 p4 = P[q], m4 = Mm[q], v4 = V[q];
+                adam4(p4, m4, v4, &gr[4 * q], part * 12 + 4 * q, h, ibc.x, ibc.y);
+                P[q] = p4;
+                Mm[q] = m4;
+                V[q] = v4;
+            }
+        }
+        // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+            const uint32_t bytes = (uint32_t)ng * kARow;
+#pragma unroll
+            for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            const int64_t next = tile + (int64_t)kAStages * gridDim.x;
+            if (next < ntiles) {
+                // the stage is refilled only after the store has read it
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                issue(next, s);
+            }
+        }
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
@@ -204,9 +299,19 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
         float2* bc = nullptr;
         RCGS_TRY(dalloc(&bc, 1, s));
         adam_prep_kernel<<<1, 1, 0, s>>>(d_step, cfg->beta1, cfg->beta2, bc);
-        adam_fused_kernel<<<div_up(sc->n * 12, 256), 256, 0, s>>>(
-            sc->pos, sc->n, sc->sh_degree, reinterpret_cast<float4*>(d_sh), reinterpret_cast<float4*>(d_m),
-            reinterpret_cast<float4*>(d_v), av, hyper(cfg), bc, d_reject);
+        static int grid = 0;
+        if (grid == 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            RCGS_CUDA(cudaGetDevice(&dev));
+            RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            RCGS_CUDA(cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kASmem));
+            RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem));
+            grid = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        const int64_t ntiles = (sc->n + kAG - 1) / kAG;
+        adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
+            sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), bc, d_reject);
         RCGS_LAUNCH_CHECK();
         dfree(bc, s);
     }

@@ -289,7 +289,9 @@ struct WarpStage {
     uint32_t s[32], j[32];
 };
 
-template <int M>
+// kInstr: the instrumented variant (work counters / per-item trace); production
+// launches carry no counter registers or checks in the entry loop.
+template <int M, bool kInstr>
 __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
     __shared__ WarpStage stage_all[kWarpsPerCTA];
     const int lane = threadIdx.x & 31;
@@ -329,11 +331,11 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             // sum_p g_p w_ip has no term from this block when all its gradients are 0
             // (the recolor gradient is local to the edited region): skip the block
             if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) {
-                if (a.counters && lane == 0) atomicAdd(&a.counters[5 * M + 3], 1ull);
+                if (kInstr && a.counters && lane == 0) atomicAdd(&a.counters[5 * M + 3], 1ull);
                 continue;
             }
         }
-        if (a.trace && lane == 0) a.trace[8 * (int64_t)item] = globaltimer_lo();
+        if (kInstr && a.trace && lane == 0) a.trace[8 * (int64_t)item] = globaltimer_lo();
         if (M == HITS && inside) done = a.mask[pix] == 0;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             for (int k = 0; k < n; ++k) {
                 float w = 0.f;
                 int r = SKIP;
-                if (a.counters || a.trace) {
+                if (kInstr) {
                     n_eval += !done;
                     ++n_iter;
                 }
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                     }
                 }
                 const bool comp = (r == COMPOSITE);
-                if (a.counters) n_comp += comp;
+                if (kInstr) n_comp += comp;
                 if (M == FWD) {
                     if (comp) {
                         const float4 c = st.col[k];
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             __syncwarp();
         }
 
-        if (a.counters) {
+        if (kInstr && a.counters) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 atomicAdd(&a.counters[5 * M + 4], (unsigned long long)n_iter);
             }
         }
-        if (a.trace) {
+        if (kInstr && a.trace) {
             uint32_t nv = n_eval;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
@@ -533,7 +535,7 @@ static int launch(RasterArgs a, cudaStream_t s) {
         int dev = 0, sms = 0, per_sm = 0;
         RCGS_CUDA(cudaGetDevice(&dev));
         RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_kernel<M>, kCTA, 0));
+        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_kernel<M, false>, kCTA, 0));
         grid[M] = sms * (per_sm > 0 ? per_sm : 1);
     }
     unsigned* counter = nullptr;
@@ -543,7 +545,12 @@ static int launch(RasterArgs a, cudaStream_t s) {
     a.counters = g_counters;
     a.trace = (g_trace && g_trace_items >= a.n_items) ? g_trace : nullptr;
     const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
-    if (blocks > 0) raster_kernel<M><<<blocks, kCTA, 0, s>>>(a);
+    if (blocks > 0) {
+        if (a.counters || a.trace)
+            raster_kernel<M, true><<<blocks, kCTA, 0, s>>>(a);
+        else
+            raster_kernel<M, false><<<blocks, kCTA, 0, s>>>(a);
+    }
     dfree(counter, s);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
