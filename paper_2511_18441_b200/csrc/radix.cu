@@ -1,4 +1,4 @@
-// Stable LSD radix sort, onesweep style (hand-written; no CUB).
+// Stable LSD radix sort, reduce-then-scan (hand-written; no CUB).
 //
 // Used for (a) the global front-to-back order of the kept gaussians: a stable
 // sort of the fp64 view-space z bit patterns (positive doubles order like their
@@ -7,56 +7,130 @@
 // emitted in depth-rank order, so a stable sort on the tile id alone yields
 // (tile, depth) order.
 //
-// Per sort: one histogram kernel computes the global digit counts of EVERY
-// 8-bit pass at once, one single-block kernel scans them, then each pass is ONE
-// scatter kernel.  A scatter block takes the next 4096-item tile (dynamic id,
-// so predecessors are always resident or done), ranks its items stably
-// (each warp owns 512 consecutive items: match_any ranks + per-warp digit
-// counters, then a cross-warp prefix), and finds its per-digit global offset by
-// decoupled look-back over the preceding tiles' published (flag | count)
-// words.  Four block barriers per tile.
+// Each 8-bit pass is three kernels over 1024-item tiles, all tiles independent:
+//   upsweep    per-tile digit histogram (warp-aggregated shared atomics), also
+//              added into the pass's global digit totals
+//   scan       one block per digit: the digit's start (totals of the digits
+//              below it) + exclusive scan of its per-tile counts
+//              -> per-(digit, tile) offsets
+//   downsweep  stable in-tile ranking (each warp owns 128 consecutive items:
+//              ballot-built peer masks + per-warp digit counters, a cross-warp
+//              prefix), a local sort by digit in shared memory, and a
+//              write-out in which each digit's run is contiguous.
+// A single-kernel onesweep pass with decoupled look-back was latency bound here:
+// with every tile resident at once, inclusive prefixes propagate ~16 tiles per
+// L2 round trip, so a pass over 225-650 tiles took 30-70 us; these three
+// kernels have no inter-tile waiting.
 #include "common.cuh"
 
 namespace rcgs {
 
 constexpr int kRNT = 256;
 constexpr int kRWarps = kRNT / 32;
-constexpr int kRIPT = 16;
-constexpr int kRTile = kRNT * kRIPT;      // 4096 items per tile
-constexpr int kRPerWarp = kRTile / kRWarps; // 512 consecutive items per warp
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagPre = 2u << 30;
+constexpr int kRIPT = 4;
+constexpr int kRTile = kRNT * kRIPT;      // 1024 items per tile
+constexpr int kRPerWarp = kRTile / kRWarps; // 128 consecutive items per warp
 constexpr uint32_t kValMask = (1u << 30) - 1u;
 constexpr int kMaxPasses = 8;
 
-template <typename K>
-__global__ void __launch_bounds__(kRNT) radix_hist_all_kernel(const K* __restrict__ keys, int64_t n,
-                                                                int npass, int end_bit,
-                                                                uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kMaxPasses][256];
-    for (int i = threadIdx.x; i < kMaxPasses * 256; i += kRNT) (&h[0][0])[i] = 0;
-    __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * kRNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRNT) {
-        const K k = keys[i];
-        for (int p = 0; p < npass; ++p) {
-            const int bits = min(8, end_bit - 8 * p);
-            atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & ((1u << bits) - 1u)], 1u);
+// Lanes holding the same digit as this lane, among the lanes with `valid` set:
+// one ballot per digit bit.  match_any computes the same mask but is a slow
+// instruction on sm_100a (measured 9.7 us vs 6.2 us for a ranking pass over 909K
+// keys, tools/bench_radix.cu).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, int bits, bool valid) {
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b < bits) {
+            const uint32_t bit = (d >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
         }
     }
+    return peers;
+}
+
+// Per-tile digit histogram of one pass: hist[d * ntiles + tile].
+template <typename K>
+__global__ void __launch_bounds__(kRNT) radix_upsweep_kernel(const K* __restrict__ keys, int64_t n, int shift,
+                                                             uint32_t mask, uint32_t* __restrict__ tile_hist,
+                                                             int ntiles) {
+    __shared__ uint32_t h[256];
+    const int t = threadIdx.x;
+    h[t] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < npass * 256; i += kRNT) {
-        const uint32_t c = (&h[0][0])[i];
-        if (c) atomicAdd(&hist[i], c);
+    const int64_t base = (int64_t)blockIdx.x * kRTile;
+    K key[kRIPT];
+#pragma unroll
+    for (int r = 0; r < kRIPT; ++r) {
+        const int64_t i = base + r * kRNT + t;
+        key[r] = i < n ? keys[i] : K(0);
+    }
+#pragma unroll
+    for (int r = 0; r < kRIPT; ++r) {
+        const int64_t i = base + r * kRNT + t;
+        // plain shared atomics (same-address lanes are combined by the hardware): as
+        // fast as a copy here, unlike match_any aggregation
+        if (i < n) atomicAdd(&h[(uint32_t)(key[r] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    tile_hist[(int64_t)t * ntiles + blockIdx.x] = h[t];
+}
+
+// One block per digit d: rewrites d's row of per-tile counts as its exclusive
+// prefix (offsets within the digit) and stores the digit total.  The digit
+// starts (exclusive scan of the totals) are formed by each downsweep block.
+__global__ void __launch_bounds__(kRNT) radix_scan_kernel(uint32_t* __restrict__ tile_hist,
+                                                          uint32_t* __restrict__ totals, int ntiles) {
+    __shared__ uint32_t ws[kRWarps];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t d = blockIdx.x;
+    uint32_t* row = tile_hist + (int64_t)d * ntiles;
+    const int per = (ntiles + kRNT - 1) / kRNT;  // consecutive tiles per thread
+    const int lo = t * per, hi = min(ntiles, lo + per);
+    uint32_t sum = 0;
+    for (int i = lo; i < hi; ++i) sum += row[i];
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    uint32_t run = x - sum;
+    for (int w = 0; w < warp; ++w) run += ws[w];
+    if (t == kRNT - 1) totals[d] = run + sum;
+    for (int i = lo; i < hi; ++i) {
+        const uint32_t c = row[i];
+        row[i] = run;
+        run += c;
     }
 }
 
-// Exclusive scan of each pass's 256 global digit counts (one block).
-__global__ void radix_hist_scan_kernel(uint32_t* __restrict__ hist, int npass) {
+// Stable in-tile ranking, a local sort by digit in shared memory, then the
+// write-out: each digit's run of the tile goes to consecutive addresses at its
+// scanned offset (coalesced segments instead of one L2 transaction per item).
+template <typename K>
+__global__ void __launch_bounds__(kRNT) radix_downsweep_kernel(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, bool vals_are_index, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
+    const uint32_t* __restrict__ totals, uint32_t nbins, int ntiles) {
+    const int bits = 31 - __clz(nbins);
+    __shared__ uint32_t wcnt[kRWarps][256];
+    __shared__ uint32_t s_base[256];   // global offset of digit d for this tile
+    __shared__ uint32_t s_start[256];  // first local slot of digit d
     __shared__ uint32_t ws[kRWarps];
+    __shared__ K sk[kRTile];
+    __shared__ uint32_t sv[kRTile];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    for (int p = 0; p < npass; ++p) {
-        const uint32_t v = hist[p * 256 + t];
-        uint32_t x = v;
+    const uint32_t tile = blockIdx.x;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) wcnt[w][t] = 0;
+    {
+        // digit start = exclusive scan of the digit totals (one digit per thread)
+        const uint32_t tot = (uint32_t)t < nbins ? totals[t] : 0u;
+        uint32_t x = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -64,34 +138,19 @@ __global__ void radix_hist_scan_kernel(uint32_t* __restrict__ hist, int npass) {
         }
         if (lane == 31) ws[warp] = x;
         __syncthreads();
-        uint32_t off = 0;
-        for (int w = 0; w < warp; ++w) off += ws[w];
-        hist[p * 256 + t] = off + x - v;
-        __syncthreads();
+        uint32_t st = x - tot;
+        for (int w = 0; w < warp; ++w) st += ws[w];
+        s_base[t] = (uint32_t)t < nbins ? st + offs[(int64_t)t * ntiles + tile] : 0u;
     }
-}
-
-template <typename K>
-__global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
-    const K* __restrict__ kin, const uint32_t* __restrict__ vin, bool vals_are_index, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, int64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ gstart,
-    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t wcnt[kRWarps][256];
-    __shared__ uint32_t s_base[256];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    if (t == 0) s_tile = atomicAdd(tile_counter, 1u);
-#pragma unroll
-    for (int w = 0; w < kRWarps; ++w) wcnt[w][t] = 0;
     __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t wbase = (int64_t)tile * kRTile + (int64_t)warp * kRPerWarp;
+    const int64_t tbase = (int64_t)tile * kRTile;
+    const int64_t wbase = tbase + (int64_t)warp * kRPerWarp;
+    const int tn = (int)(n - tbase < kRTile ? n - tbase : kRTile);
     const uint32_t lt = (1u << lane) - 1u;
 
     K key[kRIPT];
     uint32_t val[kRIPT];
     uint32_t rank[kRIPT];
-    // all 16 coalesced loads first (independent, in flight together) ...
 #pragma unroll
     for (int r = 0; r < kRIPT; ++r) {
         const int64_t i = wbase + r * 32 + lane;
@@ -99,13 +158,12 @@ __global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
         key[r] = valid ? kin[i] : K(0);
         val[r] = valid ? (vals_are_index ? (uint32_t)i : vin[i]) : 0u;
     }
-    // ... then the stable warp-level ranking
 #pragma unroll
     for (int r = 0; r < kRIPT; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         const bool valid = i < n;
-        const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & mask) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & mask) : 0u;
+        const uint32_t peers = digit_peers(d, bits, valid);
         const uint32_t before = valid ? wcnt[warp][d] : 0u;
         __syncwarp();
         rank[r] = before + __popc(peers & lt);
@@ -113,7 +171,8 @@ __global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
         __syncwarp();
     }
     __syncthreads();
-    // cross-warp exclusive prefix (digit t) and this tile's total for digit t
+    // digit t: cross-warp exclusive offsets, tile total, then the tile-level
+    // exclusive prefix over digits (block scan, one digit per thread)
     uint32_t total = 0;
 #pragma unroll
     for (int w = 0; w < kRWarps; ++w) {
@@ -121,41 +180,38 @@ __global__ void __launch_bounds__(kRNT) radix_onesweep_kernel(
         wcnt[w][t] = total;
         total += c;
     }
-    // decoupled look-back over the preceding tiles for digit t
-    volatile uint32_t* st = status;
-    uint32_t excl = 0;
-    if (tile == 0) {
-        st[t] = kFlagPre | total;
-    } else {
-        st[(int64_t)tile * 256 + t] = kFlagAgg | total;
-        // walk back in batches of 16 independent loads (memory-level parallelism
-        // instead of one dependent L2 round trip per predecessor)
-        constexpr int kLB = 16;
-        bool found = false;
-        for (int64_t hi = (int64_t)tile - 1; hi >= 0 && !found; hi -= kLB) {
-            uint32_t w[kLB];
+    uint32_t x = total;
 #pragma unroll
-            for (int b = 0; b < kLB; ++b) w[b] = hi - b >= 0 ? st[(hi - b) * 256 + t] : (2u << 30);
-#pragma unroll
-            for (int b = 0; b < kLB; ++b) {
-                if (found || hi - b < 0) continue;
-                while ((w[b] >> 30) == 0) w[b] = st[(hi - b) * 256 + t];
-                excl += w[b] & kValMask;
-                if ((w[b] >> 30) == 2) found = true;
-            }
-        }
-        st[(int64_t)tile * 256 + t] = kFlagPre | (excl + total);
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
-    s_base[t] = gstart[t] + excl;
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    uint32_t pre = x - total;
+    for (int w = 0; w < warp; ++w) pre += ws[w];
+    s_start[t] = pre;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kRIPT; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         if (i < n) {
             const uint32_t d = (uint32_t)(key[r] >> shift) & mask;
-            const uint32_t pos = s_base[d] + wcnt[warp][d] + rank[r];
-            kout[pos] = key[r];
-            vout[pos] = val[r];
+            const uint32_t lp = s_start[d] + wcnt[warp][d] + rank[r];
+            sk[lp] = key[r];
+            sv[lp] = val[r];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRIPT; ++r) {
+        const int i = r * kRNT + t;
+        if (i < tn) {
+            const K kk = sk[i];
+            const uint32_t d = (uint32_t)(kk >> shift) & mask;
+            const uint32_t pos = s_base[d] + (uint32_t)i - s_start[d];
+            kout[pos] = kk;
+            vout[pos] = sv[i];
         }
     }
 }
@@ -168,26 +224,25 @@ static int radix_sort(K** key_cur, K** key_alt, uint32_t** val_cur, uint32_t** v
     const int npass = (end_bit + 7) / 8;
     RCGS_CHECK_ARG(npass <= kMaxPasses, "radix sort: %d key bits", end_bit);
     const int64_t ntiles = (n + kRTile - 1) / kRTile;
-    // one zeroed scratch: global histograms, per-pass tile counters, per-pass status words
-    const int64_t words = (int64_t)npass * 256 + npass + (int64_t)npass * ntiles * 256;
+    // scratch: per-pass flagged digit totals + counters (zeroed), one (digit, tile) table
+    const int64_t words = (int64_t)npass * 256 + 256 * ntiles;
     uint32_t* scratch = nullptr;
     RCGS_TRY(dalloc(&scratch, words, s));
-    RCGS_CUDA(cudaMemsetAsync(scratch, 0, words * sizeof(uint32_t), s));
-    uint32_t* hist = scratch;
-    uint32_t* counters = hist + npass * 256;
-    uint32_t* status = counters + npass;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = (n + kRNT - 1) / kRNT;
-    const int hblocks = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
-    radix_hist_all_kernel<K><<<hblocks, kRNT, 0, s>>>(*key_cur, n, npass, end_bit, hist);
-    radix_hist_scan_kernel<<<1, 256, 0, s>>>(hist, npass);
+    uint32_t* totals = scratch;
+    uint32_t* table = totals + npass * 256;
+    // digits split evenly over the passes (e.g. 13 bits -> 7 + 6): fewer, longer
+    // runs per tile in the write-out
+    const int per_pass = (end_bit + npass - 1) / npass;
+    int shift = 0;
     for (int p = 0; p < npass; ++p) {
-        const int bits = min(8, end_bit - 8 * p);
-        radix_onesweep_kernel<K><<<(unsigned)ntiles, kRNT, 0, s>>>(
-            *key_cur, *val_cur, p == 0 && vals_are_index, *key_alt, *val_alt, n, 8 * p, (1u << bits) - 1u,
-            hist + p * 256, status + (int64_t)p * ntiles * 256, counters + p);
+        const int bits = min(per_pass, end_bit - shift);
+        const uint32_t mask = (1u << bits) - 1u;
+        radix_upsweep_kernel<K><<<(unsigned)ntiles, kRNT, 0, s>>>(*key_cur, n, shift, mask, table, (int)ntiles);
+        radix_scan_kernel<<<1u << bits, kRNT, 0, s>>>(table, totals + p * 256, (int)ntiles);
+        radix_downsweep_kernel<K><<<(unsigned)ntiles, kRNT, 0, s>>>(*key_cur, *val_cur, p == 0 && vals_are_index,
+                                                                      *key_alt, *val_alt, n, shift, mask, table,
+                                                                      totals + p * 256, 1u << bits, (int)ntiles);
+        shift += bits;
         K* tk = *key_cur;
         *key_cur = *key_alt;
         *key_alt = tk;
