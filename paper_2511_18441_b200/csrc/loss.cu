@@ -30,6 +30,10 @@ constexpr int kLT = 32;            // output tile edge
 constexpr int kLH = kLT + 2 * kR;  // 42
 constexpr int kRows = 4;           // output rows per thread in the vertical pass
 constexpr int kLNT = 256;          // = kLT * kLT / kRows
+#ifndef RCGS_LOSS_CTAS
+#define RCGS_LOSS_CTAS 3
+#endif
+constexpr int kLossCTAs = RCGS_LOSS_CTAS;  // resident CTAs per SM the filter passes target
 
 struct Window {
     double w[kWin];
@@ -120,20 +124,24 @@ __device__ __forceinline__ bool near_dirty(const uint8_t* __restrict__ dirty, in
 }
 
 // ---------------------------------------------------------------- pass A
-template <bool SSIM, typename T>
-__global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
-                                                    int W, Window win, double* __restrict__ maps,
+template <bool SSIM, typename T, typename MT>
+__global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
+                                                    int W, Window win, MT* __restrict__ maps,
                                                     double* __restrict__ block_part,
                                                     const uint8_t* __restrict__ dirty) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* iy = reinterpret_cast<double*>(smem_raw);  // [42][42]
-    double* ig = iy + kLH * kLH;                       // [42][42]
-    double* hs = ig + kLH * kLH;                       // [5][42][32]
+    // input planes in the input type (exact), horizontal sums in fp64
+    double* hs = reinterpret_cast<double*>(smem_raw);  // [5][42][32]
+    T* iy = reinterpret_cast<T*>(hs + 5 * kLH * kLT);  // [42][42]
+    T* ig = iy + kLH * kLH;                            // [42][42]
     __shared__ double red[2 * kLNT / 32];
+    __shared__ double mrow[kLT], mcol[kLT];  // in-image kernel mass per output row / column
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
     const int c = t % kLT, r0 = (t / kLT) * kRows;
+    if (SSIM && t < kLT) mrow[t] = mass1d(win, y0 + t, H);
+    if (SSIM && t >= kLT && t < 2 * kLT) mcol[t - kLT] = mass1d(win, x0 + t - kLT, W);
 
     // Blocks more than two blocks from any difference: L1 = 0 and the SSIM map is
     // exactly 1 (a1 == b1, a2 == b2 bitwise when y == g over the window); their
@@ -150,6 +158,12 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
     }
 
     double l1 = 0.0, ss = 0.0;
+    double inv_mass[kRows];  // 1 / (kernel mass in the image), per output pixel, all channels
+    if (SSIM) {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) inv_mass[i] = 1.0 / (mrow[r0 + i] * mcol[c]);
+    }
     for (int ch = 0; ch < 3; ++ch) {
         if (SSIM) {
             for (int i = t; i < kLH * kLH; i += kLNT) {
@@ -157,8 +171,8 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
                 const int gy = y0 - kR + r, gx = x0 - kR + cc;
                 const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
                 const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
-                iy[i] = in ? (double)y[gi] : 0.0;
-                ig[i] = in ? (double)g[gi] : 0.0;
+                iy[i] = in ? y[gi] : T(0);
+                ig[i] = in ? g[gi] : T(0);
             }
             __syncthreads();
             for (int i = t; i < kLH * kLT; i += kLNT) {
@@ -167,7 +181,7 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
 #pragma unroll
                 for (int k = 0; k < kWin; ++k) {
                     const int o = r * kLH + cc + k;
-                    const double a = iy[o], b = ig[o], w = win.w[k];
+                    const double a = (double)iy[o], b = (double)ig[o], w = win.w[k];
                     s1 = fma(w, a, s1);
                     s2 = fma(w, b, s2);
                     s11 = fma(w, a * a, s11);
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
             l1 += fabs((double)fy - (double)fg);
             if (SSIM) {
                 // three fp64 reciprocals replace the reference's divisions (same formulas)
-                const double im = 1.0 / (mass1d(win, gy, H) * mass1d(win, gx, W));
+                const double im = inv_mass[i];
                 const double mu1 = m[0][i] * im, mu2 = m[1][i] * im;
                 const double var1 = m[2][i] * im - mu1 * mu1;
                 const double var2 = m[3][i] * im - mu2 * mu2;
@@ -212,9 +226,9 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
                 const double d_cov = 2.0 * a1 * ib;
                 // channel-planar maps ([map][ch][pixel]) keep pass B's halo loads coalesced
                 const int64_t mo = (int64_t)ch * npix + (int64_t)gy * W + gx;
-                maps[mo] = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im;
-                maps[npix * 3 + mo] = d_var1 * im;
-                maps[2 * npix * 3 + mo] = d_cov * im;
+                maps[mo] = (MT)((d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im);
+                maps[npix * 3 + mo] = (MT)(d_var1 * im);
+                maps[2 * npix * 3 + mo] = (MT)(d_cov * im);
             }
         }
         if (SSIM) __syncthreads();  // shared planes are reused by the next channel
@@ -228,15 +242,15 @@ __global__ void __launch_bounds__(kLNT) loss_pass_a(const T* __restrict__ y, con
 }
 
 // ---------------------------------------------------------------- pass B
-template <bool SSIM, typename T, typename G>
-__global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
+template <bool SSIM, typename T, typename G, typename MT>
+__global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
                                                     int W, Window win, double lam,
-                                                    const double* __restrict__ maps,
+                                                    const MT* __restrict__ maps,
                                                     const int32_t* __restrict__ differ,
                                                     const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* im = reinterpret_cast<double*>(smem_raw);  // [3][42][42]
-    double* hs = im + 3 * kLH * kLH;                   // [3][42][32]
+    double* hs = reinterpret_cast<double*>(smem_raw);  // [3][42][32]
+    MT* im = reinterpret_cast<MT*>(hs + 3 * kLH * kLT); // [3][42][42]
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
@@ -253,7 +267,7 @@ __global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, 
                 const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
                 const int64_t gi = (int64_t)ch * npix + (int64_t)gy * W + gx;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) im[q * kLH * kLH + i] = in ? maps[q * npix * 3 + gi] : 0.0;
+                for (int q = 0; q < 3; ++q) im[q * kLH * kLH + i] = in ? maps[q * npix * 3 + gi] : MT(0);
             }
             __syncthreads();
             for (int i = t; i < kLH * kLT; i += kLNT) {
@@ -262,7 +276,8 @@ __global__ void __launch_bounds__(kLNT, 2) loss_pass_b(const T* __restrict__ y, 
                 for (int q = 0; q < 3; ++q) {
                     double s = 0.0;
 #pragma unroll
-                    for (int k = 0; k < kWin; ++k) s = fma(win.w[k], im[q * kLH * kLH + r * kLH + cc + k], s);
+                    for (int k = 0; k < kWin; ++k)
+                        s = fma(win.w[k], (double)im[q * kLH * kLH + r * kLH + cc + k], s);
                     hs[q * kLH * kLT + i] = s;
                 }
             }
@@ -328,7 +343,10 @@ static Window make_window() {
 
 using namespace rcgs;
 
-template <typename T, typename G>
+// MT: storage type of the three gradient maps between the passes -- fp64 for the
+// fp64 entry point, fp32 when the gradient itself is fp32 (halves the maps'
+// write + halo-read traffic; every filter sum and the SSIM algebra stay fp64).
+template <typename T, typename G, typename MT>
 static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, int32_t width, double lam,
                           double* d_loss3, G* d_grad, void* stream) {
     RCGS_CHECK_ARG(d_image && d_target && d_loss3 && d_grad, "null argument");
@@ -341,7 +359,8 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     const dim3 grid(div_up(width, kLT), div_up(height, kLT));
     const int nb = grid.x * grid.y;
     const int64_t npix = (int64_t)height * width;
-    double *maps = nullptr, *part = nullptr;
+    MT* maps = nullptr;
+    double* part = nullptr;
     int32_t* differ = nullptr;
     uint8_t* dirty = nullptr;
     RCGS_TRY(dalloc(&part, 2 * nb, s));
@@ -349,26 +368,28 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     RCGS_TRY(dalloc(&dirty, nb, s));
     RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
     loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty, differ);
-    const size_t smem_a = (2 * kLH * kLH + 5 * kLH * kLT) * sizeof(double);
-    const size_t smem_b = (3 * kLH * kLH + 3 * kLH * kLT) * sizeof(double);
+    const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
+    const size_t smem_b = 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
-        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
-        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-        loss_pass_a<true, T><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, dirty);
+        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_a));
+        RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_b));
+        loss_pass_a<true, T, MT><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, dirty);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
-            loss_pass_b<true, T, G><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                               differ, dirty, d_grad);
+            loss_pass_b<true, T, G, MT><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                                   differ, dirty, d_grad);
         } else {
-            loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps, differ,
-                                                           dirty, d_grad);
+            loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
+                                                               differ, dirty, d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
-        loss_pass_a<false, T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, dirty);
-        loss_pass_b<false, T, G><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr, differ,
-                                                       dirty, d_grad);
+        loss_pass_a<false, T, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, dirty);
+        loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr,
+                                                           differ, dirty, d_grad);
         RCGS_LAUNCH_CHECK();
     }
     loss_pass_c<<<1, kLNT, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
@@ -382,10 +403,10 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
 
 extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height, int32_t width,
                               double lam, double* d_loss3, float* d_grad, void* stream) {
-    return loss_grad_impl<float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
+    return loss_grad_impl<float, float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
 }
 
 extern "C" int rcgs_loss_grad_f64(const double* d_image, const double* d_target, int32_t height,
                                   int32_t width, double lam, double* d_loss3, double* d_grad, void* stream) {
-    return loss_grad_impl<double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
+    return loss_grad_impl<double, double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
 }
