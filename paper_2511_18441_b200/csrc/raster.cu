@@ -415,17 +415,20 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 } else if (M == BWD) {
                     float v0 = comp ? w * g0 : 0.f, v1 = comp ? w * g1 : 0.f, v2 = comp ? w * g2 : 0.f;
                     if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-                            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-                            v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-                        }
-                        if (lane < 3) {
-                            const float val = lane == 0 ? v0 : (lane == 1 ? v1 : v2);
+                        // transposed reduce-scatter of (v0, v1, v2, 0) over the warp: 6
+                        // shuffles instead of 15; channel c ends summed in lanes 8c..8c+7
+                        const bool h16 = lane & 16, h8 = lane & 8;
+                        const float ra = __shfl_xor_sync(0xffffffffu, h16 ? v0 : v2, 16);
+                        const float rb = __shfl_xor_sync(0xffffffffu, h16 ? v1 : 0.f, 16);
+                        const float ka = (h16 ? v2 : v0) + ra, kb = (h16 ? 0.f : v1) + rb;
+                        float val = (h8 ? kb : ka) + __shfl_xor_sync(0xffffffffu, h8 ? ka : kb, 8);
+                        val += __shfl_xor_sync(0xffffffffu, val, 4);
+                        val += __shfl_xor_sync(0xffffffffu, val, 2);
+                        val += __shfl_xor_sync(0xffffffffu, val, 1);
+                        if ((lane & 7) == 0 && lane < 24) {
                             if (isfinite(val)) {
                                 const long long q = llrint((double)val * kFixScale);
-                                atomicAdd(&a.acc_fx[3 * (int64_t)st.s[k] + lane], (unsigned long long)q);
+                                atomicAdd(&a.acc_fx[3 * (int64_t)st.s[k] + (lane >> 3)], (unsigned long long)q);
                             } else if (a.nonfinite) {
                                 atomicOr(a.nonfinite, 1);
                             }
