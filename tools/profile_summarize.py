@@ -1,0 +1,62 @@
+"""Summaries for profiles/ from tools/profile_round.sh outputs:
+profiles/<tag>_launches.txt (launch list by kernel), profiles/<tag>_ncu_step.md
+(ncu --set full table), profiles/traffic.json (DRAM bytes per launch per bench
+stage, read by bench.py for roofline.traffic).
+
+    python tools/profile_summarize.py r01
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import launch_summary  # noqa: E402
+import ncu_summary  # noqa: E402
+
+STAGES = {  # bench stage -> kernel name prefixes (ncu "Kernel Name" without args)
+    "raster_fwd": ["void rcgs::raster_kernel<0,", "rcgs::raster_kernel<0,"],
+    "raster_bwd": ["void rcgs::raster_kernel<2,", "rcgs::raster_kernel<2,", "bwd_finish_kernel"],
+    "adam": ["rcgs::adam_prep_kernel", "rcgs::adam_fused_kernel", "rcgs::step_commit_kernel"],
+    "color": ["rcgs::color_kernel"],
+    "loss_grad": ["void rcgs::loss_", "rcgs::loss_"],
+}
+
+
+def stage_of(name):
+    for st, prefixes in STAGES.items():
+        if any(name.startswith(p) for p in prefixes):
+            return st
+    return "view_build"
+
+
+def main(tag, outdir="profiles"):
+    os.makedirs(outdir, exist_ok=True)
+    launch_summary.main("gpurun_out/launches.csv", f"{outdir}/{tag}_launches.txt")
+    ncu_summary.main("gpurun_out/step_full.ncu-rep", f"{outdir}/{tag}_ncu_step.md")
+    raw = subprocess.run(["ncu", "-i", "gpurun_out/step_full.ncu-rep", "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    agg = {}
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0]
+        st = stage_of(name)
+        b = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(key)
+            b += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+        agg.setdefault(st, 0.0)
+        agg[st] += b
+    out = {"source": f"ncu --set full (default cache control), one optimizer step of C3: profiles/{tag}_ncu_step.md",
+           "stages": {k: {"dram_bytes_per_launch": int(v)} for k, v in agg.items()}}
+    with open(f"{outdir}/traffic.json", "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else "profiles")
