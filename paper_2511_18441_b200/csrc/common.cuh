@@ -115,8 +115,8 @@ struct __align__(16) RasterRec {
     float4 a;  // mx_hi, my_hi, half2(ex, ey) bits, opacity
     float4 b;  // mx_lo, my_lo, p_lo, p_hi     (mean2d = hi + lo; skip if power < p_lo,
                //                               exact fp64 check in [p_lo, p_hi))
-    float4 c;  // -a/2, -b, -c/2, kappa        (power = nha dx^2 + nb dx dy + nhc dy^2;
-               //                               kappa = relative power-error coefficient)
+    float4 c;  // -a/2, -b, -c/2, kappa + 2e-7  (power = nha dx^2 + nb dx dy + nhc dy^2;
+               //                                kappa = relative power-error coefficient)
 };
 
 // Exact (fp64) record for guarded decisions: the reference's own operands.

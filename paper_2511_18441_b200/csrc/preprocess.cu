@@ -273,7 +273,8 @@ __global__ void k1_record_kernel(const ProjF64* __restrict__ proj, const double*
     r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
     r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
                       (float)(P + margin));
-    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)kappa);
+    // c.w = kappa + 2e-7: the raster's per-composite error term |power| c.w + 6e-7
+    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)(kappa + 2e-7));
     rec[s] = r;
 
     Rect rc;

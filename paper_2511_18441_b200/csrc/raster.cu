@@ -192,7 +192,7 @@ __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair
 
 struct Pix {
     float uf, vf;
-    float T, E;  // fp32 transmittance and its relative error bound vs fp64
+    float T, A;  // fp32 transmittance and its absolute error bound vs the fp64 product
 };
 
 enum StepKind { SKIP = 0, COMPOSITE = 1, STOP = 2, CROSS = 3, AMBIG = 4 };
@@ -216,25 +216,28 @@ __device__ __forceinline__ int step(const float4 ra, const float4 rb, const floa
         alpha = fminf(a.f_alpha_clamp, ra.w * ex2_approx(power * kLog2e));
     }
     const float oma = 1.0f - alpha;  // >= 0.01 (alpha clamp)
-    const float delta = fmaf(fabsf(power), rc.w + 2e-7f, 6e-7f);
+    // relative error of (1 - alpha): q * delta with q = alpha / (1 - alpha) and
+    // delta = |power| (kappa + 2e-7) + 6e-7 (rc.w holds kappa + 2e-7).  Tracked as
+    // the absolute bound A = E * T: E' = E + q delta + 2.4e-7 becomes
+    // A' = A (1 - alpha) + w delta + 2.4e-7 T'  (q T' = alpha T = w), no reciprocal;
+    // its own fp32 rounding is absorbed by the 2x band below.
+    const float delta = fmaf(fabsf(power), rc.w, 6e-7f);
     const float Tkeep = px.T * oma;
-    // q = alpha / (1 - alpha) via one MUFU reciprocal (relative error ~1e-7, absorbed
-    // by the 2x safety factor of the band below)
-    const float Ekeep = fmaf(alpha * rcp_approx(oma), delta, px.E + 2.4e-7f);
+    const float wgt = alpha * px.T;
+    const float Akeep = fmaf(px.A, oma, fmaf(wgt, delta, 2.4e-7f * Tkeep));
+    *w = wgt;
     // is the exact inclusive T below a threshold?  fp32 with its error band; the
     // common case (clearly above) first
-    const float band = 2.0f * Ekeep * Tkeep;
-    *w = alpha * px.T;
     if (M == DEPTH) {
-        if (Tkeep + band < a.f_tau) return CROSS;
-        if (!(Tkeep - band >= a.f_tau)) return AMBIG;
+        if (fmaf(2.0f, Akeep, Tkeep) < a.f_tau) return CROSS;
+        if (!(fmaf(-2.0f, Akeep, Tkeep) >= a.f_tau)) return AMBIG;
     }
-    if (Tkeep - band >= a.f_floor) {
+    if (fmaf(-2.0f, Akeep, Tkeep) >= a.f_floor) {
         px.T = Tkeep;
-        px.E = Ekeep;
+        px.A = Akeep;
         return COMPOSITE;
     }
-    if (Tkeep + band < a.f_floor) return STOP;
+    if (fmaf(2.0f, Akeep, Tkeep) < a.f_floor) return STOP;
     return AMBIG;
 }
 
@@ -244,7 +247,7 @@ __device__ __forceinline__ int resolve(double T64, Pix& px, const RasterArgs& a)
     if (M == DEPTH && T64 < a.tau) return CROSS;
     if (T64 < a.t_floor) return STOP;
     px.T = (float)T64;
-    px.E = 1.2e-7f;
+    px.A = 1.2e-7f * px.T;
     return COMPOSITE;
 }
 
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
         px.uf = (float)u;
         px.vf = (float)v;
         px.T = 1.0f;
-        px.E = 0.0f;
+        px.A = 0.0f;
         uint32_t n_resync = 0;  // warp-uniform (trace launches)
         bool done = !inside;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
