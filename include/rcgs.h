@@ -176,6 +176,15 @@ int rcgs_adam_fused(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v
                     const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                     const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
                     void* stream);
+/* rcgs_adam_fused + the colour pass of `next_view` (the view the next optimizer
+ * step renders, render.py:209-214) evaluated from the updated SH tiles while they
+ * are in shared memory: saves the colour kernel's full SH read.  Equivalent to
+ * rcgs_adam_fused followed by rcgs_view_color(next_view, d_sh) (bit-identical),
+ * including on a rejected step (SH unchanged, view still coloured). */
+int rcgs_adam_fused_next(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
+                         const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                         const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                         rcgs_view* next_view, void* stream);
 /* Dense Adam on an explicit gradient (N,16,3) (adam_step API). */
 int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
                     const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,

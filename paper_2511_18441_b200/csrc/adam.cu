@@ -124,8 +124,12 @@ constexpr size_t kASmem = (size_t)kAStages * 3 * kATileBytes + kAStages * sizeof
 __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
     float* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
-    const int32_t* __restrict__ reject) {
-    if (reject && *reject) return;
+    const int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of, Center next_cen,
+    float4* __restrict__ next_color) {
+    // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
+    // colour epilogue the next view is still coloured from the unchanged SH
+    const bool upd = !(reject && *reject);
+    if (!upd && next_color == nullptr) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kAStages * 3 * kATileBytes);
     const int t = threadIdx.x;
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         const int64_t g0 = tile * kAG;
         const int ng = (int)(n - g0 < kAG ? n - g0 : kAG);
         mbar_wait(smem_addr(&bars[s]), (uint32_t)((it / kAStages) & 1));
-        if (gi < ng) {
+        if (upd && gi < ng) {
             const int64_t g = g0 + gi;
             const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
             float gr[12];
@@ -205,11 +209,41 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        if (t == 0) {
+        if (t == 0 && upd) {
             const uint32_t bytes = (uint32_t)ng * kARow;
 #pragma unroll
             for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (next_color != nullptr) {
+            // fused colour pass of the next step's view (render.py:209-214) from the
+            // updated SH tile: thread `part` < 3 evaluates channel `part` with the same
+            // fp64 basis and summation order as color_kernel (bit-identical), lane
+            // part 0 gathers the channels and writes the depth-rank slot
+            const int64_t g = g0 + gi;
+            const int32_t rs = gi < ng ? next_rank_of[g] : -1;
+            double val = 0.0;
+            if (rs >= 0 && part < 3) {
+                double x, y, z;
+                view_dir(pos, g, next_cen.c, x, y, z);
+                double b[16];
+                sh_basis16<double>(x, y, z, deg, b);
+                const float* P = reinterpret_cast<const float*>(stage_buf(s, 0)) + gi * 48;
+                double raw = 0.0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) raw = fma(b[i], (double)P[3 * i + part], raw);
+                val = raw + 0.5;
+            }
+            const double v1 = __shfl_down_sync(0xffffffffu, val, 1);
+            const double v2 = __shfl_down_sync(0xffffffffu, val, 2);
+            if (rs >= 0 && part == 0) {
+                const int act = (val > 0.0) | ((v1 > 0.0) << 1) | ((v2 > 0.0) << 2);
+                next_color[rs] = make_float4((float)fmax(0.0, val), (float)fmax(0.0, v1), (float)fmax(0.0, v2),
+                                             __int_as_float(act));
+            }
+            __syncthreads();  // the tile is refilled below only after every reader is done
+        }
+        if (t == 0) {
             const int64_t next = tile + (int64_t)kAStages * gridDim.x;
             if (next < ntiles) {
                 // the stage is refilled only after the store has read it
@@ -281,10 +315,10 @@ static AdamHyper hyper(const rcgs_adam_config* c) {
 
 using namespace rcgs;
 
-extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
-                               const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                               const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                               void* stream) {
+static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
+                           const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                           const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                           rcgs_view* next_view, void* stream) {
     RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
     RCGS_CHECK_ARG(n_views >= 1 && n_views <= kMaxViews, "views per step must be in [1, %d]", kMaxViews);
     RCGS_CHECK_ARG(sc->n < (int64_t)357913941, "scene too large for 32-bit Adam indexing");
@@ -310,14 +344,40 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
             grid = sms * (per_sm > 0 ? per_sm : 1);
         }
         const int64_t ntiles = (sc->n + kAG - 1) / kAG;
+        Center nc = {{0.0, 0.0, 0.0}};
+        const int32_t* nrank = nullptr;
+        float4* ncolor = nullptr;
+        if (next_view != nullptr && next_view->k > 0) {
+            nc = camera_center(next_view->cam);
+            nrank = next_view->rank_of;
+            ncolor = next_view->color;
+        }
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
-            sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), bc, d_reject);
+            sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), bc, d_reject, nrank, nc, ncolor);
         RCGS_LAUNCH_CHECK();
         dfree(bc, s);
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
+}
+
+extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
+                               const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                               const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                               void* stream) {
+    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step, nullptr,
+                           stream);
+}
+
+extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
+                                    const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                                    const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
+                                    rcgs_view* next_view, void* stream) {
+    RCGS_CHECK_ARG(next_view != nullptr, "null next view");
+    RCGS_CHECK_ARG(next_view->scene == sc, "next view belongs to another scene");
+    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step, next_view,
+                           stream);
 }
 
 extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,

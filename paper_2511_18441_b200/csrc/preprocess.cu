@@ -392,10 +392,10 @@ __global__ void color_kernel(const double* __restrict__ pos, const float4* __res
     }
     double raw[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        raw[0] += b[i] * (double)c[3 * i];
-        raw[1] += b[i] * (double)c[3 * i + 1];
-        raw[2] += b[i] * (double)c[3 * i + 2];
+    for (int i = 0; i < 16; ++i) {  // fused multiply-adds, as in the Adam colour epilogue
+        raw[0] = fma(b[i], (double)c[3 * i], raw[0]);
+        raw[1] = fma(b[i], (double)c[3 * i + 1], raw[1]);
+        raw[2] = fma(b[i], (double)c[3 * i + 2], raw[2]);
     }
     int act = 0;
     float col[3];

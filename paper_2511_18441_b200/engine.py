@@ -154,7 +154,7 @@ class RefitEngine:
     def __init__(self, dscene: D.DeviceScene, sh_dev: torch.Tensor, cameras, targets,
                  config, seed: int = 0, cache_views: bool = True, views=None, group=None,
                  raster=DEFAULT_CONFIG, max_pending: int = 4096, prefetch: int = 0,
-                 profile: bool = False):
+                 profile: bool = False, fuse_color: bool = True):
         self.dscene = dscene
         self.sh = sh_dev                      # (N, 16, 3) fp32, updated in place
         self.m = torch.zeros_like(sh_dev)
@@ -194,8 +194,14 @@ class RefitEngine:
         self.profile = profile
         self._prof = []
         self._build_ev = []  # inline view builds (no prefetcher)
+        # with prefetching, Adam also colours the next step's view (rcgs_adam_fused_next)
+        self.fuse_color = fuse_color
+        self._held = None
 
     def close(self):
+        if self._held is not None:
+            self._pf.retire(self._held[1])
+            self._held = None
         if self._pf is not None:
             self._pf.close()
             while self._future:
@@ -227,6 +233,16 @@ class RefitEngine:
 
     # -- one step -----------------------------------------------------------------
     def _next_prefetched(self):
+        """(picks, view, coloured) of the next step: the view taken ahead (and
+        coloured by the previous step's Adam epilogue) if any, else the next
+        prefetched one."""
+        if self._held is not None:
+            held, self._held = self._held, None
+            return held
+        picks, view = self._take_prefetched()
+        return picks, view, False
+
+    def _take_prefetched(self):
         while len(self._future) < self.prefetch:
             picks = self.draw()
             key = self._seq
@@ -239,8 +255,9 @@ class RefitEngine:
         return picks, view
 
     def step(self, picks=None, generation: int = 0):
+        coloured = False
         if picks is None and self._pf is not None:
-            picks, view = self._next_prefetched()
+            picks, view, coloured = self._next_prefetched()
             mine = picks[self.rank] if self.world > 1 else picks[0]
             prefetched = True
         else:
@@ -258,7 +275,8 @@ class RefitEngine:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if self.profile else None
         if ev:
             ev[0].record()
-        view.color(self.sh)
+        if not coloured:
+            view.color(self.sh)
         img, tgt_buf, grad = self._buf(view.height, view.width)
         if ev:
             ev[1].record()
@@ -282,9 +300,18 @@ class RefitEngine:
         cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
         if ev:
             ev[4].record()
-        N.call("rcgs_adam_fused", self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
-               (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
-               N.ptr(self.reject), N.ptr(self.step_dev), D.stream_ptr())
+        args = (self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
+                (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
+                N.ptr(self.reject), N.ptr(self.step_dev))
+        if prefetched and self.fuse_color:
+            # take the next step's view now (its build was submitted `prefetch`
+            # steps ago) and let this Adam colour it from the updated SH
+            nxt_picks, nxt = self._take_prefetched()
+            N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())
+            nxt._colored = True
+            self._held = (nxt_picks, nxt, True)
+        else:
+            N.call("rcgs_adam_fused", *args, D.stream_ptr())
         if ev:
             ev[5].record()
             self._prof.append(ev)

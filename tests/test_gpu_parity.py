@@ -463,3 +463,34 @@ def test_config1_refit_trajectory():
     print(f"c1 trajectory: worst metric diff {worst:.2e}, final render PSNR {p:.1f} dB, max |dDC| {dc:.2e}")
     assert worst < 1e-3
     assert p > 50.0
+
+
+# ---------------------------------------------------------------- engine pipelines
+def test_engine_pipelines_bit_identical():
+    """The step pipelines are scheduling choices only: inline view builds, views
+    prefetched on a side stream, and prefetching with the next view's colour
+    fused into Adam (rcgs_adam_fused_next) give bit-identical SH, Adam state and
+    per-step metrics."""
+    import sys
+    import torch
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2511_18441_b200.engine import RefitEngine
+    cfg = dict(n=30_000, deg=3, views=6, width=320, height=240)
+    scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
+    from paper_2511_18441_b200 import device as D
+    sp = P.SelectionPass(ds, cams, gt)
+    sp.run(D.to_device(cloud.points, torch.float64), (1.0, 0.2, 0.2))
+    targets = [sp.edited[i] for i in range(len(cams))]
+    out = []
+    for prefetch, fuse in ((0, False), (2, False), (2, True), (3, True)):
+        eng = RefitEngine(ds, sh0.clone(), cams, targets, P.OptimizerConfig(), seed=5, cache_views=False,
+                          prefetch=prefetch, fuse_color=fuse)
+        for _ in range(9):
+            eng.step()
+        recs = [(list(map(int, p)),) + tuple(r) for p, *r in eng.drain()]
+        eng.close()
+        out.append((eng.sh.clone(), eng.m.clone(), eng.v.clone(), recs))
+    for sh, m, v, recs in out[1:]:
+        assert torch.equal(sh, out[0][0]) and torch.equal(m, out[0][1]) and torch.equal(v, out[0][2])
+        assert recs == out[0][3]
