@@ -270,6 +270,7 @@ def run_gpu(args):
     eng.close()
     e2e = run_e2e(args, scene, cams, sp, group, world) if rank == 0 or world > 1 else None
     interactive = run_interactive(args, scene, cams, ds, sh0, sp, cloud) if args.extras and rank == 0 else None
+    resident = run_resident_views(args, ds, sh0, cams, sp) if args.extras and world == 1 else None
     if args.extras:
         del sp, targets, gt
         torch.cuda.empty_cache()
@@ -334,7 +335,7 @@ def run_gpu(args):
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-        "interactive_c5": interactive, "selection_sweep_c4": sweep,
+        "interactive_c5": interactive, "selection_sweep_c4": sweep, "resident_views": resident,
     }
     print(json.dumps(line))
 
@@ -398,13 +399,51 @@ def stage_model(eng, cams, npix, cfg, live, cnt):
         "raster_bwd": dict(ms=live["raster_bwd"], flops=11 * bwd[0] + 19 * bwd[1],
                            work={"evals": int(bwd[0]), "composites": int(bwd[1]), "blocks": int(bwd[2]),
                                  "blocks_skipped_zero_grad": int(bwd[3])}),
-        "adam": dict(ms=live["adam"], bytes=n * (6 * 192 + 12 + 24)),
+        "adam": dict(ms=live["adam"], bytes=n * (6 * 192 + 12 + 24) + (k * 20 if live.get("color_fused_steps") else 0),
+                     note=("+ next view's colour epilogue (rcgs_adam_fused_next)" if live.get("color_fused_steps")
+                           else "")),
     }
     work = {"fwd": {"evals_per_px": float(fwd[0]) / npix, "composites_per_px": float(fwd[1]) / npix,
                     "warp_iterations": int(fwd[4])},
             "bwd": {"evals_per_px": float(bwd[0]) / npix, "composites_per_px": float(bwd[1]) / npix,
                     "warp_iterations": int(bwd[4]), "blocks_skipped": int(bwd[3])}}
     return {"kernels": kern, "pairs": pairs, "kept": k, "raster_work": work}
+
+
+def run_resident_views(args, ds, sh0, cams, sp):
+    """Extra (not the headline): the same refit with every training view's
+    preprocess + binning kept resident in HBM after its first build
+    (RefitEngine(cache_views=True)).  Geometry is frozen during an SH-only
+    recolor, so a view's records, depth order and tile lists are identical every
+    time its camera is drawn; 64 views x ~140 MB fit easily in 180 GB.  The
+    headline `value` rebuilds them every step like the reference does."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200.engine import RefitEngine
+
+    eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
+                      seed=7, cache_views=True)
+    for i in range(len(cams)):  # build every view once, outside the timed region
+        eng.view(i)
+    for _ in range(max(3, args.warmup)):
+        eng.step()
+    eng.drain()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        eng.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    eng.drain()
+    for v in eng.views:
+        if v is not None:
+            v.close()
+    eng.close()
+    return {"value": round(1000.0 / ms, 3), "unit": "view-steps/s", "ms_per_step": round(ms, 4),
+            "views_resident": len(cams),
+            "note": "extra: per-view preprocess + binning kept resident (geometry frozen); not the headline"}
 
 
 def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):

@@ -272,7 +272,8 @@ class RefitEngine:
                 b1 = torch.cuda.Event(enable_timing=True)
                 b1.record()
                 self._build_ev.append((b0, b1))
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if self.profile else None
+        # stage events: colour | raster | loss | backward | (wait for the next view) | adam
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)] if self.profile else None
         if ev:
             ev[0].record()
         if not coloured:
@@ -296,25 +297,30 @@ class RefitEngine:
         view.backward(grad, acc=self.acc, nonfinite=self.reject)
         accs = parallel.exchange_accs(self.acc, self.group, out=self.acc_all)
         parallel.any_rank(self.reject, self.group)
-        ptrs = (ctypes.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
-        cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
         if ev:
             ev[4].record()
+        ptrs = (ctypes.c_void_p * len(accs))(*[a.data_ptr() for a in accs])
+        cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
         args = (self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
                 (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
                 N.ptr(self.reject), N.ptr(self.step_dev))
         if prefetched and self.fuse_color:
             # take the next step's view now (its build was submitted `prefetch`
-            # steps ago) and let this Adam colour it from the updated SH
+            # steps ago; the stream waits for it before the Adam stage event) and
+            # let this Adam colour it from the updated SH
             nxt_picks, nxt = self._take_prefetched()
+            if ev:
+                ev[5].record()
             N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())
             nxt._colored = True
             self._held = (nxt_picks, nxt, True)
         else:
+            if ev:
+                ev[5].record()
             N.call("rcgs_adam_fused", *args, D.stream_ptr())
         if ev:
-            ev[5].record()
-            self._prof.append(ev)
+            ev[6].record()
+            self._prof.append((ev, coloured))
         rec[3].copy_(self.reject[0], non_blocking=True)
         self.pending.append((picks, generation))
         if prefetched:
@@ -340,12 +346,17 @@ class RefitEngine:
         """Mean device ms per stage over the profiled steps (CUDA events on the
         launching streams; view builds on the prefetch stream)."""
         torch.cuda.synchronize()
-        names = ["color", "raster_fwd", "loss_grad", "raster_bwd", "adam"]
+        names = ["color", "raster_fwd", "loss_grad", "raster_bwd", "next_view_wait", "adam"]
         out = {}
         if self._prof:
             for i, nme in enumerate(names):
-                out[nme] = float(np.mean([e[i].elapsed_time(e[i + 1]) for e in self._prof]))
+                # colour: only steps that launched the colour kernel (else it was
+                # fused into the previous step's Adam, which the adam stage includes)
+                ts = [e[i].elapsed_time(e[i + 1]) for e, fused in self._prof if not (i == 0 and fused)]
+                if ts:
+                    out[nme] = float(np.mean(ts))
             out["step_events"] = len(self._prof)
+            out["color_fused_steps"] = sum(1 for _, fused in self._prof if fused)
         if self._pf is not None and self._pf.events:
             out["view_build"] = float(np.mean([a.elapsed_time(b) for a, b in self._pf.events]))
             if self._pf.host_build_ms:
