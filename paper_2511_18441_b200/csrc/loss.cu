@@ -30,6 +30,7 @@ constexpr int kLT = 32;            // output tile edge
 constexpr int kLH = kLT + 2 * kR;  // 42
 constexpr int kRows = 4;           // output rows per thread in the vertical pass
 constexpr int kLNT = 256;          // = kLT * kLT / kRows
+constexpr int kHS = 4;             // adjacent outputs per thread in the horizontal passes
 #ifndef RCGS_LOSS_CTAS
 #define RCGS_LOSS_CTAS 3
 #endif
@@ -175,24 +176,67 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
                 ig[i] = in ? g[gi] : T(0);
             }
             __syncthreads();
-            for (int i = t; i < kLH * kLT; i += kLNT) {
-                const int r = i / kLT, cc = i % kLT;
-                double s1 = 0, s2 = 0, s11 = 0, s22 = 0, s12 = 0;
+            // horizontal pass: each thread a strip of kHS adjacent outputs of one row
+            // from a register-resident segment (squares formed once per input);
+            // every accumulator keeps its k = 0..10 FMA sequence
+            constexpr int kP = kLH * kLT;
+            for (int i = t; i < kLH * (kLT / kHS); i += kLNT) {
+                const int r = i / (kLT / kHS), c0 = (i % (kLT / kHS)) * kHS;
+                double* out = hs + r * kLT + c0;
+                {
+                    const T* src = iy + r * kLH + c0;  // s1, s11 (image)
+                    double x[kHS + kWin - 1], xx[kHS + kWin - 1];
 #pragma unroll
-                for (int k = 0; k < kWin; ++k) {
-                    const int o = r * kLH + cc + k;
-                    const double a = (double)iy[o], b = (double)ig[o], w = win.w[k];
-                    s1 = fma(w, a, s1);
-                    s2 = fma(w, b, s2);
-                    s11 = fma(w, a * a, s11);
-                    s22 = fma(w, b * b, s22);
-                    s12 = fma(w, a * b, s12);
+                    for (int j = 0; j < kHS + kWin - 1; ++j) {
+                        x[j] = (double)src[j];
+                        xx[j] = x[j] * x[j];
+                    }
+#pragma unroll
+                    for (int o = 0; o < kHS; ++o) {
+                        double s1 = 0, s11 = 0;
+#pragma unroll
+                        for (int k = 0; k < kWin; ++k) {
+                            s1 = fma(win.w[k], x[o + k], s1);
+                            s11 = fma(win.w[k], xx[o + k], s11);
+                        }
+                        out[o] = s1;
+                        out[2 * kP + o] = s11;
+                    }
                 }
-                hs[i] = s1;
-                hs[kLH * kLT + i] = s2;
-                hs[2 * kLH * kLT + i] = s11;
-                hs[3 * kLH * kLT + i] = s22;
-                hs[4 * kLH * kLT + i] = s12;
+                {
+                    const T* src = ig + r * kLH + c0;  // s2, s22 (target)
+                    double x[kHS + kWin - 1], xx[kHS + kWin - 1];
+#pragma unroll
+                    for (int j = 0; j < kHS + kWin - 1; ++j) {
+                        x[j] = (double)src[j];
+                        xx[j] = x[j] * x[j];
+                    }
+#pragma unroll
+                    for (int o = 0; o < kHS; ++o) {
+                        double s2 = 0, s22 = 0;
+#pragma unroll
+                        for (int k = 0; k < kWin; ++k) {
+                            s2 = fma(win.w[k], x[o + k], s2);
+                            s22 = fma(win.w[k], xx[o + k], s22);
+                        }
+                        out[kP + o] = s2;
+                        out[3 * kP + o] = s22;
+                    }
+                }
+                {
+                    const T* sa = iy + r * kLH + c0;  // s12
+                    const T* sb = ig + r * kLH + c0;
+                    double xy[kHS + kWin - 1];
+#pragma unroll
+                    for (int j = 0; j < kHS + kWin - 1; ++j) xy[j] = (double)sa[j] * (double)sb[j];
+#pragma unroll
+                    for (int o = 0; o < kHS; ++o) {
+                        double s12 = 0;
+#pragma unroll
+                        for (int k = 0; k < kWin; ++k) s12 = fma(win.w[k], xy[o + k], s12);
+                        out[4 * kP + o] = s12;
+                    }
+                }
             }
             __syncthreads();
         }
@@ -270,15 +314,22 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                 for (int q = 0; q < 3; ++q) im[q * kLH * kLH + i] = in ? maps[q * npix * 3 + gi] : MT(0);
             }
             __syncthreads();
-            for (int i = t; i < kLH * kLT; i += kLNT) {
-                const int r = i / kLT, cc = i % kLT;
+            // horizontal pass in kHS-output strips from register-resident segments
+            for (int i = t; i < kLH * (kLT / kHS); i += kLNT) {
+                const int r = i / (kLT / kHS), c0 = (i % (kLT / kHS)) * kHS;
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    double s = 0.0;
+                    const MT* src = im + q * kLH * kLH + r * kLH + c0;
+                    double x[kHS + kWin - 1];
 #pragma unroll
-                    for (int k = 0; k < kWin; ++k)
-                        s = fma(win.w[k], (double)im[q * kLH * kLH + r * kLH + cc + k], s);
-                    hs[q * kLH * kLT + i] = s;
+                    for (int j = 0; j < kHS + kWin - 1; ++j) x[j] = (double)src[j];
+#pragma unroll
+                    for (int o = 0; o < kHS; ++o) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int k = 0; k < kWin; ++k) s = fma(win.w[k], x[o + k], s);
+                        hs[q * kLH * kLT + r * kLT + c0 + o] = s;
+                    }
                 }
             }
             __syncthreads();
