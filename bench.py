@@ -396,15 +396,22 @@ def stage_model(eng, cams, npix, cfg, live, cnt):
         "raster_fwd": dict(ms=live["raster_fwd"], flops=11 * fwd[0] + 13 * fwd[1],
                            work={"evals": int(fwd[0]), "composites": int(fwd[1]), "blocks": int(fwd[2])}),
         "loss_grad": dict(ms=live["loss_grad"], bytes=npix * 36, note="fp64 SSIM; fused-minimum bytes"),
-        "raster_bwd": dict(ms=live["raster_bwd"], flops=11 * bwd[0] + 19 * bwd[1],
-                           work={"evals": int(bwd[0]), "composites": int(bwd[1]), "blocks": int(bwd[2]),
-                                 "blocks_skipped_zero_grad": int(bwd[3])}),
+        # backward: streams the forward's weight records (rcgs_render_train) when it
+        # has them -- HBM bound: 132 B per record + the gradient image + the
+        # fixed-point accumulators
+        "raster_bwd": (dict(ms=live["raster_bwd"], bytes=int(fwd[3]) * 132 + npix * 12 + k * 24 * 2,
+                            note="streams the recorded composite weights (132 B/record)",
+                            work={"records": int(fwd[3])})
+                       if bwd[2] == 0 and fwd[3] > 0 else
+                       dict(ms=live["raster_bwd"], flops=11 * bwd[0] + 19 * bwd[1],
+                            work={"evals": int(bwd[0]), "composites": int(bwd[1]), "blocks": int(bwd[2]),
+                                  "blocks_skipped_zero_grad": int(bwd[3])})),
         "adam": dict(ms=live["adam"], bytes=n * (6 * 192 + 12 + 24) + (k * 20 if live.get("color_fused_steps") else 0),
                      note=("+ next view's colour epilogue (rcgs_adam_fused_next)" if live.get("color_fused_steps")
                            else "")),
     }
     work = {"fwd": {"evals_per_px": float(fwd[0]) / npix, "composites_per_px": float(fwd[1]) / npix,
-                    "warp_iterations": int(fwd[4])},
+                    "warp_iterations": int(fwd[4]), "weight_records": int(fwd[3])},
             "bwd": {"evals_per_px": float(bwd[0]) / npix, "composites_per_px": float(bwd[1]) / npix,
                     "warp_iterations": int(bwd[4]), "blocks_skipped": int(bwd[3])}}
     return {"kernels": kern, "pairs": pairs, "kept": k, "raster_work": work}

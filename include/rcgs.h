@@ -111,6 +111,13 @@ int rcgs_view_color(rcgs_view* view, const float* d_sh, void* stream);
 /* layout 0 = HWC (H,W,3), 1 = CHW (3,H,W); d_t_final (H,W) may be NULL. */
 int rcgs_render(const rcgs_view* view, const float* h_background3, int layout,
                 float* d_image, float* d_t_final, void* stream);
+/* rcgs_render that also keeps the view's composite weights w = alpha * T (they
+ * depend on geometry and camera only): rcgs_backward then streams them instead
+ * of re-traversing the tile lists, and later renders of the view are an SpMV.
+ * Results are bit-identical to the traversal paths.  Reserves up to
+ * 8 * pairs * 132 bytes (~2.8 GB at 1080p / 1M gaussians), freed with the view. */
+int rcgs_render_train(rcgs_view* view, const float* h_bg3, int layout, float* d_image, float* d_t_final,
+                      void* stream);
 
 /* depth_from_gaussians (render.py:373-398): (H,W) fp64, +inf where T never drops
  * below tau at a composited gaussian.  d_cross (H,W) int32 = kept rank or -1, may be NULL. */

@@ -86,6 +86,8 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_
 // vals_in may be null: values then start as the element index.
 int radix_sort_u64(uint64_t** key_cur, uint64_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
                    bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
+void release_records(const rcgs_view* v);  // raster.cu: drop the record-arena ownership
+
 int radix_sort_u32(uint32_t** key_cur, uint32_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
                    bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
 
@@ -144,4 +146,12 @@ struct rcgs_view {
     uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
+    // composite-weight records (rcgs_render_train; geometry + camera only), in the
+    // process-wide record arena (raster.cu) while this view owns it
+    bool wrec_valid;
+    uint64_t wrec_epoch;
+    uint32_t* wrec_n;     // (tiles * 8,) records per 8x4 block
+    uint32_t* wrec_s;     // (8 * pairs,) entry (depth rank) per record slot
+    float* wrec_w;        // (8 * pairs, 32) pixel weights per record slot
+    float* wrec_tf;       // (H * W,) final transmittance
 };

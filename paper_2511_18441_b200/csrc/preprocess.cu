@@ -501,6 +501,10 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->pair_e, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
+    release_records(v);  // records live in the raster's arena, not in the view
+    v->wrec_n = v->wrec_s = nullptr;
+    v->wrec_w = v->wrec_tf = nullptr;
+    v->wrec_valid = false;
 }
 
 extern "C" int rcgs_view_destroy(rcgs_view* v, void* stream) {

@@ -32,11 +32,15 @@
 // (mask statistics), CAPTURE (contribution lists).
 #include <cuda_fp16.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace rcgs {
 
-enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRITE = 5 };
+// FWDREC: FWD that also records the composite weights (see `WeightRecords`)
+enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRITE = 5, FWDREC = 6 };
 
 constexpr int kWarpsPerCTA = 8;
 constexpr int kCTA = 32 * kWarpsPerCTA;
@@ -47,6 +51,13 @@ constexpr int kMinCTAs = RCGS_RASTER_MIN_CTAS;  // resident CTAs per SM the regi
 constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8x4 pixels
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kFixScale = 1125899906842624.0;  // 2^50
+
+// round(v * 2^50) to int64: scaling by a power of two is exact in fp32 (|v| < 2^77
+// for a finite product here), so the fp32 round-to-nearest conversion equals
+// llrint((double)v * 2^50) with two fp32 instructions instead of three fp64 ones
+__device__ __forceinline__ long long to_fixed(float v) {
+    return __float2ll_rn(v * 1125899906842624.0f);
+}
 
 struct RasterArgs {
     const uint2* ranges;
@@ -88,6 +99,10 @@ struct RasterArgs {
     int64_t* cap_pixel;
     int64_t* cap_kept;
     double* cap_weight;
+    // FWDREC: weight records (per (tile, block): count; per record: entry, 32 weights)
+    uint32_t* wrec_n;
+    uint32_t* wrec_s;
+    float* wrec_w;
 };
 
 // Instrumentation: when set, raster launches accumulate work counters here.
@@ -296,6 +311,8 @@ struct WarpStage {
 // launches carry no counter registers or checks in the entry loop.
 template <int M, bool kInstr>
 __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
+    constexpr bool kFwd = (M == FWD || M == FWDREC);
+    constexpr int kRow = (M == FWDREC) ? (int)FWD : M;  // counter row
     __shared__ WarpStage stage_all[kWarpsPerCTA];
     const int lane = threadIdx.x & 31;
     WarpStage& st = stage_all[threadIdx.x >> 5];
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             // sum_p g_p w_ip has no term from this block when all its gradients are 0
             // (the recolor gradient is local to the edited region): skip the block
             if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) {
-                if (kInstr && a.counters && lane == 0) atomicAdd(&a.counters[5 * M + 3], 1ull);
+                if (kInstr && a.counters && lane == 0) atomicAdd(&a.counters[5 * kRow + 3], 1ull);
                 continue;
             }
         }
@@ -345,6 +362,9 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
         uint32_t n_eval = 0, n_comp = 0, n_iter = 0;
+        // FWDREC: this block's record slots, 8 per tile-list entry and block
+        const int64_t rbase = (int64_t)kBlocksPerTile * range.x + (int64_t)blk * (range.y - range.x);
+        uint32_t nrec = 0;
         for (uint32_t c0 = range.x; c0 < range.y; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const uint32_t j = c0 + lane;
@@ -369,7 +389,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 st.c[slot] = rc;
                 st.s[slot] = s;
                 st.j[slot] = j;
-                if (M == FWD) st.col[slot] = a.color[s];
+                if (kFwd) st.col[slot] = a.color[s];
             }
             __syncwarp();
             const int n = __popc(bal);
@@ -399,12 +419,21 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 }
                 const bool comp = (r == COMPOSITE);
                 if (kInstr) n_comp += comp;
-                if (M == FWD) {
+                if (kFwd) {
                     if (comp) {
                         const float4 c = st.col[k];
                         acc0 = fmaf(c.x, w, acc0);
                         acc1 = fmaf(c.y, w, acc1);
                         acc2 = fmaf(c.z, w, acc2);
+                    }
+                    if (M == FWDREC && __ballot_sync(0xffffffffu, comp)) {
+                        // record: the entry + all 32 pixel weights (0 where a pixel did not
+                        // composite): one coalesced 128-byte store.  (Packing only the
+                        // composited weights measured slower both ways: partial-sector
+                        // writes here, offset-dependent loads in the readers.)
+                        const int64_t slot = rbase + nrec++;
+                        a.wrec_w[slot * 32 + lane] = comp ? w : 0.f;
+                        if (lane == 0) a.wrec_s[slot] = st.s[k];
                     }
                 } else if (M == CAP_COUNT) {
                     ncap += comp;
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                         val += __shfl_xor_sync(0xffffffffu, val, 1);
                         if ((lane & 7) == 0 && lane < 24) {
                             if (isfinite(val)) {
-                                const long long q = llrint((double)val * kFixScale);
+                                const long long q = to_fixed(val);
                                 atomicAdd(&a.acc_fx[3 * (int64_t)st.s[k] + (lane >> 3)], (unsigned long long)q);
                             } else if (a.nonfinite) {
                                 atomicOr(a.nonfinite, 1);
@@ -462,10 +491,10 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 n_comp += __shfl_xor_sync(0xffffffffu, n_comp, o);
             }
             if (lane == 0) {
-                atomicAdd(&a.counters[5 * M + 0], (unsigned long long)n_eval);
-                atomicAdd(&a.counters[5 * M + 1], (unsigned long long)n_comp);
-                atomicAdd(&a.counters[5 * M + 2], 1ull);
-                atomicAdd(&a.counters[5 * M + 4], (unsigned long long)n_iter);
+                atomicAdd(&a.counters[5 * kRow + 0], (unsigned long long)n_eval);
+                atomicAdd(&a.counters[5 * kRow + 1], (unsigned long long)n_comp);
+                atomicAdd(&a.counters[5 * kRow + 2], 1ull);
+                atomicAdd(&a.counters[5 * kRow + 4], (unsigned long long)n_iter);
             }
         }
         if (kInstr && a.trace) {
@@ -483,8 +512,12 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 tr[7] = (uint32_t)tile;
             }
         }
+        if (M == FWDREC && lane == 0) {
+            a.wrec_n[tile * kBlocksPerTile + blk] = nrec;
+            if (kInstr && a.counters) atomicAdd(&a.counters[5 * kRow + 3], (unsigned long long)nrec);
+        }
         if (!inside) continue;
-        if (M == FWD) {
+        if (kFwd) {
             const float T = px.T;
             const float o0 = fmaf(T, a.bg0, acc0), o1 = fmaf(T, a.bg1, acc1), o2 = fmaf(T, a.bg2, acc2);
             if (a.layout == 0) {
@@ -505,6 +538,188 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             a.cap_count[pix] = ncap;
         }
     }
+}
+
+// ---------------------------------------------------------------- weight records
+// The composite weights w = alpha * T_before of a view depend on the geometry and
+// the camera only, not on the colours an SH-only recolor refits.  FWDREC stores,
+// per 8x4 block and per entry iteration in which any pixel composited, the entry
+// and the 32 pixel weights (0 where a pixel did not composite).  The backward is
+// then a streaming pass over the records (the same products, reduce-scatter and
+// fixed-point atomics, in the same entry order: bit-identical to re-traversing),
+// and a later render of the same view is an SpMV over them.
+struct RecArgs {
+    const uint2* ranges;
+    const uint32_t* tile_order;
+    unsigned* counter;
+    int W, H, tiles_x, n_items;
+    const uint32_t* wrec_n;
+    const uint32_t* wrec_s;
+    const float* wrec_w;
+    // render
+    const float4* color;
+    const float* t_in;
+    float bg0, bg1, bg2;
+    int layout;
+    float* image;
+    float* t_final;
+    // backward
+    const float* grad;
+    unsigned long long* acc_fx;
+    int32_t* nonfinite;
+};
+
+template <bool kBwd>
+__global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
+    const int lane = threadIdx.x & 31;
+    constexpr int kU = 4;  // records in flight per warp
+    for (;;) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(a.counter, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= (unsigned)a.n_items) break;
+        const int tile = a.tile_order ? (int)a.tile_order[item / kBlocksPerTile] : (int)(item / kBlocksPerTile);
+        const int blk = (int)(item % kBlocksPerTile);
+        const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+        const int u = tx * kTile + (blk & 1) * 8 + (lane & 7), v = ty * kTile + (blk >> 1) * 4 + (lane >> 3);
+        const bool inside = u < a.W && v < a.H;
+        const int64_t pix = (int64_t)v * a.W + u;
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+        if (kBwd) {
+            if (inside) {
+                g0 = a.grad[3 * pix];
+                g1 = a.grad[3 * pix + 1];
+                g2 = a.grad[3 * pix + 2];
+            }
+            if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) continue;
+        }
+        const uint2 range = a.ranges[tile];
+        const int64_t base = (int64_t)kBlocksPerTile * range.x + (int64_t)blk * (range.y - range.x);
+        const uint32_t n = a.wrec_n[tile * kBlocksPerTile + blk];
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
+        for (uint32_t r0 = 0; r0 < n; r0 += kU) {
+            float w[kU];
+            uint32_t s[kU];
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                const bool ok = r0 + q < n;
+                w[q] = ok ? __ldcs(a.wrec_w + (base + r0 + q) * 32 + lane) : 0.f;
+                s[q] = ok ? a.wrec_s[base + r0 + q] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                if (r0 + q >= n) break;
+                if (!kBwd) {
+                    if (w[q] != 0.f) {
+                        const float4 c = a.color[s[q]];
+                        acc0 = fmaf(c.x, w[q], acc0);
+                        acc1 = fmaf(c.y, w[q], acc1);
+                        acc2 = fmaf(c.z, w[q], acc2);
+                    }
+                } else {
+                    const bool comp = w[q] != 0.f;
+                    const float v0 = comp ? w[q] * g0 : 0.f, v1 = comp ? w[q] * g1 : 0.f,
+                                v2 = comp ? w[q] * g2 : 0.f;
+                    if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
+                        const bool h16 = lane & 16, h8 = lane & 8;
+                        const float ra = __shfl_xor_sync(0xffffffffu, h16 ? v0 : v2, 16);
+                        const float rb = __shfl_xor_sync(0xffffffffu, h16 ? v1 : 0.f, 16);
+                        const float ka = (h16 ? v2 : v0) + ra, kb = (h16 ? 0.f : v1) + rb;
+                        float val = (h8 ? kb : ka) + __shfl_xor_sync(0xffffffffu, h8 ? ka : kb, 8);
+                        val += __shfl_xor_sync(0xffffffffu, val, 4);
+                        val += __shfl_xor_sync(0xffffffffu, val, 2);
+                        val += __shfl_xor_sync(0xffffffffu, val, 1);
+                        if ((lane & 7) == 0 && lane < 24) {
+                            if (isfinite(val)) {
+                                const long long qq = to_fixed(val);
+                                atomicAdd(&a.acc_fx[3 * (int64_t)s[q] + (lane >> 3)], (unsigned long long)qq);
+                            } else if (a.nonfinite) {
+                                atomicOr(a.nonfinite, 1);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (!kBwd && inside) {
+            const float T = a.t_in[pix];
+            const float o0 = fmaf(T, a.bg0, acc0), o1 = fmaf(T, a.bg1, acc1), o2 = fmaf(T, a.bg2, acc2);
+            if (a.layout == 0) {
+                a.image[3 * pix] = o0;
+                a.image[3 * pix + 1] = o1;
+                a.image[3 * pix + 2] = o2;
+            } else {
+                const int64_t plane = (int64_t)a.W * a.H;
+                a.image[pix] = o0;
+                a.image[plane + pix] = o1;
+                a.image[2 * plane + pix] = o2;
+            }
+            if (a.t_final) a.t_final[pix] = T;
+        }
+    }
+}
+
+template <bool kBwd>
+static int launch_rec(RecArgs a, cudaStream_t s) {
+    static int grid = 0;
+    if (grid == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        RCGS_CUDA(cudaGetDevice(&dev));
+        RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<true>, kCTA, 0));
+        grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    unsigned* counter = nullptr;
+    RCGS_TRY(dalloc(&counter, 1, s));
+    RCGS_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+    a.counter = counter;
+    const int blocks = (int)min((int64_t)grid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
+    if (blocks > 0) rec_kernel<kBwd><<<blocks, kCTA, 0, s>>>(a);
+    dfree(counter, s);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+// One process-wide record arena (per device process): the training path records
+// one view at a time on the caller's stream, so the scratch is reused every step
+// instead of reserving (and stream-ordered freeing) ~3 GB per view.  It grows
+// with plain cudaMalloc/cudaFree (rare; cudaFree synchronises) and is never
+// released by views.  A view's records are valid while it is the arena's owner
+// at the epoch it recorded in (views are destroyed on other threads, hence the
+// atomics).
+struct RecordArena {
+    std::mutex grow;
+    unsigned char* base = nullptr;
+    size_t cap = 0;
+    std::atomic<const rcgs_view*> owner{nullptr};
+    std::atomic<uint64_t> epoch{0};
+};
+static RecordArena g_arena;
+
+static bool records_valid(const rcgs_view* v) {
+    return v->wrec_valid && g_arena.owner.load() == v && g_arena.epoch.load() == v->wrec_epoch;
+}
+
+void release_records(const rcgs_view* v) {
+    const rcgs_view* expect = v;
+    g_arena.owner.compare_exchange_strong(expect, nullptr);
+}
+
+static RecArgs rec_args(const rcgs_view* v) {
+    RecArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ranges = v->ranges;
+    a.tile_order = v->tile_order;
+    a.W = v->cam.width;
+    a.H = v->cam.height;
+    a.tiles_x = v->tiles_x;
+    a.n_items = v->tiles_x * v->tiles_y * kBlocksPerTile;
+    a.wrec_n = v->wrec_n;
+    a.wrec_s = v->wrec_s;
+    a.wrec_w = v->wrec_w;
+    a.color = v->color;
+    a.t_in = v->wrec_tf;
+    return a;
 }
 
 static RasterArgs base_args(const rcgs_view* v) {
@@ -590,7 +805,66 @@ extern "C" int rcgs_render(const rcgs_view* v, const float* h_bg, int layout, fl
     a.layout = layout;
     a.image = d_image;
     a.t_final = d_t_final;
+    if (records_valid(v)) {  // weights recorded by an earlier rcgs_render_train: SpMV
+        RecArgs ra = rec_args(v);
+        ra.bg0 = a.bg0;
+        ra.bg1 = a.bg1;
+        ra.bg2 = a.bg2;
+        ra.layout = layout;
+        ra.image = d_image;
+        ra.t_final = d_t_final;
+        return launch_rec<false>(ra, as_stream(stream));
+    }
     return launch<FWD>(a, as_stream(stream));
+}
+
+extern "C" int rcgs_render_train(rcgs_view* v, const float* h_bg, int layout, float* d_image, float* d_t_final,
+                                 void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_image != nullptr, "null argument");
+    RCGS_CHECK_ARG(layout == 0 || layout == 1, "unknown layout %d", layout);
+    if (records_valid(v) || v->pairs == 0) return rcgs_render(v, h_bg, layout, d_image, d_t_final, stream);
+    cudaStream_t s = as_stream(stream);
+    const int64_t n_items = (int64_t)v->tiles_x * v->tiles_y * kBlocksPerTile;
+    const int64_t cap = (int64_t)kBlocksPerTile * v->pairs;  // <= one record per entry and block
+    const int64_t npix = (int64_t)v->cam.width * v->cam.height;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t o_n = 0, o_s = up(o_n + 4 * n_items), o_w = up(o_s + 4 * cap), o_tf = up(o_w + 128 * cap);
+    const size_t need = up(o_tf + 4 * npix);
+    {
+        std::lock_guard<std::mutex> lock(g_arena.grow);
+        if (need > g_arena.cap) {
+            if (g_arena.base) RCGS_CUDA(cudaFree(g_arena.base));  // synchronises: no use in flight
+            g_arena.base = nullptr;
+            g_arena.cap = 0;
+            const size_t want = need + need / 8;
+            RCGS_CUDA(cudaMalloc(&g_arena.base, want));
+            g_arena.cap = want;
+        }
+    }
+    v->wrec_n = reinterpret_cast<uint32_t*>(g_arena.base + o_n);
+    v->wrec_s = reinterpret_cast<uint32_t*>(g_arena.base + o_s);
+    v->wrec_w = reinterpret_cast<float*>(g_arena.base + o_w);
+    v->wrec_tf = reinterpret_cast<float*>(g_arena.base + o_tf);
+    g_arena.owner.store(v);
+    v->wrec_epoch = g_arena.epoch.fetch_add(1) + 1;
+    RasterArgs a = base_args(v);
+    if (h_bg) {
+        a.bg0 = h_bg[0];
+        a.bg1 = h_bg[1];
+        a.bg2 = h_bg[2];
+    }
+    a.layout = layout;
+    a.image = d_image;
+    a.t_final = v->wrec_tf;
+    a.wrec_n = v->wrec_n;
+    a.wrec_s = v->wrec_s;
+    a.wrec_w = v->wrec_w;
+    RCGS_TRY(launch<FWDREC>(a, s));
+    v->wrec_valid = true;
+    if (d_t_final)
+        RCGS_CUDA(cudaMemcpyAsync(d_t_final, v->wrec_tf, sizeof(float) * v->cam.width * v->cam.height,
+                                  cudaMemcpyDeviceToDevice, s));
+    return RCGS_OK;
 }
 
 extern "C" int rcgs_depth(const rcgs_view* v, double tau, double* d_depth, int32_t* d_cross,
@@ -656,7 +930,13 @@ extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, floa
     unsigned long long* acc_fx = nullptr;
     RCGS_TRY(dalloc(&acc_fx, 3 * v->k, s));
     RCGS_CUDA(cudaMemsetAsync(acc_fx, 0, 3 * v->k * sizeof(unsigned long long), s));
-    if (v->pairs > 0) {
+    if (v->pairs > 0 && records_valid(v)) {  // stream the recorded weights
+        RecArgs ra = rec_args(v);
+        ra.grad = d_grad_image;
+        ra.acc_fx = acc_fx;
+        ra.nonfinite = d_nonfinite;
+        RCGS_TRY(launch_rec<true>(ra, s));
+    } else if (v->pairs > 0) {
         RasterArgs a = base_args(v);
         a.grad = d_grad_image;
         a.acc_fx = acc_fx;

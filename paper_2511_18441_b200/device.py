@@ -162,13 +162,16 @@ class View:
             raise ValidationError("View.color(sh) must run before rendering")
 
     # -- raster ----------------------------------------------------------------
-    def render(self, background=None, layout: int = 0, out=None, t_final=False):
+    def render(self, background=None, layout: int = 0, out=None, t_final=False, train: bool = False):
+        """Composite the view.  train=True also keeps its composite weights
+        (rcgs_render_train) so backward() streams them instead of re-traversing."""
         self._need_color()
         shape = (self.height, self.width, 3) if layout == 0 else (3, self.height, self.width)
         img = out if out is not None else torch.empty(shape, dtype=torch.float32, device=device())
         tf = torch.empty((self.height, self.width), dtype=torch.float32, device=device()) if t_final else None
         bg = (ctypes.c_float * 3)(*(np.zeros(3) if background is None else np.asarray(background, np.float64)))
-        N.call("rcgs_render", self.handle, bg, int(layout), N.ptr(img), N.ptr(tf), stream_ptr())
+        N.call("rcgs_render_train" if train else "rcgs_render", self.handle, bg, int(layout), N.ptr(img),
+               N.ptr(tf), stream_ptr())
         return (img, tf) if t_final else img
 
     def depth(self, tau: float = 0.5, with_cross: bool = False):

@@ -281,7 +281,7 @@ class RefitEngine:
         img, tgt_buf, grad = self._buf(view.height, view.width)
         if ev:
             ev[1].record()
-        view.render(None, 0, out=img)
+        view.render(None, 0, out=img, train=True)
         target = self.targets[mine]
         if not target.is_cuda:           # streamed dataset: H2D of this step's target
             tgt_buf.copy_(target, non_blocking=True)

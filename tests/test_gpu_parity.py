@@ -494,3 +494,29 @@ def test_engine_pipelines_bit_identical():
     for sh, m, v, recs in out[1:]:
         assert torch.equal(sh, out[0][0]) and torch.equal(m, out[0][1]) and torch.equal(v, out[0][2])
         assert recs == out[0][3]
+
+
+def test_weight_records_bit_identical():
+    """rcgs_render_train + record-streaming backward + SpMV re-render equal the
+    traversal render / backward bit for bit (weights depend on geometry only)."""
+    import sys
+    import torch
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2511_18441_b200 import device as D
+    cfg = dict(n=40_000, deg=3, views=3, width=400, height=300)
+    scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
+    sh = sh0 + 0.01 * torch.randn_like(sh0)  # colours away from the ground truth
+    for intr, pose in cams:
+        ref = D.View(ds, intr, pose, P.DEFAULT_CONFIG).color(sh)
+        rec = D.View(ds, intr, pose, P.DEFAULT_CONFIG).color(sh)
+        img_ref, tf_ref = ref.render(None, 0, t_final=True)
+        img_rec, tf_rec = rec.render(None, 0, t_final=True, train=True)
+        assert torch.equal(img_ref, img_rec) and torch.equal(tf_ref, tf_rec)
+        bg = np.array([0.2, 0.5, 0.9])
+        assert torch.equal(ref.render(bg, 1), rec.render(bg, 1))  # SpMV path, planar layout
+        g = torch.randn_like(img_ref) * 1e-3
+        g[: 40] = 0.0  # zero-gradient blocks are skipped by both paths
+        assert torch.equal(ref.backward(g), rec.backward(g))
+        ref.close()
+        rec.close()
