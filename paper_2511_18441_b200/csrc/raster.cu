@@ -616,27 +616,39 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                         acc1 = fmaf(c.y, w[q], acc1);
                         acc2 = fmaf(c.z, w[q], acc2);
                     }
-                } else {
+                }
+            }
+            if (kBwd) {
+                // the kU records' (w g) sums for 3 channels (+1 zero pad) = 16 values,
+                // halved across the warp: xor 16, 8, 4, 2 then a last xor 1 add, i.e.
+                // the butterfly tree of a plain warp sum (bit-identical totals) with 16
+                // shuffles per 4 records; lane L ends with record (L>>3)&3, channel (L>>1)&3
+                float x[16];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
                     const bool comp = w[q] != 0.f;
-                    const float v0 = comp ? w[q] * g0 : 0.f, v1 = comp ? w[q] * g1 : 0.f,
-                                v2 = comp ? w[q] * g2 : 0.f;
-                    if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
-                        const bool h16 = lane & 16, h8 = lane & 8;
-                        const float ra = __shfl_xor_sync(0xffffffffu, h16 ? v0 : v2, 16);
-                        const float rb = __shfl_xor_sync(0xffffffffu, h16 ? v1 : 0.f, 16);
-                        const float ka = (h16 ? v2 : v0) + ra, kb = (h16 ? 0.f : v1) + rb;
-                        float val = (h8 ? kb : ka) + __shfl_xor_sync(0xffffffffu, h8 ? ka : kb, 8);
-                        val += __shfl_xor_sync(0xffffffffu, val, 4);
-                        val += __shfl_xor_sync(0xffffffffu, val, 2);
-                        val += __shfl_xor_sync(0xffffffffu, val, 1);
-                        if ((lane & 7) == 0 && lane < 24) {
-                            if (isfinite(val)) {
-                                const long long qq = to_fixed(val);
-                                atomicAdd(&a.acc_fx[3 * (int64_t)s[q] + (lane >> 3)], (unsigned long long)qq);
-                            } else if (a.nonfinite) {
-                                atomicOr(a.nonfinite, 1);
-                            }
-                        }
+                    x[4 * q] = comp ? w[q] * g0 : 0.f;
+                    x[4 * q + 1] = comp ? w[q] * g1 : 0.f;
+                    x[4 * q + 2] = comp ? w[q] * g2 : 0.f;
+                    x[4 * q + 3] = 0.f;
+                }
+#pragma unroll
+                for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
+                    const bool hi = lane & off;
+#pragma unroll
+                    for (int p = 0; p < h; ++p) {
+                        const float send = hi ? x[p] : x[p + h];
+                        const float keep = hi ? x[p + h] : x[p];
+                        x[p] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+                const float val = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+                const int q = (lane >> 3) & 3, c = (lane >> 1) & 3;
+                if ((lane & 1) == 0 && c < 3 && val != 0.f) {
+                    if (isfinite(val)) {
+                        atomicAdd(&a.acc_fx[3 * (int64_t)s[q] + c], (unsigned long long)to_fixed(val));
+                    } else if (a.nonfinite) {
+                        atomicOr(a.nonfinite, 1);
                     }
                 }
             }
