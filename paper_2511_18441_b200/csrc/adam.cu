@@ -236,9 +236,9 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
             }
             const double v1 = __shfl_down_sync(0xffffffffu, val, 1);
             const double v2 = __shfl_down_sync(0xffffffffu, val, 2);
-            if (rs >= 0 && part == 0) {
+            if (rs >= 0 && part == 0) {  // colours are stored by scene index
                 const int act = (val > 0.0) | ((v1 > 0.0) << 1) | ((v2 > 0.0) << 2);
-                next_color[rs] = make_float4((float)fmax(0.0, val), (float)fmax(0.0, v1), (float)fmax(0.0, v2),
+                next_color[g] = make_float4((float)fmax(0.0, val), (float)fmax(0.0, v1), (float)fmax(0.0, v2),
                                              __int_as_float(act));
             }
             __syncthreads();  // the tile is refilled below only after every reader is done

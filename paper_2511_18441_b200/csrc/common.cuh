@@ -134,15 +134,16 @@ struct rcgs_view {
     int tiles_x, tiles_y, sort_bits;
     bool full_sort;       // depth order from the full 64-bit keys (fallback path)
     // per kept rank s (front to back)
-    uint32_t* gid;        // (k,) scene index
-    double* z;            // (k,) view-space z (bit-exact reference depth)
-    RasterRec* rec;       // (k,)
-    ExactRec* exact;      // (k,)
+    uint32_t* gid;        // (k,) scene index g of depth rank s
+    // per gaussian, by scene index g (written for kept gaussians only)
+    double* z;            // (n,) view-space z (bit-exact reference depth)
+    RasterRec* rec;       // (n,)
+    ExactRec* exact;      // (n,)
     uint32_t* offs;       // (k+1,) first emission slot of s; offs[k] = pairs
-    float4* color;        // (k,) rgb + active bits (as float 0..7) per step
+    float4* color;        // (n,) rgb + active bits (as float 0..7) per step
     int32_t* rank_of;     // (n,) s or -1 (culled)
     // per pair (sorted by tile, then depth)
-    uint32_t* pair_s;     // (pairs,) rank s
+    uint32_t* pair_g;     // (pairs,) scene index g
     uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)

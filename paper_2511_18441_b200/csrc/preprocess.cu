@@ -10,14 +10,18 @@
 //
 // Pipeline per view (one handle):
 //   k1_cull      per gaussian: fp64 projection -> kept flag + z key (+ key min/max)
+//                and, for kept gaussians, the raster + exact records, z, footprint
+//                tile rect and tile count, all by scene index g
 //   scan/compact stable list of kept scene indices (ascending index)
 //   radix sort   stable LSD sort of the z bit patterns over their varying bits
-//                (== np.argsort(z, kind="stable"), render.py:216)
-//   k1_record    per rank s: raster record, exact record, z, tile rect, count
+//                (== np.argsort(z, kind="stable"), render.py:216) -> gid[s]
+//   k1_rank      rank_of[g] = s, tile counts in depth order
 //   scan         emission offsets offs[s] (pairs emitted in rank order)
-//   k2_emit      one (tile, e) pair per overlapped tile
+//   k2_emit      one (tile, g) pair per overlapped tile, in depth order
 //   radix sort   stable sort on tile id -> (tile, depth) order
-//   k2_ranges    per-tile [start, end) + rank/e lookup per pair
+//   k2_ranges    per-tile [start, end) + scene index per pair
+// Records are stored by scene index: tile lists carry g, so no pass is needed to
+// lay them out in depth order (nothing reads them in that order).
 #include <cuda_fp16.h>
 #include <math.h>
 
@@ -25,6 +29,10 @@
 #include "shmath.cuh"
 
 namespace rcgs {
+
+struct Rect {
+    int16_t x0, y0, x1, y1;  // inclusive tile rect; x1 < x0 => empty
+};
 
 struct ProjF64 {
     bool kept;
@@ -124,20 +132,77 @@ __global__ void cov3d_kernel(const double* __restrict__ rot, const double* __res
 
 // ---------------------------------------------------------------- K1a cull + keys
 __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __restrict__ cov3d,
-                               int64_t n, rcgs_camera cam, rcgs_raster_config cfg,
-                               uint32_t* __restrict__ flag, uint64_t* __restrict__ key,
-                               unsigned long long* __restrict__ minmax, ProjF64* __restrict__ proj) {
+                               const double* __restrict__ opac, int64_t n, rcgs_camera cam,
+                               rcgs_raster_config cfg, uint32_t* __restrict__ flag, uint64_t* __restrict__ key,
+                               unsigned long long* __restrict__ minmax, double* __restrict__ z_out,
+                               RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
+                               Rect* __restrict__ rect, uint32_t* __restrict__ count) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (g < n) {
-        ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
+        const ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
         flag[g] = p.kept ? 1u : 0u;
         uint64_t k = (uint64_t)__double_as_longlong(p.z);  // z > near_clip > 0: bits order like values
         key[g] = k;
         if (p.kept) {
             kmin = k;
             kmax = k;
-            proj[g] = p;  // reused by k1_record (no second fp64 projection)
+            z_out[g] = p.z;
+            // raster + exact records, footprint tile rect and tile count, by scene index
+            const double op = opac[g];
+            // conic = inverse(cov2d) (render.py:221-223)
+            const double ca = __ddiv_rn(p.c, p.det), cb = __ddiv_rn(-p.b, p.det), cc = __ddiv_rn(p.a, p.det);
+            ExactRec ex;
+            ex.mx = p.mx;
+            ex.my = p.my;
+            ex.ca = ca;
+            ex.cb = cb;
+            ex.cc = cc;
+            ex.op = op;
+            exact[g] = ex;
+
+            // alpha >= skip  <=>  power >= P := log(skip / op).  The fp32 power error is bounded
+            // by |power| * 2 / (1 - |rho|) * 5.4e-7 (rho = conic correlation); with a 4x safety
+            // factor kappa = 4.4e-6 / (1 - |rho|) and the exact-check band is P -+ |P| kappa.
+            const double P = log(cfg.alpha_skip / op);
+            const double rho = fmin(fabs(cb) / sqrt(ca * cc), 0.999999);
+            const double kappa = 4.4e-6 / (1.0 - rho);
+            const double margin = fabs(P) * kappa + 1e-6;
+            // opacity-aware footprint: alpha >= skip inside d^T conic d <= r2 = 2 ln(op/skip);
+            // axis half widths r * sqrt(cov2d diag), padded for fp64 rounding.
+            const double r2 = -2.0 * P;
+            const double ex_ = r2 >= 0.0 ? sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4 : 0.0;
+            const double ey_ = r2 >= 0.0 ? sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4 : 0.0;
+            // half extents rounded up to fp16 (+0.01 px) for the raster's sub-tile culling
+            const __half hx = __float2half_ru((float)fmin(ex_ + 0.01, 60000.0));
+            const __half hy = __float2half_ru((float)fmin(ey_ + 0.01, 60000.0));
+            const unsigned packed = (unsigned)__half_as_ushort(hx) | ((unsigned)__half_as_ushort(hy) << 16);
+            RasterRec r;
+            const float mxh = (float)p.mx, myh = (float)p.my;
+            r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
+            r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
+                              (float)(P + margin));
+            // c.w = kappa + 2e-7: the raster's per-composite error term |power| c.w + 6e-7
+            r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)(kappa + 2e-7));
+            rec[g] = r;
+
+            Rect rc;
+            rc.x0 = 0;
+            rc.y0 = 0;
+            rc.x1 = -1;
+            rc.y1 = -1;
+            if (r2 >= 0.0) {
+                const double umin = fmax(ceil(p.mx - ex_), 0.0), umax = fmin(floor(p.mx + ex_), cam.width - 1.0);
+                const double vmin = fmax(ceil(p.my - ey_), 0.0), vmax = fmin(floor(p.my + ey_), cam.height - 1.0);
+                if (umin <= umax && vmin <= vmax) {
+                    rc.x0 = (int16_t)((int)umin / kTile);
+                    rc.x1 = (int16_t)((int)umax / kTile);
+                    rc.y0 = (int16_t)((int)vmin / kTile);
+                    rc.y1 = (int16_t)((int)vmax / kTile);
+                }
+            }
+            rect[g] = rc;
+            count[g] = rc.x1 >= rc.x0 ? (uint32_t)(rc.x1 - rc.x0 + 1) * (uint32_t)(rc.y1 - rc.y0 + 1) : 0u;
         }
     }
     // block min/max -> one atomic per warp
@@ -222,103 +287,41 @@ __global__ void depth_check_kernel(const uint32_t* __restrict__ k32, const uint3
 }
 
 // ---------------------------------------------------------------- K1b records
-struct Rect {
-    int16_t x0, y0, x1, y1;  // inclusive tile rect; x1 < x0 => empty
-};
-
-__global__ void k1_record_kernel(const ProjF64* __restrict__ proj, const double* __restrict__ opac,
-                                 const uint32_t* __restrict__ sgid, int64_t k, rcgs_camera cam,
-                                 rcgs_raster_config cfg, int tiles_x, int tiles_y,
-                                 uint32_t* __restrict__ gid_out, double* __restrict__ z_out,
-                                 RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
-                                 int32_t* __restrict__ rank_of, Rect* __restrict__ rect,
-                                 uint32_t* __restrict__ count) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Depth rank s of each kept gaussian: rank_of[g] = s, and its tile count in
+// depth order (the emission-offset scan runs in depth order).
+__global__ void k1_rank_kernel(const uint32_t* __restrict__ gid, int64_t k, const uint32_t* __restrict__ count_g,
+                               int32_t* __restrict__ rank_of, uint32_t* __restrict__ count_s) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
-    const uint32_t g = sgid[s];
-    const ProjF64 p = proj[g];
-    gid_out[s] = g;
-    z_out[s] = p.z;
+    const uint32_t g = gid[s];
     rank_of[g] = (int32_t)s;
-    const double op = opac[g];
-    // conic = inverse(cov2d) (render.py:221-223)
-    const double ca = __ddiv_rn(p.c, p.det), cb = __ddiv_rn(-p.b, p.det), cc = __ddiv_rn(p.a, p.det);
-    ExactRec ex;
-    ex.mx = p.mx;
-    ex.my = p.my;
-    ex.ca = ca;
-    ex.cb = cb;
-    ex.cc = cc;
-    ex.op = op;
-    exact[s] = ex;
-
-    // alpha >= skip  <=>  power >= P := log(skip / op).  The fp32 power error is bounded
-    // by |power| * 2 / (1 - |rho|) * 5.4e-7 (rho = conic correlation); with a 4x safety
-    // factor kappa = 4.4e-6 / (1 - |rho|) and the exact-check band is P -+ |P| kappa.
-    const double P = log(cfg.alpha_skip / op);
-    const double rho = fmin(fabs(cb) / sqrt(ca * cc), 0.999999);
-    const double kappa = 4.4e-6 / (1.0 - rho);
-    const double margin = fabs(P) * kappa + 1e-6;
-    // opacity-aware footprint: alpha >= skip inside d^T conic d <= r2 = 2 ln(op/skip);
-    // axis half widths r * sqrt(cov2d diag), padded for fp64 rounding.
-    const double r2 = -2.0 * P;
-    const double ex_ = r2 >= 0.0 ? sqrt(r2 * p.a) * (1.0 + 1e-7) + 1e-4 : 0.0;
-    const double ey_ = r2 >= 0.0 ? sqrt(r2 * p.c) * (1.0 + 1e-7) + 1e-4 : 0.0;
-    // half extents rounded up to fp16 (+0.01 px) for the raster's sub-tile culling
-    const __half hx = __float2half_ru((float)fmin(ex_ + 0.01, 60000.0));
-    const __half hy = __float2half_ru((float)fmin(ey_ + 0.01, 60000.0));
-    const unsigned packed = (unsigned)__half_as_ushort(hx) | ((unsigned)__half_as_ushort(hy) << 16);
-    RasterRec r;
-    const float mxh = (float)p.mx, myh = (float)p.my;
-    r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
-    r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
-                      (float)(P + margin));
-    // c.w = kappa + 2e-7: the raster's per-composite error term |power| c.w + 6e-7
-    r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)(kappa + 2e-7));
-    rec[s] = r;
-
-    Rect rc;
-    rc.x0 = 0;
-    rc.y0 = 0;
-    rc.x1 = -1;
-    rc.y1 = -1;
-    if (r2 >= 0.0) {
-        const double umin = fmax(ceil(p.mx - ex_), 0.0), umax = fmin(floor(p.mx + ex_), cam.width - 1.0);
-        const double vmin = fmax(ceil(p.my - ey_), 0.0), vmax = fmin(floor(p.my + ey_), cam.height - 1.0);
-        if (umin <= umax && vmin <= vmax) {
-            rc.x0 = (int16_t)((int)umin / kTile);
-            rc.x1 = (int16_t)((int)umax / kTile);
-            rc.y0 = (int16_t)((int)vmin / kTile);
-            rc.y1 = (int16_t)((int)vmax / kTile);
-        }
-    }
-    rect[s] = rc;
-    count[s] = rc.x1 >= rc.x0 ? (uint32_t)(rc.x1 - rc.x0 + 1) * (uint32_t)(rc.y1 - rc.y0 + 1) : 0u;
+    count_s[s] = count_g[g];
 }
 
 // ---------------------------------------------------------------- K2 emission
-__global__ void k2_emit_kernel(const Rect* __restrict__ rect, const uint32_t* __restrict__ offs,
-                               int64_t k, int tiles_x, uint32_t* __restrict__ tile_key,
-                               uint32_t* __restrict__ emit_s) {
+__global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __restrict__ rect,
+                               const uint32_t* __restrict__ offs, int64_t k, int tiles_x,
+                               uint32_t* __restrict__ tile_key, uint32_t* __restrict__ emit_g) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
-    Rect rc = rect[s];
+    const uint32_t g = gid[s];
+    const Rect rc = rect[g];
     uint32_t e = offs[s];
     for (int ty = rc.y0; ty <= rc.y1; ++ty)
         for (int tx = rc.x0; tx <= rc.x1; ++tx) {
             tile_key[e] = (uint32_t)(ty * tiles_x + tx);
-            emit_s[e] = (uint32_t)s;
+            emit_g[e] = g;
             ++e;
         }
 }
 
 __global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key,
                                  const uint32_t* __restrict__ pair_e,
-                                 const uint32_t* __restrict__ emit_s, int64_t pairs,
-                                 uint2* __restrict__ ranges, uint32_t* __restrict__ pair_s) {
+                                 const uint32_t* __restrict__ emit_g, int64_t pairs,
+                                 uint2* __restrict__ ranges, uint32_t* __restrict__ pair_g) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= pairs) return;
-    pair_s[j] = emit_s[pair_e[j]];
+    pair_g[j] = emit_g[pair_e[j]];
     uint32_t t = tile_key[j];
     if (j == 0 || tile_key[j - 1] != t) ranges[t].x = (uint32_t)j;
     if (j == pairs - 1 || tile_key[j + 1] != t) ranges[t].y = (uint32_t)(j + 1);
@@ -374,8 +377,7 @@ __global__ void color_kernel(const double* __restrict__ pos, const float4* __res
                              float4* __restrict__ color) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    const int32_t s = rank_of[g];
-    if (s < 0) return;
+    if (rank_of[g] < 0) return;  // culled in this view
     double x, y, z;
     view_dir(pos, g, cen.c, x, y, z);
     double b[16];
@@ -405,7 +407,7 @@ __global__ void color_kernel(const double* __restrict__ pos, const float4* __res
         act |= (v > 0.0) << ch;
         col[ch] = (float)fmax(0.0, v);
     }
-    color[s] = make_float4(col[0], col[1], col[2], __int_as_float(act));
+    color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
 }
 
 __global__ void basis_export_kernel(const double* __restrict__ pos, const uint32_t* __restrict__ gid,
@@ -421,7 +423,7 @@ __global__ void basis_export_kernel(const double* __restrict__ pos, const uint32
         for (int i = 0; i < 16; ++i) basis[16 * s + i] = b[i];
     }
     if (active) {
-        const int a = __float_as_int(color[s].w);
+        const int a = __float_as_int(color[gid[s]].w);
         active[3 * s] = a & 1;
         active[3 * s + 1] = (a >> 1) & 1;
         active[3 * s + 2] = (a >> 2) & 1;
@@ -434,7 +436,7 @@ __global__ void kept_export_kernel(const uint32_t* __restrict__ gid, const doubl
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
     if (idx_out) idx_out[s] = gid[s];
-    if (z_out) z_out[s] = z[s];
+    if (z_out) z_out[s] = z[gid[s]];
 }
 
 static int validate_camera(const rcgs_camera* cam) {
@@ -497,7 +499,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->offs, s);
     dfree(v->color, s);
     dfree(v->rank_of, s);
-    dfree(v->pair_s, s);
+    dfree(v->pair_g, s);
     dfree(v->pair_e, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
@@ -530,22 +532,27 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         RCGS_CUDA(cudaMemsetAsync(v->offs, 0, sizeof(uint32_t), s));
         return RCGS_OK;
     }
-    // ---- K1a: cull + keys
-    uint32_t *flag = nullptr, *kpos = nullptr, *kgid = nullptr, *kgid_alt = nullptr;
+    // ---- K1: cull, keys and (for kept gaussians) the records, by scene index
+    uint32_t *flag = nullptr, *kpos = nullptr, *kgid = nullptr, *kgid_alt = nullptr, *count_g = nullptr;
     uint64_t *key = nullptr, *kkey = nullptr, *kkey_alt = nullptr;
     unsigned long long* minmax = nullptr;
+    Rect* rect = nullptr;
     RCGS_TRY(dalloc(&flag, n, s));
     RCGS_TRY(dalloc(&kpos, n + 1, s));
     RCGS_TRY(dalloc(&key, n, s));
     RCGS_TRY(dalloc(&minmax, 2, s));
-    ProjF64* proj = nullptr;
-    RCGS_TRY(dalloc(&proj, n, s));
+    RCGS_TRY(dalloc(&v->z, n, s));
+    RCGS_TRY(dalloc(&v->rec, n, s));
+    RCGS_TRY(dalloc(&v->exact, n, s));
+    RCGS_TRY(dalloc(&v->color, n, s));
+    RCGS_TRY(dalloc(&rect, n, s));
+    RCGS_TRY(dalloc(&count_g, n, s));
     {
         unsigned long long init[2] = {~0ull, 0ull};
         RCGS_CUDA(cudaMemcpyAsync(minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
-    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, n, v->cam, v->cfg, flag, key, minmax,
-                                                  proj);
+    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, sc->opac, n, v->cam, v->cfg, flag, key,
+                                                  minmax, v->z, v->rec, v->exact, rect, count_g);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
     uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));
@@ -564,7 +571,8 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(kpos, s);
         dfree(key, s);
         dfree(minmax, s);
-        dfree(proj, s);
+        dfree(rect, s);
+        dfree(count_g, s);
         return RCGS_OK;
     }
     RCGS_TRY(dalloc(&kkey, k, s));
@@ -611,22 +619,13 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     dfree(kkey, s);
     dfree(kkey_alt, s);
     dfree(kgid_alt, s);
-    // ---- K1b records
-    Rect* rect = nullptr;
+    // ---- depth ranks: gid[s] (the sorted scene indices), rank_of, counts in depth order
+    v->gid = kgid;
     uint32_t* count = nullptr;
-    RCGS_TRY(dalloc(&v->gid, k, s));
-    RCGS_TRY(dalloc(&v->z, k, s));
-    RCGS_TRY(dalloc(&v->rec, k, s));
-    RCGS_TRY(dalloc(&v->exact, k, s));
-    RCGS_TRY(dalloc(&v->color, k, s));
-    RCGS_TRY(dalloc(&rect, k, s));
     RCGS_TRY(dalloc(&count, k, s));
-    k1_record_kernel<<<div_up(k, 256), 256, 0, s>>>(proj, sc->opac, kgid, k, v->cam, v->cfg, v->tiles_x,
-                                                    v->tiles_y, v->gid, v->z, v->rec, v->exact, v->rank_of,
-                                                    rect, count);
+    k1_rank_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, k, count_g, v->rank_of, count);
     RCGS_LAUNCH_CHECK();
-    dfree(kgid, s);
-    dfree(proj, s);
+    dfree(count_g, s);
     RCGS_TRY(exclusive_scan_u32(count, v->offs, k, s));
     uint32_t* hp = reinterpret_cast<uint32_t*>(host);
     RCGS_CUDA(cudaMemcpyAsync(hp, v->offs + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -634,32 +633,31 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_CUDA(cudaStreamSynchronize(s));
     const int64_t pairs = hp[0];
     dfree(fix_flag, s);
+    dfree(count, s);
     if (hp[1] != 0) {  // a long tie run needs the full 64-bit key sort: rebuild
-        dfree(count, s);
         dfree(rect, s);
         return kRetryFullSort;
     }
     v->pairs = pairs;
-    dfree(count, s);
     if (pairs == 0) {
         dfree(rect, s);
         return RCGS_OK;
     }
-    // ---- K2 emit + stable tile sort
-    uint32_t *tkey = nullptr, *tkey_alt = nullptr, *emit_s = nullptr, *pe = nullptr, *pe_alt = nullptr;
+    // ---- K2 emit (depth order, values = scene index) + stable tile sort
+    uint32_t *tkey = nullptr, *tkey_alt = nullptr, *emit_g = nullptr, *pe = nullptr, *pe_alt = nullptr;
     RCGS_TRY(dalloc(&tkey, pairs, s));
     RCGS_TRY(dalloc(&tkey_alt, pairs, s));
-    RCGS_TRY(dalloc(&emit_s, pairs, s));
+    RCGS_TRY(dalloc(&emit_g, pairs, s));
     RCGS_TRY(dalloc(&pe, pairs, s));
     RCGS_TRY(dalloc(&pe_alt, pairs, s));
-    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(rect, v->offs, k, v->tiles_x, tkey, emit_s);
+    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g);
     RCGS_LAUNCH_CHECK();
     dfree(rect, s);
     int tile_bits = 1;
     while ((1 << tile_bits) < ntiles) ++tile_bits;
     RCGS_TRY(radix_sort_u32(&tkey, &tkey_alt, &pe, &pe_alt, true, pairs, tile_bits, s));
-    RCGS_TRY(dalloc(&v->pair_s, pairs, s));
-    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pe, emit_s, pairs, v->ranges, v->pair_s);
+    RCGS_TRY(dalloc(&v->pair_g, pairs, s));
+    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pe, emit_g, pairs, v->ranges, v->pair_g);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
     tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order);
@@ -668,7 +666,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     dfree(pe_alt, s);
     dfree(tkey, s);
     dfree(tkey_alt, s);
-    dfree(emit_s, s);
+    dfree(emit_g, s);
     return RCGS_OK;
 }
 

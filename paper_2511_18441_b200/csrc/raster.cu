@@ -62,7 +62,8 @@ __device__ __forceinline__ long long to_fixed(float v) {
 struct RasterArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // work order (nullptr: row-major)
-    const uint32_t* pair_s;
+    const uint32_t* pair_g;  // tile lists: scene indices in depth order
+    const int32_t* rank_of;  // scene index -> depth rank (capture output)
     const RasterRec* rec;
     const ExactRec* exact;
     const float4* color;
@@ -167,7 +168,7 @@ __device__ __forceinline__ float cull_power(const float4 ra, const float4 rb, co
 // the reference's.  32 lanes x 4 entries in flight per round instead of one
 // lane walking up to a few thousand entries with a dependent fp64 exp each
 // (those serial re-walks were the launch tail: one warp busy for 0.7 ms).
-__device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair_s,
+__device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair_g,
                                             const RasterRec* __restrict__ rec,
                                             const ExactRec* __restrict__ exact, double clamp, double skip,
                                             uint32_t j0, uint32_t j1, float uf, float vf, int lane) {
@@ -179,7 +180,7 @@ __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair
 #pragma unroll
         for (int q = 0; q < kU; ++q) {
             const uint32_t j = c + q * 32 + lane;
-            sv[q] = j <= j1 ? pair_s[j] : 0xffffffffu;
+            sv[q] = j <= j1 ? pair_g[j] : 0xffffffffu;
         }
         bool live[kU];
 #pragma unroll
@@ -304,7 +305,7 @@ __device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const floa
 struct WarpStage {
     float4 a[32], b[32], c[32];
     float4 col[32];
-    uint32_t s[32], j[32];
+    uint32_t g[32], j[32];  // entry: scene index, tile-list position
 };
 
 // kInstr: the instrumented variant (work counters / per-item trace); production
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
             uint32_t s = 0;
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
             if (j < range.y) {
-                s = a.pair_s[j];
+                s = a.pair_g[j];
                 ra = a.rec[s].a;
                 keep = touches_block(ra, fbx0, fby0);
                 if (keep) {
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 st.a[slot] = ra;
                 st.b[slot] = rb;
                 st.c[slot] = rc;
-                st.s[slot] = s;
+                st.g[slot] = s;
                 st.j[slot] = j;
                 if (kFwd) st.col[slot] = a.color[s];
             }
@@ -400,12 +401,12 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                     n_eval += !done;
                     ++n_iter;
                 }
-                if (!done) r = step<M>(st.a[k], st.b[k], st.c[k], st.s[k], px, a, &w);
+                if (!done) r = step<M>(st.a[k], st.b[k], st.c[k], st.g[k], px, a, &w);
                 // ambiguous threshold tests: exact transmittance, one pixel at a time, by the warp
                 for (unsigned amb = __ballot_sync(0xffffffffu, r == AMBIG); amb; amb &= amb - 1) {
                     const int L = __ffs(amb) - 1;
                     const float lu = __shfl_sync(0xffffffffu, px.uf, L), lv = __shfl_sync(0xffffffffu, px.vf, L);
-                    const double T64 = warp_exact_T(a.pair_s, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, range.x,
+                    const double T64 = warp_exact_T(a.pair_g, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, range.x,
                                                     st.j[k], lu, lv, lane);
                     if (lane == L) r = resolve<M>(T64, px, a);
                     ++n_resync;
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                 if (!done) {
                     if (r == STOP) done = true;
                     if (r == CROSS) {
-                        cross = (int32_t)st.s[k];
+                        cross = (int32_t)st.g[k];
                         done = true;
                     }
                 }
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                         // writes here, offset-dependent loads in the readers.)
                         const int64_t slot = rbase + nrec++;
                         a.wrec_w[slot * 32 + lane] = comp ? w : 0.f;
-                        if (lane == 0) a.wrec_s[slot] = st.s[k];
+                        if (lane == 0) a.wrec_s[slot] = st.g[k];
                     }
                 } else if (M == CAP_COUNT) {
                     ncap += comp;
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                     if (comp) {
                         const uint32_t o = cap_base + ncap++;
                         a.cap_pixel[o] = pix;
-                        a.cap_kept[o] = st.s[k];
+                        a.cap_kept[o] = a.rank_of[st.g[k]];  // the API reports depth ranks
                         a.cap_weight[o] = (double)w;
                     }
                 } else if (M == BWD) {
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                         if ((lane & 7) == 0 && lane < 24) {
                             if (isfinite(val)) {
                                 const long long q = to_fixed(val);
-                                atomicAdd(&a.acc_fx[3 * (int64_t)st.s[k] + (lane >> 3)], (unsigned long long)q);
+                                atomicAdd(&a.acc_fx[3 * (int64_t)st.g[k] + (lane >> 3)], (unsigned long long)q);
                             } else if (a.nonfinite) {
                                 atomicOr(a.nonfinite, 1);
                             }
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
                         if (lane == 0) {
-                            const uint32_t g = a.gid[st.s[k]];
+                            const uint32_t g = st.g[k];
                             atomicAdd(&a.hits[g], __popc(hb));
                             atomicAdd(&a.wsum[g], (unsigned long long)llrint((double)ws * 4294967296.0));
                         }
@@ -739,7 +740,8 @@ static RasterArgs base_args(const rcgs_view* v) {
     memset(&a, 0, sizeof(a));
     a.ranges = v->ranges;
     a.tile_order = v->tile_order;
-    a.pair_s = v->pair_s;
+    a.pair_g = v->pair_g;
+    a.rank_of = v->rank_of;
     a.rec = v->rec;
     a.exact = v->exact;
     a.color = v->color;
@@ -922,26 +924,30 @@ extern "C" int rcgs_capture(const rcgs_view* v, int64_t* h_count, int64_t* d_pix
 }
 
 // acc[gid] = active * acc_fx[s] / 2^50 (fixed point -> fp32), zero for culled gaussians.
+// acc[g] = fixed-point sums -> fp32, masked by the colour clamp's active channels
+// (render.py:211-214); culled gaussians get 0.  Elementwise over the scene.
 __global__ void bwd_finish_kernel(const long long* __restrict__ acc_fx, const float4* __restrict__ color,
-                                  const uint32_t* __restrict__ gid, int64_t k, float* __restrict__ acc) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= k) return;
-    const int act = __float_as_int(color[s].w);
-    const uint32_t g = gid[s];
+                                  const int32_t* __restrict__ rank_of, int64_t n, float* __restrict__ acc) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int act = rank_of[g] >= 0 ? __float_as_int(color[g].w) : 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
-        acc[3 * (int64_t)g + ch] = ((act >> ch) & 1) ? (float)((double)acc_fx[3 * s + ch] / kFixScale) : 0.f;
+        acc[3 * g + ch] = ((act >> ch) & 1) ? (float)((double)acc_fx[3 * g + ch] / kFixScale) : 0.f;
 }
 
 extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, float* d_acc,
                              int32_t* d_nonfinite, void* stream) {
     RCGS_CHECK_ARG(v != nullptr && d_grad_image != nullptr && d_acc != nullptr, "null argument");
     cudaStream_t s = as_stream(stream);
-    if (v->n > 0) RCGS_CUDA(cudaMemsetAsync(d_acc, 0, 3 * v->n * sizeof(float), s));
-    if (v->k == 0) return RCGS_OK;
-    unsigned long long* acc_fx = nullptr;
-    RCGS_TRY(dalloc(&acc_fx, 3 * v->k, s));
-    RCGS_CUDA(cudaMemsetAsync(acc_fx, 0, 3 * v->k * sizeof(unsigned long long), s));
+    if (v->n == 0) return RCGS_OK;
+    if (v->k == 0) {
+        RCGS_CUDA(cudaMemsetAsync(d_acc, 0, 3 * v->n * sizeof(float), s));
+        return RCGS_OK;
+    }
+    unsigned long long* acc_fx = nullptr;  // by scene index (entries carry g)
+    RCGS_TRY(dalloc(&acc_fx, 3 * v->n, s));
+    RCGS_CUDA(cudaMemsetAsync(acc_fx, 0, 3 * v->n * sizeof(unsigned long long), s));
     if (v->pairs > 0 && records_valid(v)) {  // stream the recorded weights
         RecArgs ra = rec_args(v);
         ra.grad = d_grad_image;
@@ -955,8 +961,8 @@ extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, floa
         a.nonfinite = d_nonfinite;
         RCGS_TRY(launch<BWD>(a, s));
     }
-    bwd_finish_kernel<<<div_up(v->k, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(acc_fx), v->color,
-                                                        v->gid, v->k, d_acc);
+    bwd_finish_kernel<<<div_up(v->n, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(acc_fx), v->color,
+                                                        v->rank_of, v->n, d_acc);
     RCGS_LAUNCH_CHECK();
     dfree(acc_fx, s);
     return RCGS_OK;
