@@ -363,8 +363,9 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
         uint32_t n_eval = 0, n_comp = 0, n_iter = 0;
-        // FWDREC: this block's record slots, 8 per tile-list entry and block
-        const int64_t rbase = (int64_t)kBlocksPerTile * range.x + (int64_t)blk * (range.y - range.x);
+        // FWDREC: this block's record slots, 8 per tile-list entry and block (32-bit:
+        // the host checks 8 * pairs < 2^32)
+        const uint32_t rbase = kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x);
         uint32_t nrec = 0;
         for (uint32_t c0 = range.x; c0 < range.y; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
@@ -432,8 +433,8 @@ __global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
                         // composite): one coalesced 128-byte store.  (Packing only the
                         // composited weights measured slower both ways: partial-sector
                         // writes here, offset-dependent loads in the readers.)
-                        const int64_t slot = rbase + nrec++;
-                        a.wrec_w[slot * 32 + lane] = comp ? w : 0.f;
+                        const uint32_t slot = rbase + nrec++;
+                        a.wrec_w[(size_t)slot * 32 + lane] = comp ? w : 0.f;
                         if (lane == 0) a.wrec_s[slot] = st.g[k];
                     }
                 } else if (M == CAP_COUNT) {
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
             if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) continue;
         }
         const uint2 range = a.ranges[tile];
-        const int64_t base = (int64_t)kBlocksPerTile * range.x + (int64_t)blk * (range.y - range.x);
+        const uint32_t base = kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x);
         const uint32_t n = a.wrec_n[tile * kBlocksPerTile + blk];
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
         for (uint32_t r0 = 0; r0 < n; r0 += kU) {
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 const bool ok = r0 + q < n;
-                w[q] = ok ? __ldcs(a.wrec_w + (base + r0 + q) * 32 + lane) : 0.f;
+                w[q] = ok ? __ldcs(a.wrec_w + (size_t)(base + r0 + q) * 32 + lane) : 0.f;
                 s[q] = ok ? a.wrec_s[base + r0 + q] : 0u;
             }
 #pragma unroll
@@ -840,6 +841,7 @@ extern "C" int rcgs_render_train(rcgs_view* v, const float* h_bg, int layout, fl
     cudaStream_t s = as_stream(stream);
     const int64_t n_items = (int64_t)v->tiles_x * v->tiles_y * kBlocksPerTile;
     const int64_t cap = (int64_t)kBlocksPerTile * v->pairs;  // <= one record per entry and block
+    RCGS_CHECK_ARG(cap < ((int64_t)1 << 32), "too many tile-list entries for weight records");
     const int64_t npix = (int64_t)v->cam.width * v->cam.height;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t o_n = 0, o_s = up(o_n + 4 * n_items), o_w = up(o_s + 4 * cap), o_tf = up(o_w + 128 * cap);
