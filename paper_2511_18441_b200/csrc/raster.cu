@@ -310,8 +310,11 @@ struct WarpStage {
 
 // kInstr: the instrumented variant (work counters / per-item trace); production
 // launches carry no counter registers or checks in the entry loop.
+#ifndef RCGS_FWDREC_MIN_CTAS
+#define RCGS_FWDREC_MIN_CTAS 4
+#endif
 template <int M, bool kInstr>
-__global__ void __launch_bounds__(kCTA, kMinCTAs) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMinCTAs) raster_kernel(RasterArgs a) {
     constexpr bool kFwd = (M == FWD || M == FWDREC);
     constexpr int kRow = (M == FWDREC) ? (int)FWD : M;  // counter row
     __shared__ WarpStage stage_all[kWarpsPerCTA];
