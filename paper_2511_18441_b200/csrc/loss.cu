@@ -101,15 +101,21 @@ __global__ void __launch_bounds__(kLNT) loss_dirty_kernel(const T* __restrict__ 
                                                           int32_t* __restrict__ differ) {
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     int d = 0;
-    for (int i = threadIdx.x; i < kLT * kLT * 3; i += kLNT) {
-        const int p = i / 3, ch = i % 3;
-        const int gy = y0 + p / kLT, gx = x0 + p % kLT;
-        if (gy < H && gx < W) {
-            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
-            d |= y[o] != g[o];
+    // chunk by chunk with a block vote: a block that differs (every block, once the
+    // refit is under way) stops after its first chunk
+    for (int c0 = 0; c0 < kLT * kLT * 3 && !d; c0 += kLNT) {
+        const int i = c0 + threadIdx.x;
+        int di = 0;
+        if (i < kLT * kLT * 3) {
+            const int p = i / 3, ch = i % 3;
+            const int gy = y0 + p / kLT, gx = x0 + p % kLT;
+            if (gy < H && gx < W) {
+                const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+                di = y[o] != g[o];
+            }
         }
+        d = __syncthreads_or(di);
     }
-    d = __syncthreads_or(d);
     if (threadIdx.x == 0) {
         dirty[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)d;
         if (d) atomicOr(differ, 1);
@@ -262,7 +268,8 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
                 const double cov = m[4][i] * im - mu1 * mu2;
                 const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
                 const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
-                const double ib1 = 1.0 / b1, ib2 = 1.0 / b2, ib = ib1 * ib2;
+                // one fp64 division: 1/(b1 b2), then 1/b1 = b2 * that and 1/b2 = b1 * that
+                const double ib = 1.0 / (b1 * b2), ib1 = b2 * ib, ib2 = b1 * ib;
                 const double a12 = a1 * a2;
                 ss += a12 * ib;
                 const double d_mu1 = 2.0 * (mu2 * a2) * ib - 2.0 * mu1 * a12 * ib * ib1;
