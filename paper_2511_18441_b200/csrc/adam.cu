@@ -123,9 +123,9 @@ constexpr size_t kASmem = (size_t)kAStages * 3 * kATileBytes + kAStages * sizeof
 // elementwise update.
 __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
-    float* __restrict__ v, AccViews views, AdamHyper h, const float2* __restrict__ bc,
-    const int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of, Center next_cen,
-    float4* __restrict__ next_color) {
+    float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
+    unsigned* __restrict__ ticket, const int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
+    Center next_cen, float4* __restrict__ next_color) {
     // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
     // colour epilogue the next view is still coloured from the unchanged SH
     const bool upd = !(reject && *reject);
@@ -147,16 +147,20 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         for (int arr = 0; arr < 3; ++arr)
             bulk_load(smem_addr(stage_buf(s, arr)), arrays[arr] + g0 * 48, bytes, bar);
     };
+    __shared__ float2 s_bc;
     if (t == 0) {
         for (int s = 0; s < kAStages; ++s) mbar_init(smem_addr(&bars[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // bias corrections 1 / (1 - beta^t) for t = step + 1 (fp64 pow)
+        const double tt = (double)(*step + 1);
+        s_bc = make_float2((float)(1.0 / (1.0 - pow(db1, tt))), (float)(1.0 / (1.0 - pow(db2, tt))));
     }
     __syncthreads();
     if (t == 0) {
         for (int s = 0; s < kAStages; ++s)
             if ((int64_t)blockIdx.x + (int64_t)s * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
     }
-    const float2 ibc = *bc;
+    const float2 ibc = s_bc;
     const int gi = t >> 2, part = t & 3;  // gaussian in the tile, 12-coefficient quarter
     const float invn = 1.0f / (float)views.n;
     int it = 0;
@@ -252,7 +256,15 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
             }
         }
     }
-    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (t == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // the last block to finish (every block has read *step by then) commits the step
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            if (upd) *step += 1;
+            *ticket = 0;
+        }
+    }
 }
 
 __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
@@ -330,10 +342,8 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             av.acc[i] = h_d_accs[i];
             for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
         }
-        float2* bc = nullptr;
-        RCGS_TRY(dalloc(&bc, 1, s));
-        adam_prep_kernel<<<1, 1, 0, s>>>(d_step, cfg->beta1, cfg->beta2, bc);
         static int grid = 0;
+        static unsigned* ticket = nullptr;  // last-block ticket (reset by the last block)
         if (grid == 0) {
             int dev = 0, sms = 0, per_sm = 0;
             RCGS_CUDA(cudaGetDevice(&dev));
@@ -341,6 +351,8 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             RCGS_CUDA(cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kASmem));
             RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem));
+            RCGS_CUDA(cudaMalloc(&ticket, sizeof(unsigned)));
+            RCGS_CUDA(cudaMemset(ticket, 0, sizeof(unsigned)));
             grid = sms * (per_sm > 0 ? per_sm : 1);
         }
         const int64_t ntiles = (sc->n + kAG - 1) / kAG;
@@ -352,10 +364,12 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             nrank = next_view->rank_of;
             ncolor = next_view->color;
         }
+        // bias corrections from and commit of the device step counter happen inside
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
-            sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), bc, d_reject, nrank, nc, ncolor);
+            sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
+            d_reject, nrank, nc, ncolor);
         RCGS_LAUNCH_CHECK();
-        dfree(bc, s);
+        return RCGS_OK;
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
     RCGS_LAUNCH_CHECK();

@@ -147,6 +147,7 @@ struct rcgs_view {
     uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
+    unsigned* work;       // (2,) work-item / exited-warp counters of the persistent launches
     // composite-weight records (rcgs_render_train; geometry + camera only), in the
     // process-wide record arena (raster.cu) while this view owns it
     bool wrec_valid;

@@ -503,6 +503,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->pair_e, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
+    dfree(v->work, s);
     release_records(v);  // records live in the raster's arena, not in the view
     v->wrec_n = v->wrec_s = nullptr;
     v->wrec_w = v->wrec_tf = nullptr;
@@ -522,6 +523,8 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     const int ntiles = v->tiles_x * v->tiles_y;
     RCGS_TRY(dalloc(&v->rank_of, n, s));
     RCGS_TRY(dalloc(&v->ranges, ntiles, s));
+    RCGS_TRY(dalloc(&v->work, 2, s));
+    RCGS_CUDA(cudaMemsetAsync(v->work, 0, 2 * sizeof(unsigned), s));
     if (n > 0) RCGS_CUDA(cudaMemsetAsync(v->rank_of, 0xff, n * sizeof(int32_t), s));
     RCGS_CUDA(cudaMemsetAsync(v->ranges, 0, ntiles * sizeof(uint2), s));
     v->k = 0;

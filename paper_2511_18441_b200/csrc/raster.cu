@@ -135,6 +135,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Persistent launches pull work items from ctr[0]; the last warp to exit resets
+// ctr[0..1] for the next launch on the view (ctr[1] counts exited warps), so no
+// per-launch allocation or memset is needed.
+__device__ __forceinline__ void work_counter_exit(unsigned* ctr, int lane) {
+    if (lane == 0 && atomicAdd(&ctr[1], 1u) == gridDim.x * (blockDim.x >> 5) - 1) {
+        ctr[0] = 0;
+        ctr[1] = 0;
+    }
+}
+
 // Reference alpha in fp64 with numpy's operation order (render.py:265-271).
 __device__ __forceinline__ double exact_alpha(const ExactRec& r, double u, double v, double clamp,
                                               double skip) {
@@ -543,6 +553,7 @@ __global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMi
             a.cap_count[pix] = ncap;
         }
     }
+    work_counter_exit(a.counter, lane);
 }
 
 // ---------------------------------------------------------------- weight records
@@ -674,6 +685,7 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
             if (a.t_final) a.t_final[pix] = T;
         }
     }
+    work_counter_exit(a.counter, lane);
 }
 
 template <bool kBwd>
@@ -686,13 +698,8 @@ static int launch_rec(RecArgs a, cudaStream_t s) {
         RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<true>, kCTA, 0));
         grid = sms * (per_sm > 0 ? per_sm : 1);
     }
-    unsigned* counter = nullptr;
-    RCGS_TRY(dalloc(&counter, 1, s));
-    RCGS_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
-    a.counter = counter;
     const int blocks = (int)min((int64_t)grid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
     if (blocks > 0) rec_kernel<kBwd><<<blocks, kCTA, 0, s>>>(a);
-    dfree(counter, s);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }
@@ -727,6 +734,7 @@ static RecArgs rec_args(const rcgs_view* v) {
     memset(&a, 0, sizeof(a));
     a.ranges = v->ranges;
     a.tile_order = v->tile_order;
+    a.counter = v->work;
     a.W = v->cam.width;
     a.H = v->cam.height;
     a.tiles_x = v->tiles_x;
@@ -746,6 +754,7 @@ static RasterArgs base_args(const rcgs_view* v) {
     a.tile_order = v->tile_order;
     a.pair_g = v->pair_g;
     a.rank_of = v->rank_of;
+    a.counter = v->work;
     a.rec = v->rec;
     a.exact = v->exact;
     a.color = v->color;
@@ -777,10 +786,6 @@ static int launch(RasterArgs a, cudaStream_t s) {
         RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_kernel<M, false>, kCTA, 0));
         grid[M] = sms * (per_sm > 0 ? per_sm : 1);
     }
-    unsigned* counter = nullptr;
-    RCGS_TRY(dalloc(&counter, 1, s));
-    RCGS_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
-    a.counter = counter;
     a.counters = g_counters;
     a.trace = (g_trace && g_trace_items >= a.n_items) ? g_trace : nullptr;
     const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
@@ -790,7 +795,6 @@ static int launch(RasterArgs a, cudaStream_t s) {
         else
             raster_kernel<M, false><<<blocks, kCTA, 0, s>>>(a);
     }
-    dfree(counter, s);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }
