@@ -588,7 +588,7 @@ struct RecArgs {
 template <bool kBwd>
 __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
     const int lane = threadIdx.x & 31;
-    constexpr int kU = 4;  // records in flight per warp
+    constexpr int kU = 8;  // records in flight per warp
     for (;;) {
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(a.counter, 1u);
@@ -635,11 +635,11 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                 }
             }
             if (kBwd) {
-                // the kU records' (w g) sums for 3 channels (+1 zero pad) = 16 values,
-                // halved across the warp: xor 16, 8, 4, 2 then a last xor 1 add, i.e.
-                // the butterfly tree of a plain warp sum (bit-identical totals) with 16
-                // shuffles per 4 records; lane L ends with record (L>>3)&3, channel (L>>1)&3
-                float x[16];
+                // the kU = 8 records' (w g) sums for 3 channels (+1 zero pad) = 32 values,
+                // halved across the warp: xor 16, 8, 4, 2, 1 -- the butterfly tree of a
+                // plain warp sum (bit-identical totals), 31 shuffles per 8 records; lane L
+                // ends with record L >> 2, channel L & 3
+                float x[32];
 #pragma unroll
                 for (int q = 0; q < kU; ++q) {
                     const bool comp = w[q] != 0.f;
@@ -649,18 +649,18 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                     x[4 * q + 3] = 0.f;
                 }
 #pragma unroll
-                for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
-                    const bool hi = lane & off;
+                for (int h = 16; h >= 1; h >>= 1) {
+                    const bool hi = lane & h;
 #pragma unroll
                     for (int p = 0; p < h; ++p) {
                         const float send = hi ? x[p] : x[p + h];
                         const float keep = hi ? x[p + h] : x[p];
-                        x[p] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                        x[p] = keep + __shfl_xor_sync(0xffffffffu, send, h);
                     }
                 }
-                const float val = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
-                const int q = (lane >> 3) & 3, c = (lane >> 1) & 3;
-                if ((lane & 1) == 0 && c < 3 && val != 0.f) {
+                const float val = x[0];
+                const int q = lane >> 2, c = lane & 3;
+                if (c < 3 && val != 0.f) {
                     if (isfinite(val)) {
                         atomicAdd(&a.acc_fx[3 * (int64_t)s[q] + c], (unsigned long long)to_fixed(val));
                     } else if (a.nonfinite) {
