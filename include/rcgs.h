@@ -118,6 +118,12 @@ int rcgs_render(const rcgs_view* view, const float* h_background3, int layout,
  * 8 * pairs * 132 bytes (~2.8 GB at 1080p / 1M gaussians), freed with the view. */
 int rcgs_render_train(rcgs_view* view, const float* h_bg3, int layout, float* d_image, float* d_t_final,
                       void* stream);
+/* Keep the composite weights recorded by rcgs_render_train resident with the
+ * view (a compact copy, ~130 B per record; ~314 MB at 1080p / 1M gaussians)
+ * instead of in the shared per-step arena: every later render / backward of the
+ * view streams them (views reused across steps, e.g. a refit over a fixed set of
+ * training cameras).  Synchronises `stream` once (record count). */
+int rcgs_view_keep_records(rcgs_view* view, void* stream);
 
 /* depth_from_gaussians (render.py:373-398): (H,W) fp64, +inf where T never drops
  * below tau at a composited gaussian.  d_cross (H,W) int32 = kept rank or -1, may be NULL. */

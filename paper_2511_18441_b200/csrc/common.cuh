@@ -86,7 +86,7 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_
 // vals_in may be null: values then start as the element index.
 int radix_sort_u64(uint64_t** key_cur, uint64_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
                    bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
-void release_records(const rcgs_view* v);  // raster.cu: drop the record-arena ownership
+void release_records(rcgs_view* v, cudaStream_t s);  // raster.cu: drop or free the view's weight records
 
 int radix_sort_u32(uint32_t** key_cur, uint32_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
                    bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
@@ -151,7 +151,9 @@ struct rcgs_view {
     // composite-weight records (rcgs_render_train; geometry + camera only), in the
     // process-wide record arena (raster.cu) while this view owns it
     bool wrec_valid;
+    bool wrec_owned;      // records copied out of the arena into view-owned memory
     uint64_t wrec_epoch;
+    uint32_t* wrec_off;   // (tiles * 8 + 1,) per-block first record (owned records only)
     uint32_t* wrec_n;     // (tiles * 8,) records per 8x4 block
     uint32_t* wrec_s;     // (8 * pairs,) entry (depth rank) per record slot
     float* wrec_w;        // (8 * pairs, 32) pixel weights per record slot

@@ -504,7 +504,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
     dfree(v->work, s);
-    release_records(v);  // records live in the raster's arena, not in the view
+    release_records(v, s);  // arena ownership, or the view-owned compact copy
     v->wrec_n = v->wrec_s = nullptr;
     v->wrec_w = v->wrec_tf = nullptr;
     v->wrec_valid = false;

@@ -572,6 +572,7 @@ struct RecArgs {
     const uint32_t* wrec_n;
     const uint32_t* wrec_s;
     const float* wrec_w;
+    const uint32_t* wrec_off;  // per-block first record (view-owned compact records) or null
     // render
     const float4* color;
     const float* t_in;
@@ -610,7 +611,8 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
             if (__all_sync(0xffffffffu, g0 == 0.f && g1 == 0.f && g2 == 0.f)) continue;
         }
         const uint2 range = a.ranges[tile];
-        const uint32_t base = kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x);
+        const uint32_t base = a.wrec_off ? a.wrec_off[tile * kBlocksPerTile + blk]
+                                         : kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x);
         const uint32_t n = a.wrec_n[tile * kBlocksPerTile + blk];
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
         for (uint32_t r0 = 0; r0 < n; r0 += kU) {
@@ -721,12 +723,39 @@ struct RecordArena {
 static RecordArena g_arena;
 
 static bool records_valid(const rcgs_view* v) {
-    return v->wrec_valid && g_arena.owner.load() == v && g_arena.epoch.load() == v->wrec_epoch;
+    return v->wrec_owned || (v->wrec_valid && g_arena.owner.load() == v && g_arena.epoch.load() == v->wrec_epoch);
 }
 
-void release_records(const rcgs_view* v) {
+void release_records(rcgs_view* v, cudaStream_t s) {
+    if (v->wrec_owned) {  // view-owned compact copy (rcgs_view_keep_records)
+        dfree(v->wrec_n, s);
+        dfree(v->wrec_s, s);
+        dfree(v->wrec_w, s);
+        dfree(v->wrec_tf, s);
+        dfree(v->wrec_off, s);
+        v->wrec_owned = false;
+        return;
+    }
     const rcgs_view* expect = v;
     g_arena.owner.compare_exchange_strong(expect, nullptr);
+}
+
+// Copy each block's records from the arena layout to a compact layout at the
+// scanned per-block offsets (one warp per block).
+__global__ void records_compact_kernel(const uint32_t* __restrict__ n_rec, const uint2* __restrict__ ranges,
+                                       int n_blocks, const uint32_t* __restrict__ src_s,
+                                       const float* __restrict__ src_w, const uint32_t* __restrict__ off,
+                                       uint32_t* __restrict__ dst_s, float* __restrict__ dst_w) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= n_blocks) return;
+    const uint2 range = ranges[b / kBlocksPerTile];
+    const uint32_t src = kBlocksPerTile * range.x + (uint32_t)(b % kBlocksPerTile) * (range.y - range.x);
+    const uint32_t dst = off[b], n = n_rec[b];
+    for (uint32_t r = 0; r < n; ++r) {
+        dst_w[(size_t)(dst + r) * 32 + lane] = src_w[(size_t)(src + r) * 32 + lane];
+        if (lane == 0) dst_s[dst + r] = src_s[src + r];
+    }
 }
 
 static RecArgs rec_args(const rcgs_view* v) {
@@ -742,6 +771,7 @@ static RecArgs rec_args(const rcgs_view* v) {
     a.wrec_n = v->wrec_n;
     a.wrec_s = v->wrec_s;
     a.wrec_w = v->wrec_w;
+    a.wrec_off = v->wrec_owned ? v->wrec_off : nullptr;
     a.color = v->color;
     a.t_in = v->wrec_tf;
     return a;
@@ -943,6 +973,41 @@ __global__ void bwd_finish_kernel(const long long* __restrict__ acc_fx, const fl
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
         acc[3 * g + ch] = ((act >> ch) & 1) ? (float)((double)acc_fx[3 * g + ch] / kFixScale) : 0.f;
+}
+
+extern "C" int rcgs_view_keep_records(rcgs_view* v, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr, "null view");
+    if (v->wrec_owned || v->pairs == 0) return RCGS_OK;
+    RCGS_CHECK_ARG(records_valid(v), "no weight records to keep (call rcgs_render_train first)");
+    cudaStream_t s = as_stream(stream);
+    const int n_blocks = v->tiles_x * v->tiles_y * kBlocksPerTile;
+    const int64_t npix = (int64_t)v->cam.width * v->cam.height;
+    uint32_t *off = nullptr, *rs = nullptr, *ntab = nullptr;
+    float *rw = nullptr, *tf = nullptr;
+    RCGS_TRY(dalloc(&off, n_blocks + 1, s));
+    RCGS_TRY(exclusive_scan_u32(v->wrec_n, off, n_blocks, s));
+    uint32_t* host = static_cast<uint32_t*>(pinned_scratch(sizeof(uint32_t)));
+    RCGS_CUDA(cudaMemcpyAsync(host, off + n_blocks, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaStreamSynchronize(s));
+    const int64_t total = *host;
+    RCGS_TRY(dalloc(&ntab, n_blocks, s));
+    RCGS_TRY(dalloc(&rs, total > 0 ? total : 1, s));
+    RCGS_TRY(dalloc(&rw, (total > 0 ? total : 1) * 32, s));
+    RCGS_TRY(dalloc(&tf, npix, s));
+    RCGS_CUDA(cudaMemcpyAsync(ntab, v->wrec_n, sizeof(uint32_t) * n_blocks, cudaMemcpyDeviceToDevice, s));
+    RCGS_CUDA(cudaMemcpyAsync(tf, v->wrec_tf, sizeof(float) * npix, cudaMemcpyDeviceToDevice, s));
+    records_compact_kernel<<<div_up(n_blocks, 8), 256, 0, s>>>(v->wrec_n, v->ranges, n_blocks, v->wrec_s, v->wrec_w,
+                                                              off, rs, rw);
+    RCGS_LAUNCH_CHECK();
+    release_records(v, s);  // the arena copy is no longer needed
+    v->wrec_n = ntab;
+    v->wrec_s = rs;
+    v->wrec_w = rw;
+    v->wrec_tf = tf;
+    v->wrec_off = off;
+    v->wrec_owned = true;
+    v->wrec_valid = true;
+    return RCGS_OK;
 }
 
 extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, float* d_acc,

@@ -174,6 +174,13 @@ class View:
                N.ptr(tf), stream_ptr())
         return (img, tf) if t_final else img
 
+    def keep_records(self):
+        """Keep the composite weights recorded by a train render resident with the
+        view (rcgs_view_keep_records): later renders / backwards stream them."""
+        if not getattr(self, "_records_kept", False):
+            N.call("rcgs_view_keep_records", self.handle, stream_ptr())
+            self._records_kept = True
+
     def depth(self, tau: float = 0.5, with_cross: bool = False):
         d = torch.empty((self.height, self.width), dtype=torch.float64, device=device())
         c = torch.empty((self.height, self.width), dtype=torch.int32, device=device()) if with_cross else None

@@ -282,6 +282,8 @@ class RefitEngine:
         if ev:
             ev[1].record()
         view.render(None, 0, out=img, train=True)
+        if self.cache_views:  # resident views also keep their weights (SpMV from then on)
+            view.keep_records()
         target = self.targets[mine]
         if not target.is_cuda:           # streamed dataset: H2D of this step's target
             tgt_buf.copy_(target, non_blocking=True)

@@ -520,3 +520,31 @@ def test_weight_records_bit_identical():
         assert torch.equal(ref.backward(g), rec.backward(g))
         ref.close()
         rec.close()
+
+
+def test_kept_records_bit_identical():
+    """A view whose weights were copied into view-owned memory renders (SpMV) and
+    back-propagates exactly like the traversal paths, also after another view has
+    recorded into the shared arena."""
+    import sys
+    import torch
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2511_18441_b200 import device as D
+    cfg = dict(n=30_000, deg=3, views=2, width=320, height=256)
+    scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
+    sh = sh0 + 0.01 * torch.randn_like(sh0)
+    (i0, p0), (i1, p1) = cams
+    ref = D.View(ds, i0, p0, P.DEFAULT_CONFIG).color(sh)
+    kept = D.View(ds, i0, p0, P.DEFAULT_CONFIG).color(sh)
+    img_ref = ref.render(None, 0)
+    assert torch.equal(kept.render(None, 0, train=True), img_ref)
+    kept.keep_records()
+    other = D.View(ds, i1, p1, P.DEFAULT_CONFIG).color(sh)
+    other.render(None, 0, train=True)  # takes over the shared arena
+    assert torch.equal(kept.render(None, 0), img_ref)
+    assert torch.equal(kept.render(None, 0, train=True), img_ref)
+    g = torch.randn_like(img_ref) * 1e-3
+    assert torch.equal(kept.backward(g), ref.backward(g))
+    for v in (ref, kept, other):
+        v.close()
