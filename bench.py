@@ -543,8 +543,9 @@ def run_selection_sweep(group, world, rank, dev):
 
 def run_e2e(args, scene, cams, sp, group, world):
     """Same metric through the public API: BackgroundOptimizer with the targets
-    in pinned host memory (one H2D per step) and the step's metrics read back
-    every step (snapshot_every=1)."""
+    in pinned host memory (one H2D per step, uploaded by the view prefetcher on
+    its stream) and every step's metrics read back to the host (non-blocking,
+    one step behind: _flush(wait=False)); SH snapshots at the default cadence."""
     import torch
     import paper_2511_18441_b200 as P
     from types import SimpleNamespace
@@ -554,7 +555,7 @@ def run_e2e(args, scene, cams, sp, group, world):
     views = tuple(P.EditedView(view=SimpleNamespace(view_id=i, intrinsics=cams[i][0], pose=cams[i][1]),
                                mask=masks[i], image=edited[i].numpy()) for i in range(len(cams)))
     ds = P.EditedDataset(views=views, generation=0, tint=np.array([1.0, 0.2, 0.2]))
-    cfg = P.OptimizerConfig(snapshot_every=1)
+    cfg = P.OptimizerConfig()
     opt = P.BackgroundOptimizer(scene, ds, cfg, seed=7, group=group, cache_views=False, stream_targets=True,
                                 prefetch=2)
     opt.run_iterations(args.warmup)
@@ -564,7 +565,8 @@ def run_e2e(args, scene, cams, sp, group, world):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         opt._step()
-        opt._flush()
+        opt._flush(wait=False)
+    opt._flush()  # the last steps' metrics
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     dt = sync_max(dt, world)
@@ -572,7 +574,8 @@ def run_e2e(args, scene, cams, sp, group, world):
     h, w = edited.shape[1], edited.shape[2]
     return {"value": round(world * args.steps / dt, 3), "unit": "view-steps/s",
             "h2d_bytes_per_step": int(h * w * 3 * 4), "d2h_bytes_per_step": 32,
-            "api": "BackgroundOptimizer(stream_targets=True), metrics read back every step"}
+            "api": "BackgroundOptimizer(stream_targets=True): target H2D every step on the prefetch stream, "
+                   "metrics D2H every step (pipelined one step)"}
 
 
 # ----------------------------------------------------------------------------- CPU reference arm

@@ -52,9 +52,17 @@ class ViewPrefetcher:
     for 30-800 ms when views were freed on the consumer stream instead.
     """
 
-    def __init__(self, dscene, cameras, raster, device, profile=False):
+    def __init__(self, dscene, cameras, raster, device, profile=False, targets=None, depth=2):
         self.dscene, self.cameras, self.raster, self.device = dscene, cameras, raster, device
         self.profile = profile
+        # host-resident targets (streamed datasets): each upcoming step's target is
+        # uploaded on the side stream into a small device ring (copy engine,
+        # overlapping compute); a slot is rewritten only after the step that read it
+        # has been retired (its event)
+        self.targets = targets if targets is not None and any(not t.is_cuda for t in targets) else None
+        self.ring = [None] * (depth + 4)
+        self.ring_free = [None] * (depth + 4)
+        self.copy_stream = torch.cuda.Stream(device=device) if self.targets is not None else None
         self.events = []  # (start, end) of each view build on the side stream
         self.host_build_ms = []
         self.host_wait_ms = []
@@ -73,13 +81,16 @@ class ViewPrefetcher:
             self.jobs.append((key, index))
             self.cv.notify_all()
 
-    def retire(self, view):
+    def retire(self, view, key=None):
         """Hand a used view back; it is freed on the side stream once the current
-        stream's work queued so far (which reads the view) has completed."""
+        stream's work queued so far (which reads the view) has completed.  `key`
+        releases the step's target-ring slot at the same event."""
         ev = torch.cuda.Event()
         ev.record()
         with self.cv:
             self.retired.append((view, ev))
+            if key is not None and self.targets is not None:
+                self.ring_free[key % len(self.ring)] = ev
             self.cv.notify_all()
 
     def _free_retired(self):
@@ -117,6 +128,22 @@ class ViewPrefetcher:
                 key, index = job
                 try:
                     intr, pose = self.cameras[index]
+                    tgt, copied = None, None
+                    if self.targets is not None:
+                        # the upload runs on its own stream, concurrently with the build
+                        src = self.targets[index]
+                        slot = key % len(self.ring)
+                        with self.cv:
+                            free = self.ring_free[slot]
+                        with torch.cuda.stream(self.copy_stream):
+                            if free is not None:
+                                self.copy_stream.wait_event(free)
+                            if self.ring[slot] is None or self.ring[slot].shape != src.shape:
+                                self.ring[slot] = torch.empty(src.shape, dtype=torch.float32, device=self.device)
+                            tgt = self.ring[slot]
+                            tgt.copy_(src, non_blocking=True)
+                            copied = torch.cuda.Event()
+                            copied.record(self.copy_stream)
                     t0 = time.perf_counter()
                     if self.profile:
                         e0 = torch.cuda.Event(enable_timing=True)
@@ -124,12 +151,14 @@ class ViewPrefetcher:
                     view = D.View(self.dscene, intr, pose, self.raster)
                     if self.profile:
                         self.host_build_ms.append((time.perf_counter() - t0) * 1000.0)
+                    if copied is not None:
+                        self.stream.wait_event(copied)  # one ready event covers view + target
                     ev = torch.cuda.Event(enable_timing=self.profile)
                     ev.record(self.stream)
                     if self.profile:
                         self.events.append((e0, ev))
                     with self.cv:
-                        self.ready[key] = (view, ev)
+                        self.ready[key] = (view, ev, tgt)
                         self.cv.notify_all()
                     self._free_retired()
                 except Exception as e:  # surfaced to the consumer
@@ -145,7 +174,7 @@ class ViewPrefetcher:
         self.thread.join(timeout=30)
         with torch.cuda.stream(self.stream):
             self._free_retired()
-            for view, _ in self.ready.values():
+            for view, _, _ in self.ready.values():
                 view.close()
         self.ready.clear()
 
@@ -189,7 +218,9 @@ class RefitEngine:
             # up to prefetch + 1 views alive at once, ~170 B per gaussian each plus
             # build temporaries: grow the pool once, outside any timed region
             N.call("rcgs_pool_reserve", int((self.prefetch + 2) * dscene.n * 400), D.stream_ptr())
-        self._pf = ViewPrefetcher(dscene, self.cameras, raster, dev, profile) if self.prefetch else None
+        self._pf = (ViewPrefetcher(dscene, self.cameras, raster, dev, profile, targets=self.targets,
+                                   depth=self.prefetch) if self.prefetch else None)
+        self._d2h = collections.deque()  # in-flight metric read-backs (drain(wait=False))
         # profile: CUDA events around every stage of every step (negligible cost)
         self.profile = profile
         self._prof = []
@@ -239,8 +270,8 @@ class RefitEngine:
         if self._held is not None:
             held, self._held = self._held, None
             return held
-        picks, view = self._take_prefetched()
-        return picks, view, False
+        picks, view, key, tgt = self._take_prefetched()
+        return picks, view, False, key, tgt
 
     def _take_prefetched(self):
         while len(self._future) < self.prefetch:
@@ -250,14 +281,15 @@ class RefitEngine:
             self._pf.submit(key, picks[self.rank] if self.world > 1 else picks[0])
             self._future.append((key, picks))
         key, picks = self._future.popleft()
-        view, ev = self._pf.take(key)
+        view, ev, tgt = self._pf.take(key)
         torch.cuda.current_stream().wait_event(ev)
-        return picks, view
+        return picks, view, key, tgt
 
     def step(self, picks=None, generation: int = 0):
         coloured = False
+        key, tgt_pf = None, None
         if picks is None and self._pf is not None:
-            picks, view, coloured = self._next_prefetched()
+            picks, view, coloured, key, tgt_pf = self._next_prefetched()
             mine = picks[self.rank] if self.world > 1 else picks[0]
             prefetched = True
         else:
@@ -285,7 +317,9 @@ class RefitEngine:
         if self.cache_views:  # resident views also keep their weights (SpMV from then on)
             view.keep_records()
         target = self.targets[mine]
-        if not target.is_cuda:           # streamed dataset: H2D of this step's target
+        if tgt_pf is not None:           # streamed dataset, uploaded by the prefetcher
+            target = tgt_pf
+        elif not target.is_cuda:         # streamed dataset: H2D of this step's target
             tgt_buf.copy_(target, non_blocking=True)
             target = tgt_buf
         slot = len(self.pending) % self.max_pending
@@ -310,12 +344,12 @@ class RefitEngine:
             # take the next step's view now (its build was submitted `prefetch`
             # steps ago; the stream waits for it before the Adam stage event) and
             # let this Adam colour it from the updated SH
-            nxt_picks, nxt = self._take_prefetched()
+            nxt_picks, nxt, nxt_key, nxt_tgt = self._take_prefetched()
             if ev:
                 ev[5].record()
             N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())
             nxt._colored = True
-            self._held = (nxt_picks, nxt, True)
+            self._held = (nxt_picks, nxt, True, nxt_key, nxt_tgt)
         else:
             if ev:
                 ev[5].record()
@@ -326,22 +360,34 @@ class RefitEngine:
         rec[3].copy_(self.reject[0], non_blocking=True)
         self.pending.append((picks, generation))
         if prefetched:
-            self._pf.retire(view)
+            self._pf.retire(view, key)
         elif not self.cache_views:
             view.close()
         return picks
 
-    def drain(self):
-        """Synchronise and return [(picks, generation, l1, ssim, total, rejected)]."""
-        if not self.pending:
-            return []
-        n = len(self.pending)
-        recs = self.records[:min(n, self.max_pending)].cpu().numpy()
+    def drain(self, wait: bool = True):
+        """Return [(picks, generation, l1, ssim, total, rejected)] of the steps whose
+        metrics have reached the host.  wait=True synchronises on every pending
+        step; wait=False starts a non-blocking read-back of the pending steps
+        (pinned memory, stream ordered) and returns only those already landed --
+        every step is still read back, one call later, without stalling the host
+        pipeline."""
+        if self.pending:
+            n = len(self.pending)
+            host = torch.empty((min(n, self.max_pending), 4), dtype=torch.float64, pin_memory=True)
+            host.copy_(self.records[:host.shape[0]], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._d2h.append((ev, host, self.pending))
+            self.pending = []
         out = []
-        for i, (picks, gen) in enumerate(self.pending):
-            r = recs[i % self.max_pending]
-            out.append((picks, gen, float(r[0]), float(r[1]), float(r[2]), bool(r[3] != 0)))
-        self.pending = []
+        while self._d2h and (wait or self._d2h[0][0].query()):
+            ev, host, pend = self._d2h.popleft()
+            ev.synchronize()
+            recs = host.numpy()
+            for i, (picks, gen) in enumerate(pend):
+                r = recs[i % self.max_pending]
+                out.append((picks, gen, float(r[0]), float(r[1]), float(r[2]), bool(r[3] != 0)))
         return out
 
     def stage_report(self, reset: bool = True) -> dict:

@@ -281,8 +281,8 @@ class BackgroundOptimizer:
         if len(self._engine.pending) >= min(self._config.snapshot_every, self._engine.max_pending):
             self._flush()
 
-    def _flush(self) -> None:
-        recs = self._engine.drain()
+    def _flush(self, wait: bool = True) -> None:
+        recs = self._engine.drain(wait)
         lines = []
         for picks, gen, l1, ss, total, rejected in recs:
             it = self._accepted + 1

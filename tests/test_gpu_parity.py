@@ -548,3 +548,28 @@ def test_kept_records_bit_identical():
     assert torch.equal(kept.backward(g), ref.backward(g))
     for v in (ref, kept, other):
         v.close()
+
+
+def test_streamed_targets_pipeline_identical(two_blobs):
+    """BackgroundOptimizer with host-resident targets uploaded by the prefetcher
+    (copy stream) and metrics read back one step late gives the same SH and
+    metric lines as the device-resident, synchronous configuration."""
+    scene = p_scene(two_blobs)
+    views = []
+    for v in (0, 1):
+        intr, pose = p_cam(two_blobs, f"v{v}_")
+        views.append(P.TrainingView(v, intr, pose, P.render(scene, intr, pose)))
+    ds = P.build_edited_dataset(views, P.SelectionCloud(two_blobs["cloud"]), (1.0, 0.2, 0.2), scene)
+    runs = []
+    for stream_targets, prefetch in ((False, 0), (True, 2)):
+        lines = []
+        opt = P.BackgroundOptimizer(scene, ds, seed=3, metrics_sink=lambda m: lines.append(m.line()),
+                                    stream_targets=stream_targets, prefetch=prefetch)
+        for _ in range(7):
+            opt._step()
+            opt._flush(wait=False)
+        opt._flush()
+        runs.append((opt._engine.sh.detach().cpu().numpy().copy(), lines))
+        opt.stop()
+    np.testing.assert_array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
