@@ -271,6 +271,7 @@ def run_gpu(args):
     e2e = run_e2e(args, scene, cams, sp, group, world) if rank == 0 or world > 1 else None
     interactive = run_interactive(args, scene, cams, ds, sh0, sp, cloud) if args.extras and rank == 0 else None
     resident = run_resident_views(args, ds, sh0, cams, sp) if args.extras and world == 1 else None
+    select_mask = run_select_from_mask(scene, cams, ds) if args.extras and rank == 0 else None
     if args.extras:
         del sp, targets, gt
         torch.cuda.empty_cache()
@@ -336,6 +337,7 @@ def run_gpu(args):
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         "interactive_c5": interactive, "selection_sweep_c4": sweep, "resident_views": resident,
+        "select_from_mask": select_mask,
     }
     print(json.dumps(line))
 
@@ -457,6 +459,41 @@ def run_resident_views(args, ds, sh0, cams, sp):
             "views_resident": len(cams),
             "note": "extra: per-view preprocess, binning and composite weights kept resident (geometry frozen); "
                     "not the headline"}
+
+
+def run_select_from_mask(scene, cams, ds):
+    """the select-from-mask step before a selection pass,
+    at its largest (a full-frame brush on a 1080p view): unproject the masked
+    depth (seeded 70% subsample, host numpy -- the permutation must be numpy's)
+    and remove_outliers with the GPU kNN mean distances (threshold on the host
+    in numpy).  Reported beside the same step with scipy's cKDTree (all host
+    cores), which the reference uses; the kept clouds must be identical."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import device as D
+    from scipy.spatial import cKDTree
+
+    intr, pose = cams[0]
+    v = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
+    depth = v.depth(0.5).cpu().numpy()
+    v.close()
+    mask = P.SelectionMask2D(np.ones((intr.height, intr.width), bool), intr, pose)
+    t0 = time.perf_counter()
+    cloud = P.unproject(mask, depth, 0.7, 0)
+    t_unp = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    kept = P.remove_outliers(cloud, 16, 1.0)
+    t_gpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    d, _ = cKDTree(cloud.points).query(cloud.points, k=17, workers=-1)
+    means = d[:, 1:].mean(axis=1)
+    ref = cloud.points[means <= means.mean() + 1.0 * means.std()]
+    t_cpu = time.perf_counter() - t0
+    return {"points": int(len(cloud)), "kept": int(len(kept)), "unproject_ms": round(t_unp * 1e3, 2),
+            "remove_outliers_ms": round(t_gpu * 1e3, 2), "scipy_remove_outliers_ms": round(t_cpu * 1e3, 2),
+            "identical": bool(np.array_equal(kept.points, ref)),
+            "note": "full-frame 1080p brush on view 0; GPU kNN (k=16) + host numpy threshold vs scipy cKDTree"}
 
 
 def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):

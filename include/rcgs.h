@@ -205,6 +205,14 @@ int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grad
 /* OR 1 into *d_flag if any of d_x[0..count) is non-finite. */
 int rcgs_nonfinite_check(const float* d_x, int64_t count, int32_t* d_flag, void* stream);
 
+/* ---- select-from-mask outlier statistics (selection.py:155-181) ---------------------- */
+/* knn_mean_distances: per point of the (m,3) fp64 cloud, the mean distance to its
+ * k nearest neighbours (self excluded), bit-identical to scipy cKDTree.query(k+1)
+ * + numpy mean (unfused squared distances, correctly rounded sqrt, numpy's
+ * pairwise summation); exact uniform-grid search.  1 <= k <= 32, m > k.
+ * Synchronises `stream` twice (bounding box, cell-size sample). */
+int rcgs_knn_mean_distances(const double* d_points, int64_t m, int32_t k, double* d_means, void* stream);
+
 /* ---- selection pass (selection.py:184-235, recolor.py:30-81) ------------------------- */
 /* Stamp quad x quad squares of the visible cloud points into d_mask (H,W) uint8
  * (caller zero-fills); visibility z <= depth * (1 + tol), fp64, bit-exact. */

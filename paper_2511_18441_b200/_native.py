@@ -74,6 +74,7 @@ _SIGNATURES = {
     "rcgs_adam_dense": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, P(AdamConfig), c_void_p,
                         c_void_p, c_void_p],
     "rcgs_nonfinite_check": [c_void_p, c_i64, c_void_p, c_void_p],
+    "rcgs_knn_mean_distances": [c_void_p, c_i64, c_i32, c_void_p, c_void_p],
     "rcgs_project_cloud": [c_void_p, c_i64, P(Camera), c_void_p, c_i32, c_double, c_void_p,
                            c_void_p],
     "rcgs_apply_recolor": [c_void_p, c_void_p, c_i64, P(ctypes.c_float), c_void_p, c_void_p],

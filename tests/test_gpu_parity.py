@@ -573,3 +573,32 @@ def test_streamed_targets_pipeline_identical(two_blobs):
         opt.stop()
     np.testing.assert_array_equal(runs[0][0], runs[1][0])
     assert runs[0][1] == runs[1][1]
+
+
+# ---------------------------------------------------------------- select-from-mask (8(f) row 1)
+def test_knn_mean_distances_bit_exact():
+    """GPU kNN mean distances == scipy cKDTree + numpy mean, bit for bit, on
+    uniform, surface-like (unprojected depth), duplicated and tiny clouds."""
+    from scipy.spatial import cKDTree
+
+    def ref(p, k):
+        d, _ = cKDTree(p).query(p, k=k + 1)
+        return d[:, 1:].mean(axis=1)
+
+    rng = np.random.default_rng(5)
+    u, v = rng.uniform(0, 1, 20000), rng.uniform(0, 1, 20000)
+    surface = np.stack([u, v, 0.3 * np.sin(6 * u) + 0.01 * rng.normal(size=u.size)], axis=1)
+    clouds = {
+        "uniform": rng.uniform(-2, 3, (30000, 3)),
+        "surface": surface,
+        "dups": np.repeat(rng.uniform(0, 1, (700, 3)), 3, axis=0),
+        "tiny": rng.uniform(0, 1, (18, 3)),
+        "far_outliers": np.concatenate([rng.normal(size=(5000, 3)) * 0.01, rng.uniform(-50, 50, (40, 3))]),
+    }
+    for name, pts in clouds.items():
+        for k in ((16, 5) if name != "tiny" else (16,)):
+            got = P.knn_mean_distances(pts, k)
+            np.testing.assert_array_equal(got, ref(pts, k), err_msg=f"{name} k={k}")
+    cloud = P.SelectionCloud(clouds["far_outliers"])
+    kept = P.remove_outliers(cloud, 16, 1.0)
+    np.testing.assert_array_equal(kept.points, OS.remove_outliers(clouds["far_outliers"], 16, 1.0))
