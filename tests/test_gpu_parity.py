@@ -602,3 +602,14 @@ def test_knn_mean_distances_bit_exact():
     cloud = P.SelectionCloud(clouds["far_outliers"])
     kept = P.remove_outliers(cloud, 16, 1.0)
     np.testing.assert_array_equal(kept.points, OS.remove_outliers(clouds["far_outliers"], 16, 1.0))
+
+
+def test_select_from_mask_matches_reference_cloud(two_blobs):
+    """unproject + GPU remove_outliers reproduce the reference's golden cloud."""
+    from conftest import golden_camera
+    intr, pose = golden_camera(two_blobs, "v0_")
+    intr_p = P.CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+    pose_p = P.CameraPose(pose.rotation, pose.translation)
+    mask = P.SelectionMask2D(two_blobs["brush"], intr_p, pose_p)
+    cloud = P.remove_outliers(P.unproject(mask, two_blobs["v0_depth"], 0.7, 0), 16, 0.007)
+    np.testing.assert_array_equal(cloud.points, two_blobs["cloud"])
