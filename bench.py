@@ -498,10 +498,11 @@ def run_select_from_mask(scene, cams, ds):
 
 def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
     """Config 5 (BASELINE.json): 1M gaussians, one 1080p viewer.  Per frame: one
-    optimizer step (on the sampled training view), the viewer's render of an orbit
-    camera (preprocess + bin + colour + raster), the selection overlay (depth +
-    cloud projection, blended 0.45 as session.py:381-402) and RGBA8 quantisation;
-    latency = host wall time per frame including the device sync."""
+    optimizer step (on the sampled training view), the viewer's frame of an orbit
+    camera (session.py:381-405: preprocess + bin + colour, occlusion depth + cloud
+    projection, render with the selection overlay and RGBA8 quantisation in one
+    pass) and its readback; latency = host wall time per frame including the
+    device sync."""
     import torch
     import paper_2511_18441_b200 as P
     from paper_2511_18441_b200 import device as D
@@ -514,7 +515,6 @@ def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
     intr = cams[0][0]
     orbit = ring_cameras(intr.width, intr.height, frames)
     pts = D.to_device(cloud.points, torch.float64)
-    tint = torch.tensor([1.0, 0.2, 0.2], device="cuda")
     lat = []
     for f in range(frames + 5):
         torch.cuda.synchronize()
@@ -523,14 +523,9 @@ def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
         ci, cp = orbit[f % frames]
         v = D.View(ds, ci, cp, P.DEFAULT_CONFIG)
         v.color(eng.sh)
-        img = v.render(None, 0)
         depth = v.depth(0.5)
         mask = project_cloud_device(pts, ci, cp, depth, 5, 0.02)
-        m = mask.unsqueeze(-1).float()
-        img = img * (1 - 0.45 * m) + (0.45 * m) * tint
-        rgba = torch.empty((ci.height, ci.width, 4), dtype=torch.uint8, device="cuda")
-        rgba[..., :3] = (img.clamp(0, 1) * 255.0 + 0.5).to(torch.uint8)
-        rgba[..., 3] = 255
+        rgba = v.render_rgba(mask)  # render + selection overlay + RGBA8 in one pass
         frame = rgba.cpu()
         v.close()
         torch.cuda.synchronize()
@@ -542,7 +537,8 @@ def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
     return {"frames": len(lat), "p50_ms": round(float(np.percentile(lat, 50)), 3),
             "p99_ms": round(float(np.percentile(lat, 99)), 3), "fps_p50": round(1000.0 / float(np.percentile(lat, 50)), 1),
             "frame_bytes_d2h": int(frame.numel()),
-            "note": "1 optimizer step + viewer render + depth/cloud overlay + RGBA8 readback per frame"}
+            "note": "1 optimizer step + viewer frame (depth, cloud projection, render with the selection "
+                    "overlay and RGBA8 quantisation fused, rcgs_render_rgba) + RGBA8 readback per frame"}
 
 
 def run_selection_sweep(group, world, rank, dev):

@@ -116,6 +116,14 @@ int rcgs_render(const rcgs_view* view, const float* h_background3, int layout,
  * of re-traversing the tile lists, and later renders of the view are an SpMV.
  * Results are bit-identical to the traversal paths.  Reserves up to
  * 8 * pairs * 132 bytes (~2.8 GB at 1080p / 1M gaussians), freed with the view. */
+/* Viewer frame (session.py:381-405 render_rgba, protocol.py:29-38 image_to_rgba)
+ * in one pass: the view composited with a zero background, where d_overlay (H,W)
+ * uint8 != 0 blended (1 - strength) * img + strength * highlight in fp64, then
+ * rint(clip(x, 0, 1) * 255) into d_rgba (H,W,4) uint8 with alpha 255 --
+ * bit-identical to image_to_rgba(overlay(render)) on the host.  d_overlay may be
+ * NULL (no selection). */
+int rcgs_render_rgba(const rcgs_view* view, const uint8_t* d_overlay, const double* h_highlight3,
+                     double strength, uint8_t* d_rgba, void* stream);
 int rcgs_render_train(rcgs_view* view, const float* h_bg3, int layout, float* d_image, float* d_t_final,
                       void* stream);
 /* Keep the composite weights recorded by rcgs_render_train resident with the

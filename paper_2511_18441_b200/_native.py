@@ -60,6 +60,7 @@ _SIGNATURES = {
     "rcgs_view_color": [c_void_p, c_void_p, c_void_p],
     "rcgs_render": [c_void_p, P(ctypes.c_float), c_int, c_void_p, c_void_p, c_void_p],
     "rcgs_view_keep_records": [c_void_p, c_void_p],
+    "rcgs_render_rgba": [c_void_p, c_void_p, P(c_double), c_double, c_void_p, c_void_p],
     "rcgs_render_train": [c_void_p, P(ctypes.c_float), c_int, c_void_p, c_void_p, c_void_p],
     "rcgs_depth": [c_void_p, c_double, c_void_p, c_void_p, c_void_p],
     "rcgs_capture": [c_void_p, P(c_i64), c_void_p, c_void_p, c_void_p, c_void_p],

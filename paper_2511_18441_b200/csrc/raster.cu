@@ -59,6 +59,49 @@ __device__ __forceinline__ long long to_fixed(float v) {
     return __float2ll_rn(v * 1125899906842624.0f);
 }
 
+// Where a composited pixel goes: fp32 HWC / CHW image, or an RGBA8 viewer frame
+// (layout 2): the selection overlay (1 - s) img + s hl in fp64 where
+// overlay[pix] != 0 (session.py:392-402) then rint(clip(x, 0, 1) * 255) with
+// opaque alpha (protocol.py image_to_rgba), bit-identical to doing both on the
+// host from the same render.
+struct PixelOut {
+    float bg0, bg1, bg2;
+    int layout;  // 0 HWC, 1 CHW, 2 RGBA8
+    float* image;
+    float* t_final;
+    uint8_t* rgba;
+    const uint8_t* overlay;
+    double ov_keep, ov_add0, ov_add1, ov_add2;  // 1 - s, s * highlight
+};
+
+__device__ __forceinline__ uint8_t to_u8(double x) {
+    return (uint8_t)__double2int_rn(__dmul_rn(fmin(fmax(x, 0.0), 1.0), 255.0));
+}
+
+__device__ __forceinline__ void write_pixel(const PixelOut& o, int W, int H, int64_t pix, float acc0, float acc1,
+                                            float acc2, float T) {
+    const float o0 = fmaf(T, o.bg0, acc0), o1 = fmaf(T, o.bg1, acc1), o2 = fmaf(T, o.bg2, acc2);
+    if (o.layout == 0) {
+        o.image[3 * pix] = o0;
+        o.image[3 * pix + 1] = o1;
+        o.image[3 * pix + 2] = o2;
+    } else if (o.layout == 1) {
+        const int64_t plane = (int64_t)W * H;
+        o.image[pix] = o0;
+        o.image[plane + pix] = o1;
+        o.image[2 * plane + pix] = o2;
+    } else {
+        double c0 = o0, c1 = o1, c2 = o2;
+        if (o.overlay && o.overlay[pix]) {
+            c0 = __dadd_rn(__dmul_rn(o.ov_keep, c0), o.ov_add0);
+            c1 = __dadd_rn(__dmul_rn(o.ov_keep, c1), o.ov_add1);
+            c2 = __dadd_rn(__dmul_rn(o.ov_keep, c2), o.ov_add2);
+        }
+        reinterpret_cast<uchar4*>(o.rgba)[pix] = make_uchar4(to_u8(c0), to_u8(c1), to_u8(c2), 255);
+    }
+    if (o.t_final) o.t_final[pix] = T;
+}
+
 struct RasterArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // work order (nullptr: row-major)
@@ -74,10 +117,7 @@ struct RasterArgs {
     double alpha_clamp, alpha_skip, t_floor, tau;
     float f_alpha_clamp, f_floor, f_tau;
     // FWD
-    float bg0, bg1, bg2;
-    int layout;
-    float* image;
-    float* t_final;
+    PixelOut out;
     // DEPTH
     int32_t* cross;
     double* depth;
@@ -533,19 +573,7 @@ __global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMi
         }
         if (!inside) continue;
         if (kFwd) {
-            const float T = px.T;
-            const float o0 = fmaf(T, a.bg0, acc0), o1 = fmaf(T, a.bg1, acc1), o2 = fmaf(T, a.bg2, acc2);
-            if (a.layout == 0) {
-                a.image[3 * pix] = o0;
-                a.image[3 * pix + 1] = o1;
-                a.image[3 * pix + 2] = o2;
-            } else {
-                const int64_t plane = (int64_t)a.W * a.H;
-                a.image[pix] = o0;
-                a.image[plane + pix] = o1;
-                a.image[2 * plane + pix] = o2;
-            }
-            if (a.t_final) a.t_final[pix] = T;
+            write_pixel(a.out, a.W, a.H, pix, acc0, acc1, acc2, px.T);
         } else if (M == DEPTH) {
             if (a.cross) a.cross[pix] = cross;
             if (a.depth) a.depth[pix] = cross >= 0 ? a.z[cross] : __longlong_as_double(0x7ff0000000000000ll);
@@ -576,10 +604,7 @@ struct RecArgs {
     // render
     const float4* color;
     const float* t_in;
-    float bg0, bg1, bg2;
-    int layout;
-    float* image;
-    float* t_final;
+    PixelOut out;
     // backward
     const float* grad;
     unsigned long long* acc_fx;
@@ -671,21 +696,7 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                 }
             }
         }
-        if (!kBwd && inside) {
-            const float T = a.t_in[pix];
-            const float o0 = fmaf(T, a.bg0, acc0), o1 = fmaf(T, a.bg1, acc1), o2 = fmaf(T, a.bg2, acc2);
-            if (a.layout == 0) {
-                a.image[3 * pix] = o0;
-                a.image[3 * pix + 1] = o1;
-                a.image[3 * pix + 2] = o2;
-            } else {
-                const int64_t plane = (int64_t)a.W * a.H;
-                a.image[pix] = o0;
-                a.image[plane + pix] = o1;
-                a.image[2 * plane + pix] = o2;
-            }
-            if (a.t_final) a.t_final[pix] = T;
-        }
+        if (!kBwd && inside) write_pixel(a.out, a.W, a.H, pix, acc0, acc1, acc2, a.t_in[pix]);
     }
     work_counter_exit(a.counter, lane);
 }
@@ -844,30 +855,56 @@ extern "C" int rcgs_raster_counters(uint64_t* d_counters30) {
     return RCGS_OK;
 }
 
+// Composite into `out`: an SpMV over the view's recorded weights when it has
+// them, else the traversal (FWD).
+static int render_into(const rcgs_view* v, const PixelOut& out, cudaStream_t s) {
+    if (records_valid(v)) {  // weights recorded by an earlier rcgs_render_train: SpMV
+        RecArgs ra = rec_args(v);
+        ra.out = out;
+        return launch_rec<false>(ra, s);
+    }
+    RasterArgs a = base_args(v);
+    a.out = out;
+    return launch<FWD>(a, s);
+}
+
+static PixelOut image_out(const float* h_bg, int layout, float* d_image, float* d_t_final) {
+    PixelOut o;
+    memset(&o, 0, sizeof(o));
+    if (h_bg) {
+        o.bg0 = h_bg[0];
+        o.bg1 = h_bg[1];
+        o.bg2 = h_bg[2];
+    }
+    o.layout = layout;
+    o.image = d_image;
+    o.t_final = d_t_final;
+    return o;
+}
+
 extern "C" int rcgs_render(const rcgs_view* v, const float* h_bg, int layout, float* d_image,
                            float* d_t_final, void* stream) {
     RCGS_CHECK_ARG(v != nullptr && d_image != nullptr, "null argument");
     RCGS_CHECK_ARG(layout == 0 || layout == 1, "unknown layout %d", layout);
-    RasterArgs a = base_args(v);
-    if (h_bg) {
-        a.bg0 = h_bg[0];
-        a.bg1 = h_bg[1];
-        a.bg2 = h_bg[2];
+    return render_into(v, image_out(h_bg, layout, d_image, d_t_final), as_stream(stream));
+}
+
+extern "C" int rcgs_render_rgba(const rcgs_view* v, const uint8_t* d_overlay, const double* h_highlight3,
+                                double strength, uint8_t* d_rgba, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_rgba != nullptr, "null argument");
+    RCGS_CHECK_ARG(d_overlay == nullptr || h_highlight3 != nullptr, "overlay needs a highlight colour");
+    PixelOut o;
+    memset(&o, 0, sizeof(o));
+    o.layout = 2;
+    o.rgba = d_rgba;
+    o.overlay = d_overlay;
+    if (d_overlay) {  // (1 - s) * img + s * highlight, the reference's operand order
+        o.ov_keep = 1.0 - strength;
+        o.ov_add0 = strength * h_highlight3[0];
+        o.ov_add1 = strength * h_highlight3[1];
+        o.ov_add2 = strength * h_highlight3[2];
     }
-    a.layout = layout;
-    a.image = d_image;
-    a.t_final = d_t_final;
-    if (records_valid(v)) {  // weights recorded by an earlier rcgs_render_train: SpMV
-        RecArgs ra = rec_args(v);
-        ra.bg0 = a.bg0;
-        ra.bg1 = a.bg1;
-        ra.bg2 = a.bg2;
-        ra.layout = layout;
-        ra.image = d_image;
-        ra.t_final = d_t_final;
-        return launch_rec<false>(ra, as_stream(stream));
-    }
-    return launch<FWD>(a, as_stream(stream));
+    return render_into(v, o, as_stream(stream));
 }
 
 extern "C" int rcgs_render_train(rcgs_view* v, const float* h_bg, int layout, float* d_image, float* d_t_final,
@@ -901,14 +938,7 @@ extern "C" int rcgs_render_train(rcgs_view* v, const float* h_bg, int layout, fl
     g_arena.owner.store(v);
     v->wrec_epoch = g_arena.epoch.fetch_add(1) + 1;
     RasterArgs a = base_args(v);
-    if (h_bg) {
-        a.bg0 = h_bg[0];
-        a.bg1 = h_bg[1];
-        a.bg2 = h_bg[2];
-    }
-    a.layout = layout;
-    a.image = d_image;
-    a.t_final = v->wrec_tf;
+    a.out = image_out(h_bg, layout, d_image, v->wrec_tf);
     a.wrec_n = v->wrec_n;
     a.wrec_s = v->wrec_s;
     a.wrec_w = v->wrec_w;

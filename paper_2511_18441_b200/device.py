@@ -174,6 +174,22 @@ class View:
                N.ptr(tf), stream_ptr())
         return (img, tf) if t_final else img
 
+    def render_rgba(self, overlay=None, highlight=(1.0, 0.8, 0.1), strength: float = 0.45, out=None):
+        """Viewer frame (session.py:381-405 render_rgba): the view composited on a
+        zero background, `overlay` (H,W) pixels blended toward `highlight`, then
+        quantised to (H,W,4) uint8 RGBA (protocol.py image_to_rgba) -- one pass
+        (rcgs_render_rgba)."""
+        self._need_color()
+        rgba = out if out is not None else torch.empty((self.height, self.width, 4), dtype=torch.uint8,
+                                                         device=device())
+        ov = None
+        if overlay is not None:
+            ov = overlay if overlay.dtype == torch.uint8 else overlay.to(torch.uint8)
+            ov = ov.contiguous()
+        hl = (ctypes.c_double * 3)(*[float(c) for c in highlight])
+        N.call("rcgs_render_rgba", self.handle, N.ptr(ov), hl, float(strength), N.ptr(rgba), stream_ptr())
+        return rgba
+
     def keep_records(self):
         """Keep the composite weights recorded by a train render resident with the
         view (rcgs_view_keep_records): later renders / backwards stream them."""

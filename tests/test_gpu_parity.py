@@ -613,3 +613,29 @@ def test_select_from_mask_matches_reference_cloud(two_blobs):
     mask = P.SelectionMask2D(two_blobs["brush"], intr_p, pose_p)
     cloud = P.remove_outliers(P.unproject(mask, two_blobs["v0_depth"], 0.7, 0), 16, 0.007)
     np.testing.assert_array_equal(cloud.points, two_blobs["cloud"])
+
+
+# ---------------------------------------------------------------- viewer frames (8(f) row 2)
+def test_render_rgba_bit_identical_to_host_frame():
+    """rcgs_render_rgba == image_to_rgba(overlay(render)) computed on the host
+    (session.py:381-405), with and without a selection, for the traversal and
+    the recorded-weights (SpMV) render paths."""
+    import sys
+    import torch
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2511_18441_b200 import device as D
+    cfg = dict(n=30_000, deg=3, views=1, width=320, height=240)
+    scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
+    intr, pose = cams[0]
+    v = D.View(ds, intr, pose, P.DEFAULT_CONFIG).color(sh0 * 1.7)  # some values beyond 1 (clipped)
+    img = v.render(None, 0).double().cpu().numpy()
+    bits = np.random.default_rng(3).uniform(size=(intr.height, intr.width)) < 0.3
+    bits_dev = torch.from_numpy(bits.astype(np.uint8)).cuda()
+    for train in (False, True):
+        if train:
+            v.render(None, 0, train=True)  # later renders stream the recorded weights
+        np.testing.assert_array_equal(v.render_rgba().cpu().numpy(), P.image_to_rgba(img))
+        np.testing.assert_array_equal(v.render_rgba(bits_dev).cpu().numpy(),
+                                      P.image_to_rgba(P.overlay(img, bits)))
+    v.close()
