@@ -17,8 +17,10 @@ import launch_summary  # noqa: E402
 import ncu_summary  # noqa: E402
 
 STAGES = {  # bench stage -> kernel name prefixes (ncu "Kernel Name" without args)
-    "raster_fwd": ["void rcgs::raster_kernel<0,", "rcgs::raster_kernel<0,"],
-    "raster_bwd": ["void rcgs::raster_kernel<2,", "rcgs::raster_kernel<2,", "bwd_finish_kernel"],
+    "raster_fwd": ["void rcgs::raster_kernel<0,", "rcgs::raster_kernel<0,", "void rcgs::raster_kernel<6,",
+                   "rcgs::raster_kernel<6,", "void rcgs::rec_kernel<0>", "rcgs::rec_kernel<0>"],
+    "raster_bwd": ["void rcgs::raster_kernel<2,", "rcgs::raster_kernel<2,", "void rcgs::rec_kernel<1>",
+                   "rcgs::rec_kernel<1>", "bwd_finish_kernel"],
     "adam": ["rcgs::adam_prep_kernel", "rcgs::adam_fused_kernel", "rcgs::step_commit_kernel"],
     "color": ["rcgs::color_kernel"],
     "loss_grad": ["void rcgs::loss_", "rcgs::loss_"],
@@ -30,6 +32,27 @@ def stage_of(name):
         if any(name.startswith(p) for p in prefixes):
             return st
     return "view_build"
+
+
+def traffic_from_table(md_path, out_path, tag):
+    """traffic.json from the step summary table (DRAM read / write columns)."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    agg = {}
+    for line in open(md_path):
+        cells = [c.strip() for c in line.strip().strip("|").split("|")]
+        if len(cells) < 4 or cells[0] in ("kernel", "---") or cells[0].startswith("---"):
+            continue
+        b = 0.0
+        for cell in cells[2:4]:
+            v, u = cell.split()
+            b += float(v) * scale.get(u, 1)
+        st = stage_of(cells[0])
+        agg[st] = agg.get(st, 0.0) + b
+    out = {"source": f"ncu --set full (default cache control), one optimizer step of C3: profiles/{tag}_ncu_step.md",
+           "stages": {k: {"dram_bytes_per_launch": int(v)} for k, v in agg.items()}}
+    with open(out_path, "w") as f:
+        json.dump(out, f, indent=1)
+    return out
 
 
 def main(tag, outdir="profiles"):
