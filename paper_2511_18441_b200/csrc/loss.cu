@@ -292,6 +292,15 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
     }
 }
 
+// 4- or 8-byte asynchronous global -> shared copy (LDGSTS); `in` false zero-fills
+template <typename E>
+__device__ __forceinline__ void cp_async_elem(E* dst, const E* src, bool in) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(sizeof(E)),
+                 "r"(in ? (int)sizeof(E) : 0)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- pass B
 template <bool SSIM, typename T, typename G, typename MT>
 __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
@@ -300,8 +309,8 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                                                     const int32_t* __restrict__ differ,
                                                     const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* hs = reinterpret_cast<double*>(smem_raw);  // [3][42][32]
-    MT* im = reinterpret_cast<MT*>(hs + 3 * kLH * kLT); // [3][42][42]
+    double* hs = reinterpret_cast<double*>(smem_raw);   // [3][42][32]
+    MT* imb = reinterpret_cast<MT*>(hs + 3 * kLH * kLT); // [2][3][42][42]: double-buffered map planes
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
@@ -310,17 +319,42 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
     // images are identical (losses.py:127-130), else outside one block of a difference
     const bool any = *differ != 0 && near_dirty(dirty, SSIM ? 1 : 0);
     const int c = t % kLT, r0 = (t / kLT) * kRows;
-    for (int ch = 0; ch < 3; ++ch) {
-        if (SSIM && any) {
-            for (int i = t; i < kLH * kLH; i += kLNT) {
-                const int r = i / kLH, cc = i % kLH;
-                const int gy = y0 - kR + r, gx = x0 - kR + cc;
-                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-                const int64_t gi = (int64_t)ch * npix + (int64_t)gy * W + gx;
+    // the next channel's three map planes (with the 5-px halo, zero outside the
+    // image) stream into the other buffer while this channel computes
+    auto issue = [&](int ch) {
+        MT* buf = imb + (ch & 1) * 3 * kLH * kLH;
+        for (int i = t; i < kLH * kLH; i += kLNT) {
+            const int r = i / kLH, cc = i % kLH;
+            const int gy = y0 - kR + r, gx = x0 - kR + cc;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const int64_t gi = in ? (int64_t)ch * npix + (int64_t)gy * W + gx : 0;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) im[q * kLH * kLH + i] = in ? maps[q * npix * 3 + gi] : MT(0);
+            for (int q = 0; q < 3; ++q) cp_async_elem(buf + q * kLH * kLH + i, maps + q * npix * 3 + gi, in);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (SSIM && any) issue(0);
+    const int gx = x0 + c;
+    for (int ch = 0; ch < 3; ++ch) {
+        // this channel's image / target values, loaded early (used after the filters)
+        T fyv[kRows], fgv[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int gy = y0 + r0 + i;
+            const bool ok = any && gy < H && gx < W;
+            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+            fyv[i] = ok ? y[o] : T(0);
+            fgv[i] = ok ? g[o] : T(0);
+        }
+        if (SSIM && any) {
+            if (ch + 1 < 3) {
+                issue(ch + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
             __syncthreads();
+            const MT* im = imb + (ch & 1) * 3 * kLH * kLH;
             // horizontal pass in kHS-output strips from register-resident segments
             for (int i = t; i < kLH * (kLT / kHS); i += kLNT) {
                 const int r = i / (kLT / kHS), c0 = (i % (kLT / kHS)) * kHS;
@@ -346,7 +380,6 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
 #pragma unroll
             for (int q = 0; q < 3; ++q) vfilter(hs + q * kLH * kLT, r0, c, win, f[q]);
         }
-        const int gx = x0 + c;
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             const int gy = y0 + r0 + i;
@@ -356,7 +389,7 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                 grad[o] = G(0);
                 continue;
             }
-            const T fy = y[o], fg = g[o];
+            const T fy = fyv[i], fg = fgv[i];
             const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
             double out = (1.0 - lam) * sgn / n;
             if (SSIM) out -= lam * ((f[0][i] + 2.0 * (double)fy * f[1][i] + (double)fg * f[2][i]) / n);
@@ -427,7 +460,7 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
     loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty, differ);
     const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
-    const size_t smem_b = 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
+    const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
