@@ -144,7 +144,6 @@ struct rcgs_view {
     int32_t* rank_of;     // (n,) s or -1 (culled)
     // per pair (sorted by tile, then depth)
     uint32_t* pair_g;     // (pairs,) scene index g
-    uint32_t* pair_e;     // (pairs,) emission slot e (offs[s] <= e < offs[s+1])
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
     unsigned* work;       // (2,) work-item / exited-warp counters of the persistent launches

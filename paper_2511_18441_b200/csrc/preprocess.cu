@@ -19,7 +19,7 @@
 //   scan         emission offsets offs[s] (pairs emitted in rank order)
 //   k2_emit      one (tile, g) pair per overlapped tile, in depth order
 //   radix sort   stable sort on tile id -> (tile, depth) order
-//   k2_ranges    per-tile [start, end) + scene index per pair
+//   k2_ranges    per-tile [start, end)
 // Records are stored by scene index: tile lists carry g, so no pass is needed to
 // lay them out in depth order (nothing reads them in that order).
 #include <cuda_fp16.h>
@@ -299,29 +299,61 @@ __global__ void k1_rank_kernel(const uint32_t* __restrict__ gid, int64_t k, cons
 }
 
 // ---------------------------------------------------------------- K2 emission
+// One warp per 32 consecutive depth ranks: their pairs are one contiguous range of
+// emission slots, spread evenly over the lanes (a gaussian's footprint spans 1 to
+// hundreds of tiles, so one thread per gaussian diverged); each lane finds the
+// owning gaussian of its slot by a shuffle binary search over the warp's prefix of
+// counts.  Slot order is the per-gaussian row-major tile order, as before.
 __global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __restrict__ rect,
                                const uint32_t* __restrict__ offs, int64_t k, int tiles_x,
                                uint32_t* __restrict__ tile_key, uint32_t* __restrict__ emit_g) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= k) return;
-    const uint32_t g = gid[s];
-    const Rect rc = rect[g];
-    uint32_t e = offs[s];
-    for (int ty = rc.y0; ty <= rc.y1; ++ty)
-        for (int tx = rc.x0; tx <= rc.x1; ++tx) {
-            tile_key[e] = (uint32_t)(ty * tiles_x + tx);
-            emit_g[e] = g;
-            ++e;
+    const int lane = threadIdx.x & 31;
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) >= k) return;  // whole warp beyond k
+    uint32_t g = 0, cnt = 0, w = 1;
+    int x0 = 0, y0 = 0;
+    if (s < k) {
+        g = gid[s];
+        const Rect rc = rect[g];
+        if (rc.x1 >= rc.x0) {
+            w = (uint32_t)(rc.x1 - rc.x0 + 1);
+            cnt = w * (uint32_t)(rc.y1 - rc.y0 + 1);
         }
+        x0 = rc.x0;
+        y0 = rc.y0;
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t base = __shfl_sync(0xffffffffu, s < k ? offs[s] : 0u, 0);
+    for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        int L = 0;  // last lane with excl <= p
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, (L + step) & 31);
+            if (L + step < 32 && ex <= p) L += step;
+        }
+        const uint32_t exL = __shfl_sync(0xffffffffu, excl, L), wL = __shfl_sync(0xffffffffu, w, L);
+        const int x0L = __shfl_sync(0xffffffffu, x0, L), y0L = __shfl_sync(0xffffffffu, y0, L);
+        const uint32_t gL = __shfl_sync(0xffffffffu, g, L);
+        if (p < total) {
+            const uint32_t q = p - exL;
+            const uint32_t ty = (uint32_t)y0L + q / wL, tx = (uint32_t)x0L + q % wL;
+            tile_key[base + p] = ty * (uint32_t)tiles_x + tx;
+            emit_g[base + p] = gL;
+        }
+    }
 }
 
-__global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key,
-                                 const uint32_t* __restrict__ pair_e,
-                                 const uint32_t* __restrict__ emit_g, int64_t pairs,
-                                 uint2* __restrict__ ranges, uint32_t* __restrict__ pair_g) {
+__global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key, int64_t pairs, uint2* __restrict__ ranges) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= pairs) return;
-    pair_g[j] = emit_g[pair_e[j]];
     uint32_t t = tile_key[j];
     if (j == 0 || tile_key[j - 1] != t) ranges[t].x = (uint32_t)j;
     if (j == pairs - 1 || tile_key[j + 1] != t) ranges[t].y = (uint32_t)(j + 1);
@@ -500,7 +532,6 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->color, s);
     dfree(v->rank_of, s);
     dfree(v->pair_g, s);
-    dfree(v->pair_e, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
     dfree(v->work, s);
@@ -646,30 +677,28 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(rect, s);
         return RCGS_OK;
     }
-    // ---- K2 emit (depth order, values = scene index) + stable tile sort
-    uint32_t *tkey = nullptr, *tkey_alt = nullptr, *emit_g = nullptr, *pe = nullptr, *pe_alt = nullptr;
+    // ---- K2 emit (depth order, values = scene index) + stable tile sort; the sort
+    // carries the scene indices themselves, so its output values are the tile lists
+    uint32_t *tkey = nullptr, *tkey_alt = nullptr, *emit_g = nullptr, *g_alt = nullptr;
     RCGS_TRY(dalloc(&tkey, pairs, s));
     RCGS_TRY(dalloc(&tkey_alt, pairs, s));
     RCGS_TRY(dalloc(&emit_g, pairs, s));
-    RCGS_TRY(dalloc(&pe, pairs, s));
-    RCGS_TRY(dalloc(&pe_alt, pairs, s));
+    RCGS_TRY(dalloc(&g_alt, pairs, s));
     k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g);
     RCGS_LAUNCH_CHECK();
     dfree(rect, s);
     int tile_bits = 1;
     while ((1 << tile_bits) < ntiles) ++tile_bits;
-    RCGS_TRY(radix_sort_u32(&tkey, &tkey_alt, &pe, &pe_alt, true, pairs, tile_bits, s));
-    RCGS_TRY(dalloc(&v->pair_g, pairs, s));
-    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pe, emit_g, pairs, v->ranges, v->pair_g);
+    RCGS_TRY(radix_sort_u32(&tkey, &tkey_alt, &emit_g, &g_alt, false, pairs, tile_bits, s));
+    v->pair_g = emit_g;
+    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pairs, v->ranges);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
     tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order);
     RCGS_LAUNCH_CHECK();
-    v->pair_e = pe;
-    dfree(pe_alt, s);
+    dfree(g_alt, s);
     dfree(tkey, s);
     dfree(tkey_alt, s);
-    dfree(emit_g, s);
     return RCGS_OK;
 }
 
