@@ -40,7 +40,9 @@
 namespace rcgs {
 
 // FWDREC: FWD that also records the composite weights (see `WeightRecords`)
-enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRITE = 5, FWDREC = 6 };
+// FWDRGBA: FWD into an RGBA8 viewer frame (separate instantiation, so the
+// training / image paths keep their lean epilogue)
+enum RasterMode { FWD = 0, DEPTH = 1, BWD = 2, HITS = 3, CAP_COUNT = 4, CAP_WRITE = 5, FWDREC = 6, FWDRGBA = 7 };
 
 constexpr int kWarpsPerCTA = 8;
 constexpr int kCTA = 32 * kWarpsPerCTA;
@@ -78,14 +80,15 @@ __device__ __forceinline__ uint8_t to_u8(double x) {
     return (uint8_t)__double2int_rn(__dmul_rn(fmin(fmax(x, 0.0), 1.0), 255.0));
 }
 
+template <bool kRgba>
 __device__ __forceinline__ void write_pixel(const PixelOut& o, int W, int H, int64_t pix, float acc0, float acc1,
                                             float acc2, float T) {
     const float o0 = fmaf(T, o.bg0, acc0), o1 = fmaf(T, o.bg1, acc1), o2 = fmaf(T, o.bg2, acc2);
-    if (o.layout == 0) {
+    if (!kRgba && o.layout == 0) {
         o.image[3 * pix] = o0;
         o.image[3 * pix + 1] = o1;
         o.image[3 * pix + 2] = o2;
-    } else if (o.layout == 1) {
+    } else if (!kRgba) {
         const int64_t plane = (int64_t)W * H;
         o.image[pix] = o0;
         o.image[plane + pix] = o1;
@@ -365,8 +368,8 @@ struct WarpStage {
 #endif
 template <int M, bool kInstr>
 __global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMinCTAs) raster_kernel(RasterArgs a) {
-    constexpr bool kFwd = (M == FWD || M == FWDREC);
-    constexpr int kRow = (M == FWDREC) ? (int)FWD : M;  // counter row
+    constexpr bool kFwd = (M == FWD || M == FWDREC || M == FWDRGBA);
+    constexpr int kRow = (M == FWDREC || M == FWDRGBA) ? (int)FWD : M;  // counter row
     __shared__ WarpStage stage_all[kWarpsPerCTA];
     const int lane = threadIdx.x & 31;
     WarpStage& st = stage_all[threadIdx.x >> 5];
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMi
         }
         if (!inside) continue;
         if (kFwd) {
-            write_pixel(a.out, a.W, a.H, pix, acc0, acc1, acc2, px.T);
+            write_pixel<M == FWDRGBA>(a.out, a.W, a.H, pix, acc0, acc1, acc2, px.T);
         } else if (M == DEPTH) {
             if (a.cross) a.cross[pix] = cross;
             if (a.depth) a.depth[pix] = cross >= 0 ? a.z[cross] : __longlong_as_double(0x7ff0000000000000ll);
@@ -611,8 +614,10 @@ struct RecArgs {
     int32_t* nonfinite;
 };
 
-template <bool kBwd>
+// kMode: 0 SpMV render into an image, 1 backward, 2 SpMV render into an RGBA8 frame
+template <int kMode>
 __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
+    constexpr bool kBwd = kMode == 1;
     const int lane = threadIdx.x & 31;
     constexpr int kU = 8;  // records in flight per warp
     for (;;) {
@@ -696,23 +701,23 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                 }
             }
         }
-        if (!kBwd && inside) write_pixel(a.out, a.W, a.H, pix, acc0, acc1, acc2, a.t_in[pix]);
+        if (!kBwd && inside) write_pixel<kMode == 2>(a.out, a.W, a.H, pix, acc0, acc1, acc2, a.t_in[pix]);
     }
     work_counter_exit(a.counter, lane);
 }
 
-template <bool kBwd>
+template <int kMode>
 static int launch_rec(RecArgs a, cudaStream_t s) {
     static int grid = 0;
     if (grid == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         RCGS_CUDA(cudaGetDevice(&dev));
         RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<true>, kCTA, 0));
+        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<1>, kCTA, 0));
         grid = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int blocks = (int)min((int64_t)grid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
-    if (blocks > 0) rec_kernel<kBwd><<<blocks, kCTA, 0, s>>>(a);
+    if (blocks > 0) rec_kernel<kMode><<<blocks, kCTA, 0, s>>>(a);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }
@@ -861,11 +866,11 @@ static int render_into(const rcgs_view* v, const PixelOut& out, cudaStream_t s) 
     if (records_valid(v)) {  // weights recorded by an earlier rcgs_render_train: SpMV
         RecArgs ra = rec_args(v);
         ra.out = out;
-        return launch_rec<false>(ra, s);
+        return out.layout == 2 ? launch_rec<2>(ra, s) : launch_rec<0>(ra, s);
     }
     RasterArgs a = base_args(v);
     a.out = out;
-    return launch<FWD>(a, s);
+    return out.layout == 2 ? launch<FWDRGBA>(a, s) : launch<FWD>(a, s);
 }
 
 static PixelOut image_out(const float* h_bg, int layout, float* d_image, float* d_t_final) {
@@ -1057,7 +1062,7 @@ extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, floa
         ra.grad = d_grad_image;
         ra.acc_fx = acc_fx;
         ra.nonfinite = d_nonfinite;
-        RCGS_TRY(launch_rec<true>(ra, s));
+        RCGS_TRY(launch_rec<1>(ra, s));
     } else if (v->pairs > 0) {
         RasterArgs a = base_args(v);
         a.grad = d_grad_image;
