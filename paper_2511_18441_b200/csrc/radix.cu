@@ -7,7 +7,7 @@
 // emitted in depth-rank order, so a stable sort on the tile id alone yields
 // (tile, depth) order.
 //
-// Each 8-bit pass is three kernels over 1024-item tiles, all tiles independent:
+// Each 8-bit pass is three kernels over 2048-item tiles, all tiles independent:
 //   upsweep    per-tile digit histogram (warp-aggregated shared atomics), also
 //              added into the pass's global digit totals
 //   scan       one block per digit: the digit's start (totals of the digits
@@ -27,9 +27,12 @@ namespace rcgs {
 
 constexpr int kRNT = 256;
 constexpr int kRWarps = kRNT / 32;
-constexpr int kRIPT = 4;
-constexpr int kRTile = kRNT * kRIPT;      // 1024 items per tile
-constexpr int kRPerWarp = kRTile / kRWarps; // 128 consecutive items per warp
+#ifndef RCGS_RADIX_IPT
+#define RCGS_RADIX_IPT 8
+#endif
+constexpr int kRIPT = RCGS_RADIX_IPT;
+constexpr int kRTile = kRNT * kRIPT;      // 2048 items per tile
+constexpr int kRPerWarp = kRTile / kRWarps; // 256 consecutive items per warp
 constexpr uint32_t kValMask = (1u << 30) - 1u;
 constexpr int kMaxPasses = 8;
 
