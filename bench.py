@@ -146,7 +146,8 @@ def sync_max(t, world):
     import torch
     if world == 1:
         return t
-    x = torch.tensor([t], dtype=torch.float64, device="cuda")
+    dev = "cpu" if torch.distributed.get_backend() == "gloo" else "cuda"
+    x = torch.tensor([t], dtype=torch.float64, device=dev)
     torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
     return float(x.item())
 
@@ -160,11 +161,20 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RCGS_DEVICE_OVERRIDE / RCGS_DIST_BACKEND=gloo: functional test of the multi-rank
+    # path with every rank on one GPU (host-staged collectives); the scaling runs use
+    # one GPU per rank and NCCL
+    if "RCGS_DEVICE_OVERRIDE" in os.environ:
+        local = int(os.environ["RCGS_DEVICE_OVERRIDE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("RCGS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:
+            torch.distributed.init_process_group(backend)
         group = torch.distributed.group.WORLD
     cfg = CONFIGS[args.config]
     npix = cfg["width"] * cfg["height"]

@@ -37,6 +37,11 @@ def draw_views(rng: np.random.Generator, n_views: int, world: int) -> list[int]:
     return [int(x) for x in rng.integers(n_views, size=world)]
 
 
+def _host_staged(group) -> bool:
+    """gloo cannot run every collective on device tensors: stage them through host memory."""
+    return dist.get_backend(group) == "gloo"
+
+
 def exchange_accs(acc: torch.Tensor, group, out: torch.Tensor | None = None) -> list[torch.Tensor]:
     """All-gather the local (N, 3) channel sums; returns one tensor per rank in rank order."""
     world, _ = world_of(group)
@@ -44,8 +49,13 @@ def exchange_accs(acc: torch.Tensor, group, out: torch.Tensor | None = None) -> 
         return [acc]
     if out is None:
         out = torch.empty((world,) + tuple(acc.shape), dtype=acc.dtype, device=acc.device)
-    if acc.is_cuda:
+    if acc.is_cuda and not _host_staged(group):
         dist.all_gather_into_tensor(out, acc.contiguous(), group=group)
+    elif acc.is_cuda:  # gloo with device tensors (functional multi-rank tests on one GPU)
+        host = out.cpu()
+        parts = list(host.unbind(0))
+        dist.all_gather(parts, acc.contiguous().cpu(), group=group)
+        out.copy_(host)
     else:  # gloo: list form
         parts = list(out.unbind(0))
         dist.all_gather(parts, acc.contiguous(), group=group)
@@ -55,7 +65,12 @@ def exchange_accs(acc: torch.Tensor, group, out: torch.Tensor | None = None) -> 
 def any_rank(flag: torch.Tensor, group) -> torch.Tensor:
     world, _ = world_of(group)
     if world > 1:
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        if flag.is_cuda and _host_staged(group):
+            h = flag.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+            flag.copy_(h)
+        else:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
     return flag
 
 
@@ -69,4 +84,9 @@ def reduce_counts(group, *tensors: torch.Tensor) -> None:
     world, _ = world_of(group)
     if world > 1:
         for t in tensors:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            if t.is_cuda and _host_staged(group):
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
