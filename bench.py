@@ -282,6 +282,7 @@ def run_gpu(args):
     interactive = run_interactive(args, scene, cams, ds, sh0, sp, cloud) if args.extras and rank == 0 else None
     resident = run_resident_views(args, ds, sh0, cams, sp) if args.extras and world == 1 else None
     select_mask = run_select_from_mask(scene, cams, ds) if args.extras and rank == 0 else None
+    checkpoint = run_checkpoint_io(scene, sh0) if args.extras and rank == 0 else None
     if args.extras:
         del sp, targets, gt
         torch.cuda.empty_cache()
@@ -348,6 +349,7 @@ def run_gpu(args):
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         "interactive_c5": interactive, "selection_sweep_c4": sweep, "resident_views": resident,
         "select_from_mask": select_mask,
+        "checkpoint_io": checkpoint,
     }
     print(json.dumps(line))
 
@@ -504,6 +506,58 @@ def run_select_from_mask(scene, cams, ds):
             "remove_outliers_ms": round(t_gpu * 1e3, 2), "scipy_remove_outliers_ms": round(t_cpu * 1e3, 2),
             "identical": bool(np.array_equal(kept.points, ref)),
             "note": "full-frame 1080p brush on view 0; GPU kNN (k=16) + host numpy threshold vs scipy cKDTree"}
+
+
+def run_checkpoint_io(scene, sh_dev):
+    """the workload scene as a PLY checkpoint (scene_io.py:108-180).
+    Host load/save (the reference's numpy path, restated) beside the device
+    decode (rcgs_ply_decode into DeviceScene + fp32 SH) and the device encode of
+    the live SH (rcgs_ply_encode_sh + one D2H); wall-clock, file in a temp dir
+    (page cache warm after the first write).  Outputs are checked identical."""
+    import tempfile
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200 import scene_io as S
+
+    out = {"gaussians": len(scene)}
+    with tempfile.TemporaryDirectory() as tmp:
+        host_path, dev_path = os.path.join(tmp, "h.ply"), os.path.join(tmp, "d.ply")
+        t0 = time.perf_counter()
+        P.save_scene_ply(scene, host_path)
+        out["host_save_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        times = []
+        for _ in range(3):  # the first call also encodes + uploads the geometry columns
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            S.save_scene_ply_device(scene, sh_dev, dev_path)
+            times.append((time.perf_counter() - t0) * 1e3)
+        out["device_save_ms_first"], out["device_save_ms"] = round(times[0], 1), round(min(times[1:]), 1)
+        with open(host_path, "rb") as fa, open(dev_path, "rb") as fb:
+            same_file = fa.read() == fb.read()
+        out["file_mb"] = round(os.path.getsize(host_path) / 1e6, 1)
+        t0 = time.perf_counter()
+        host = P.load_scene_ply(host_path)
+        out["host_load_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dsc, sh = P.load_scene_ply_device(host_path)
+            torch.cuda.synchronize()
+            times.append((time.perf_counter() - t0) * 1e3)
+            if len(times) < 3:
+                dsc.close()
+        out["device_load_ms"] = round(min(times), 1)
+        same_load = (np.array_equal(dsc.positions.cpu().numpy(), host.positions)
+                     and np.array_equal(dsc.rotations.cpu().numpy(), host.rotations)
+                     and np.array_equal(dsc.scales.cpu().numpy(), host.scales)
+                     and np.array_equal(dsc.opacities.cpu().numpy(), host.opacities)
+                     and np.array_equal(sh.cpu().numpy(), host.sh.astype(np.float32)))
+        dsc.close()
+    out["identical"] = bool(same_file and same_load)
+    out["note"] = ("device load = DeviceScene + fp32 SH ready for the refit; host load = host Scene only "
+                   "(the reference's path, which then still needs the upload)")
+    return out
 
 
 def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):

@@ -213,6 +213,23 @@ int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grad
 /* OR 1 into *d_flag if any of d_x[0..count) is non-finite. */
 int rcgs_nonfinite_check(const float* d_x, int64_t count, int32_t* d_flag, void* stream);
 
+/* ---- scene checkpoints (scene_io.py:108-153) --------------------------------------------- */
+/* Decode n raw float32 PLY vertex rows of row_floats floats (property positions
+ * in h_offsets59: x y z, rot_0..3, f_dc_0..2, f_rest_0..44, opacity, scale_0..2)
+ * into fp64 positions (N,3), normalised fp64 rotations (N,4) and fp32 SH
+ * (N,16,3) (channel-major f_rest transposed), values identical to the reference
+ * loader; h_first_bad7 receives the first vertex with a non-finite position /
+ * opacity / scale / rotation / f_dc / f_rest and the first zero-norm quaternion
+ * (-1 if none).  Synchronises `stream`. */
+int rcgs_ply_decode(const float* d_rows, int64_t n, int32_t row_floats, const int32_t* h_offsets59,
+                    double* d_pos, double* d_rot, float* d_sh, int64_t* h_first_bad7, void* stream);
+/* Write the 48 SH columns of n checkpoint rows (same offsets as rcgs_ply_decode) from
+ * the device SH (scene_io.py:156-166): float32(d_base + (d_new - d_old)) in fp64 when
+ * d_base (N,16,3 fp64) is given -- the published snapshot's value, optimize.py:226-238 --
+ * else d_new.  The other columns of d_rows are left as they are.  Asynchronous. */
+int rcgs_ply_encode_sh(const double* d_base, const float* d_old, const float* d_new, int64_t n,
+                       int32_t row_floats, const int32_t* h_offsets59, float* d_rows, void* stream);
+
 /* ---- select-from-mask outlier statistics (selection.py:155-181) ---------------------- */
 /* knn_mean_distances: per point of the (m,3) fp64 cloud, the mean distance to its
  * k nearest neighbours (self excluded), bit-identical to scipy cKDTree.query(k+1)

@@ -83,6 +83,22 @@ class DeviceScene:
         torch.cuda.current_stream().synchronize()  # inputs may be freed after this
 
     @classmethod
+    def from_device(cls, pos, rot, scl, opa, sh_degree: int) -> "DeviceScene":
+        """From fp64 device tensors (N,3) positions, (N,4) unit rotations, (N,3) scales, (N,)."""
+        self = cls.__new__(cls)
+        self.n = int(pos.shape[0])
+        self.sh_degree = int(sh_degree)
+        self.positions = pos.contiguous()
+        # the decoded geometry stays readable (checkpoint parity, host snapshots)
+        self.rotations, self.scales, self.opacities = rot.contiguous(), scl.contiguous(), opa.contiguous()
+        h = ctypes.c_void_p()
+        N.call("rcgs_scene_create", N.ptr(self.positions), N.ptr(self.rotations), N.ptr(self.scales),
+               N.ptr(self.opacities), self.n, self.sh_degree, stream_ptr(), ctypes.byref(h))
+        self.handle = h
+        torch.cuda.current_stream().synchronize()  # inputs may be freed after this
+        return self
+
+    @classmethod
     def from_scene(cls, scene) -> "DeviceScene":
         return cls(scene.positions, scene.rotations, scene.scales, scene.opacities, scene.sh_degree)
 

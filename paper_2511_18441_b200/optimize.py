@@ -168,6 +168,7 @@ class BackgroundOptimizer:
         self._pending_dataset = None
         self._accepted = 0
         self._snapshot_sh = self._sh0.clone()
+        self._sh_base = None  # fp64 host SH on the device, uploaded on the first save_ply
         self._snapshot_cache = (None, None)
         self._current_cache = (None, None)
         self._version = 0
@@ -226,6 +227,17 @@ class BackgroundOptimizer:
     def current_scene(self):
         with self._lock:
             return self._materialise(self._engine.sh, "_current_cache")
+
+    def save_ply(self, path) -> None:
+        """Checkpoint of the current SH (session.py:328-333 saves current_scene()
+        through scene_io.py:156): encoded on the device from the live fp32 SH and
+        byte-identical to save_scene_ply(self.current_scene())."""
+        from .scene_io import save_scene_ply_device
+
+        with self._lock:
+            if self._sh_base is None:
+                self._sh_base = torch.from_numpy(np.ascontiguousarray(self._scene0.sh)).to(self._sh0.device)
+            save_scene_ply_device(self._scene0, self._engine.sh, path, sh_base=(self._sh_base, self._sh0))
 
     def status(self) -> OptimizerStatus:
         with self._lock:
