@@ -213,6 +213,24 @@ int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grad
 /* OR 1 into *d_flag if any of d_x[0..count) is non-finite. */
 int rcgs_nonfinite_check(const float* d_x, int64_t count, int32_t* d_flag, void* stream);
 
+/* ---- stereo depth (stereo.py:61-219) ------------------------------------------------------ */
+/* match_disparity (stereo.py:142-161): ZNCC block matching of two (H,W,channels)
+ * float32/float64 (elem_bytes 4/8, both alike) images (gray = channel mean) with parabolic sub-pixel refinement and
+ * the left-right check; transpose != 0 matches along the image columns (the
+ * vertical pair, stereo.py:207-209).  Writes the (H,W) float64 disparity, -1 where
+ * invalid; bit-identical to the reference for the same images (the box means
+ * restate scipy.ndimage.uniform_filter's running sums).  variance_floor_sq is the
+ * host's variance_floor ** 2.  Asynchronous on `stream` (workspace from the pool). */
+int rcgs_stereo_match(const void* d_left, const void* d_right, int32_t height, int32_t width,
+                      int32_t channels_left, int32_t channels_right, int32_t elem_bytes, int32_t transpose, int32_t max_disparity, int32_t window_radius,
+                      double variance_floor, double variance_floor_sq, double lr_tolerance, double* d_disparity,
+                      void* stream);
+/* disparity_to_depth + aggregate_hv (+ estimate_depth's backfill when d_fallback is
+ * non-null) over n pixels (stereo.py:164-219): fx_baseline = fx * baseline. */
+int rcgs_stereo_depth(const double* d_disp_h, const double* d_disp_v, int64_t n, double fx_baseline,
+                      double fy_baseline, double min_disparity, const double* d_fallback, double* d_depth,
+                      void* stream);
+
 /* ---- scene checkpoints (scene_io.py:108-153) --------------------------------------------- */
 /* Decode n raw float32 PLY vertex rows of row_floats floats (property positions
  * in h_offsets59: x y z, rot_0..3, f_dc_0..2, f_rest_0..44, opacity, scale_0..2)
