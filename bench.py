@@ -283,6 +283,7 @@ def run_gpu(args):
     resident = run_resident_views(args, ds, sh0, cams, sp) if args.extras and world == 1 else None
     select_mask = run_select_from_mask(scene, cams, ds) if args.extras and rank == 0 else None
     checkpoint = run_checkpoint_io(scene, sh0) if args.extras and rank == 0 else None
+    stereo = run_stereo(scene, cams, ds, sh0) if args.extras and rank == 0 else None
     if args.extras:
         del sp, targets, gt
         torch.cuda.empty_cache()
@@ -350,6 +351,7 @@ def run_gpu(args):
         "interactive_c5": interactive, "selection_sweep_c4": sweep, "resident_views": resident,
         "select_from_mask": select_mask,
         "checkpoint_io": checkpoint,
+        "stereo_depth": stereo,
     }
     print(json.dumps(line))
 
@@ -506,6 +508,32 @@ def run_select_from_mask(scene, cams, ds):
             "remove_outliers_ms": round(t_gpu * 1e3, 2), "scipy_remove_outliers_ms": round(t_cpu * 1e3, 2),
             "identical": bool(np.array_equal(kept.points, ref)),
             "note": "full-frame 1080p brush on view 0; GPU kNN (k=16) + host numpy threshold vs scipy cKDTree"}
+
+
+def run_stereo(scene, cams, ds, sh_dev, reps=5):
+    """estimate_depth("stereo-hv") of a workload view on the
+    device -- 3 renders (left, +x and +y eyes), 2 ZNCC matches with the LR check
+    (65 disparities, 11x11 windows, fp64), fusion and the gaussian-depth backfill.
+    CUDA events around `reps` calls."""
+    import torch
+    from paper_2511_18441_b200 import stereo as S
+
+    intr, pose = cams[0]
+    base = S.default_baseline(scene)
+    run = lambda: S.stereo_hv_depth_device(ds, sh_dev, intr, pose, base, backfill_tau=0.5)  # noqa: E731
+    out = run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"ms_per_view": round(ms, 2), "resolution": [int(intr.width), int(intr.height)],
+"depth_finite": round(float(torch.isfinite(out).double().mean()), 4),
+            "match_mpix_per_s": round(2 * intr.width * intr.height / (ms * 1e3), 1),
+            "note": "3 renders + 2 matches (each with its mirrored LR pass) + fusion + backfill, per view"}
 
 
 def run_checkpoint_io(scene, sh_dev):

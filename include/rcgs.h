@@ -225,6 +225,9 @@ int rcgs_stereo_match(const void* d_left, const void* d_right, int32_t height, i
                       int32_t channels_left, int32_t channels_right, int32_t elem_bytes, int32_t transpose, int32_t max_disparity, int32_t window_radius,
                       double variance_floor, double variance_floor_sq, double lr_tolerance, double* d_disparity,
                       void* stream);
+/* Diagnostics: count operands t where the matcher's fused division by the window
+ * size differs from IEEE t / size (n pseudo-random t over 64 binades); must be 0. */
+int rcgs_stereo_div_check(int32_t size, int64_t n, uint64_t seed, int64_t* h_mismatches, void* stream);
 /* disparity_to_depth + aggregate_hv (+ estimate_depth's backfill when d_fallback is
  * non-null) over n pixels (stereo.py:164-219): fx_baseline = fx * baseline. */
 int rcgs_stereo_depth(const double* d_disp_h, const double* d_disp_v, int64_t n, double fx_baseline,

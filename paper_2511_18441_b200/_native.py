@@ -80,6 +80,7 @@ _SIGNATURES = {
     "rcgs_ply_encode_sh": [c_void_p, c_void_p, c_void_p, c_i64, c_i32, P(ctypes.c_int32), c_void_p, c_void_p],
     "rcgs_stereo_match": [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_double,
                           c_double, c_double, c_void_p, c_void_p],
+    "rcgs_stereo_div_check": [c_i32, c_i64, ctypes.c_uint64, P(c_i64), c_void_p],
     "rcgs_stereo_depth": [c_void_p, c_void_p, c_i64, c_double, c_double, c_double, c_void_p, c_void_p, c_void_p],
     "rcgs_knn_mean_distances": [c_void_p, c_i64, c_i32, c_void_p, c_void_p],
     "rcgs_project_cloud": [c_void_p, c_i64, P(Camera), c_void_p, c_i32, c_double, c_void_p,

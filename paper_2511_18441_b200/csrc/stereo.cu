@@ -24,8 +24,10 @@ struct StereoDims {
     int h, w;      // oriented image (rows matched along x)
     int nd;        // max_disparity + 1 (score entries per pixel)
     int nde;       // min(nd, w): disparities that can be valid
+    int nw;        // warps of 32 disparities per row (ceil(nde / 32))
     int r;         // window radius
     double size;   // 2r + 1
+    double inv;    // RN(1 / size)
     double floor_v, floor_sq, lr_tol;
 };
 
@@ -35,14 +37,23 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// RN(t / size) without the general division routine: q = RN(t * RN(1/size)) is
+// faithful, the remainder t - q*size is exact in one fma, and RN(q + rem/size
+// estimate) is the correctly rounded quotient (Markstein's correction step);
+// rcgs_stereo_div_check verifies it against __ddiv_rn on the GPU.
+__device__ __forceinline__ double div_size(double t, double size, double inv) {
+    const double q = __dmul_rn(t, inv);
+    const double rem = __fma_rn(-q, size, t);
+    return __fma_rn(rem, inv, q);
+}
+
 // Gray planes in the matching orientation (transpose: rows of the match are the
 // image columns, stereo.py:207-209): P0 = gray(left), P1 = gray(right),
 // P2 = mirror(gray(right)), P3 = mirror(gray(left)) (the LR pass, stereo.py:143).
 // gray = mean over channels, numpy order ((r + g) + b) / 3 (stereo.py:87-94).
 template <typename T>
 __global__ void stereo_gray_kernel(const T* __restrict__ left, const T* __restrict__ right, int ch_l, int ch_r,
-                                   int transpose,
-                                   StereoDims sd, double* __restrict__ planes) {
+                                   int transpose, StereoDims sd, double* __restrict__ planes) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t np = (int64_t)sd.h * sd.w;
     if (i >= np) return;
@@ -63,146 +74,311 @@ __global__ void stereo_gray_kernel(const T* __restrict__ left, const T* __restri
     planes[3 * np + mi] = gl;
 }
 
-// Vertical running box of A, A*A, B, B*B (thread per (column, plane)).
-__global__ void stereo_vbox_planes_kernel(const double* __restrict__ A, const double* __restrict__ B, StereoDims sd,
-                                          double* __restrict__ out4) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 4 * sd.w) return;
-    const int k = i / sd.w, x = i - k * sd.w;
-    const double* src = k < 2 ? A : B;
-    const bool sq = k & 1;
-    double* out = out4 + (int64_t)k * sd.h * sd.w;
-    auto val = [&](int y) {
-        const double v = src[(int64_t)clampi(y, sd.h) * sd.w + x];
-        return sq ? dmul(v, v) : v;
-    };
+// One line of scipy's uniform_filter1d(mode="nearest"): tmp = sum of the first
+// window (in order), then tmp += (new - old); every output is tmp / size.  val(i)
+// reads the line at a clamped index.  Loads are issued kU steps ahead of the
+// dependent adds so the walk is bound by the add chain, not by load latency.
+template <int kU, class Val, class Emit>
+__device__ __forceinline__ void box_line(int n, const StereoDims& sd, Val val, Emit emit) {
     double tmp = 0.0;
     for (int j = -sd.r; j <= sd.r; ++j) tmp = dadd(tmp, val(j));
-    out[x] = ddiv(tmp, sd.size);
-    for (int y = 1; y < sd.h; ++y) {
-        tmp = dadd(tmp, dsub(val(y + sd.r), val(y - sd.r - 1)));
-        out[(int64_t)y * sd.w + x] = ddiv(tmp, sd.size);
+    emit(0, div_size(tmp, sd.size, sd.inv));
+    int i = 1;
+    for (; i + kU <= n; i += kU) {
+        double vn[kU], vo[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            vn[u] = val(i + u + sd.r);
+            vo[u] = val(i + u - sd.r - 1);
+        }
+        asm volatile("" ::: "memory");  // keep the kU loads in flight together (ptxas sinks them otherwise)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            tmp = dadd(tmp, dsub(vn[u], vo[u]));
+            emit(i + u, div_size(tmp, sd.size, sd.inv));
+        }
     }
+    for (; i < n; ++i) {
+        tmp = dadd(tmp, dsub(val(i + sd.r), val(i - sd.r - 1)));
+        emit(i, div_size(tmp, sd.size, sd.inv));
+    }
+}
+
+// The same line walk with the line streamed through a private shared-memory ring
+// by cp.async (8-byte copies, kGA groups of kC elements in flight): the copies
+// cannot be sunk next to their use by the compiler, so the walk is bound by the
+// add chain even with few lines in flight.  Element k of the stream is the line
+// at clamp(k - r); ring slot k % kR, thread stride `ts` (conflict-free).
+// Requires kR > 2r + 1 + (kGA + 1) * kC (old values are read from the ring).
+constexpr int kRing = 64, kRingC = 8, kRingGA = 4;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+__host__ __device__ constexpr int ring_max_radius() { return (kRing - 2 - (kRingGA + 1) * kRingC) / 2; }
+
+template <class Addr, class Xf, class Emit>
+__device__ __forceinline__ void box_line_ring(int n, const StereoDims& sd, Addr addr, Xf xf, double* ring, int ts,
+                                              Emit emit) {
+    const int total = n + 2 * sd.r;
+    auto issue = [&](int g) {
+#pragma unroll
+        for (int u = 0; u < kRingC; ++u) {
+            const int k = g * kRingC + u;
+            if (k < total) cp_async8(ring + (k % kRing) * ts, addr(clampi(k - sd.r, n)));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // one group per call keeps the count uniform
+    };
+    auto e = [&](int k) { return xf(ring[(k % kRing) * ts]); };
+#pragma unroll 1
+    for (int g = 0; g < kRingGA; ++g) issue(g);
+    double tmp = 0.0;
+    const int last = 2 * sd.r;
+    const int groups = (total + kRingC - 1) / kRingC;
+#pragma unroll 1
+    for (int g = 0; g < groups; ++g) {
+        issue(g + kRingGA);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRingGA) : "memory");
+#pragma unroll
+        for (int u = 0; u < kRingC; ++u) {
+            const int k = g * kRingC + u;
+            if (k >= total) break;
+            if (k <= last) {
+                tmp = dadd(tmp, e(k));
+                if (k == last) emit(0, div_size(tmp, sd.size, sd.inv));
+            } else {
+                tmp = dadd(tmp, dsub(e(k), e(k - last - 1)));
+                emit(k - last, div_size(tmp, sd.size, sd.inv));
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Vertical running box of A, A*A, B, B*B (thread per (column, plane)).
+// blockIdx.y = pass (0: left/right, 1: mirrored right/left); gray planes 2p, 2p+1.
+__global__ void __launch_bounds__(64) stereo_vbox_planes_kernel(const double* __restrict__ planes, StereoDims sd, double* __restrict__ v4) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * sd.w) return;
+    const int64_t np = (int64_t)sd.h * sd.w;
+    const int k = i / sd.w, x = i - k * sd.w;
+    const double* src = planes + (2 * blockIdx.y + (k >> 1)) * np;
+    const bool sq = k & 1;
+    double* out = v4 + (4 * blockIdx.y + k) * np + x;
+    __shared__ double ring[kRing * 64];
+    if (sd.r <= ring_max_radius()) {
+        box_line_ring(sd.h, sd, [&](int y) { return src + (int64_t)y * sd.w + x; },
+                      [&](double v) { return sq ? dmul(v, v) : v; }, ring + threadIdx.x, 64,
+                      [&](int y, double m) { out[(int64_t)y * sd.w] = m; });
+        return;
+    }
+    box_line<32>(sd.h, sd, [&](int y) {
+        const double v = src[(int64_t)clampi(y, sd.h) * sd.w + x];
+        return sq ? dmul(v, v) : v;
+    }, [&](int y, double m) { out[(int64_t)y * sd.w] = m; });
 }
 
 // Horizontal running box of the vertical planes VA, VA2 -> box(A), box(A*A)
 // (thread per (row, plane)).
-__global__ void stereo_hbox_left_kernel(const double* __restrict__ v4, StereoDims sd, double* __restrict__ mu_ex) {
+__global__ void __launch_bounds__(64) stereo_hbox_left_kernel(const double* __restrict__ v4, StereoDims sd, double* __restrict__ mu_ex) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * sd.h) return;
+    const int64_t np = (int64_t)sd.h * sd.w;
     const int k = i / sd.h, y = i - k * sd.h;
-    const double* line = v4 + (int64_t)k * sd.h * sd.w + (int64_t)y * sd.w;
-    double* out = mu_ex + (int64_t)k * sd.h * sd.w + (int64_t)y * sd.w;
-    auto val = [&](int x) { return line[clampi(x, sd.w)]; };
-    double tmp = 0.0;
-    for (int j = -sd.r; j <= sd.r; ++j) tmp = dadd(tmp, val(j));
-    out[0] = ddiv(tmp, sd.size);
-    for (int x = 1; x < sd.w; ++x) {
-        tmp = dadd(tmp, dsub(val(x + sd.r), val(x - sd.r - 1)));
-        out[x] = ddiv(tmp, sd.size);
+    const double* line = v4 + (4 * blockIdx.y + k) * np + (int64_t)y * sd.w;
+    double* out = mu_ex + (2 * blockIdx.y + k) * np + (int64_t)y * sd.w;
+    __shared__ double ring[kRing * 64];
+    if (sd.r <= ring_max_radius()) {
+        box_line_ring(sd.w, sd, [&](int x) { return line + x; }, [](double v) { return v; }, ring + threadIdx.x, 64,
+                      [&](int x, double m) { out[x] = m; });
+        return;
     }
+    box_line<32>(sd.w, sd, [&](int x) { return line[clampi(x, sd.w)]; }, [&](int x, double m) { out[x] = m; });
 }
 
 // Vertical running box of A * shift_d(B) for every disparity, written [y][x][d]
 // (thread per (column, d), d fastest).  shift_d(B)[y, x] = B[y, max(x - d, 0)]
 // (stereo.py:110-112).
-__global__ void stereo_vbox_products_kernel(const double* __restrict__ A, const double* __restrict__ B, StereoDims sd,
-                                            double* __restrict__ vab) {
+__global__ void stereo_vbox_products_kernel(const double* __restrict__ planes, StereoDims sd,
+                                            double* __restrict__ vab_all) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)sd.w * sd.nde) return;
+    const int64_t np = (int64_t)sd.h * sd.w;
+    const double* A = planes + (2 * blockIdx.y) * np;
+    const double* B = planes + (2 * blockIdx.y + 1) * np;
+    double* vab = vab_all + blockIdx.y * np * sd.nd;
     const int x = (int)(i / sd.nde), d = (int)(i - (int64_t)x * sd.nde);
     const int xs = x - d > 0 ? x - d : 0;
-    auto val = [&](int y) {
-        const int64_t row = (int64_t)clampi(y, sd.h) * sd.w;
-        return dmul(A[row + x], B[row + xs]);
-    };
     const int64_t pitch = (int64_t)sd.w * sd.nd;  // one row of the volume
     double* out = vab + (int64_t)x * sd.nd + d;
-    double tmp = 0.0;
-    for (int j = -sd.r; j <= sd.r; ++j) tmp = dadd(tmp, val(j));
-    out[0] = ddiv(tmp, sd.size);
-    for (int y = 1; y < sd.h; ++y) {
-        tmp = dadd(tmp, dsub(val(y + sd.r), val(y - sd.r - 1)));
-        out[(int64_t)y * pitch] = ddiv(tmp, sd.size);
-    }
+    box_line<8>(sd.h, sd, [&](int y) {
+        const int64_t row = (int64_t)clampi(y, sd.h) * sd.w;
+        return dmul(A[row + x], B[row + xs]);
+    }, [&](int y, double m) { out[(int64_t)y * pitch] = m; });
 }
 
-// Horizontal running boxes of shift_d(VB), shift_d(VB2) and V(A*shift_d(B)) along
-// each row, with the ZNCC score of every (x, d) (stereo.py:113-117); thread per
-// (row, d), d fastest.  Scores are written [y][x][d].
-__global__ void stereo_hscore_kernel(const double* __restrict__ v4, const double* __restrict__ mu_ex,
-                                     const double* __restrict__ vab, StereoDims sd, double* __restrict__ scores) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)sd.h * sd.nde) return;
-    const int y = (int)(i / sd.nde), d = (int)(i - (int64_t)y * sd.nde);
-    const int64_t np = (int64_t)sd.h * sd.w;
-    const double* vb = v4 + 2 * np + (int64_t)y * sd.w;
-    const double* vb2 = v4 + 3 * np + (int64_t)y * sd.w;
-    const double* mul = mu_ex + (int64_t)y * sd.w;
-    const double* exl = mu_ex + np + (int64_t)y * sd.w;
-    const double* pab = vab + (int64_t)y * sd.w * sd.nd + d;
-    double* out = scores + (int64_t)y * sd.w * sd.nd + d;
-    auto sh = [&](int x) {  // column of the shifted image's vertical box at x (nearest-extended)
-        const int c = clampi(x, sd.w) - d;
+// Per (pixel, warp of 32 disparities): the warp's first maximum and the scores
+// around it -- enough to finish np.argmax + the parabolic refinement without the
+// (nd, H, W) score volume.
+struct ScorePart {
+    double best_d, s_best, s_prev, s_next, s_first, s_last;
+};
+
+__device__ __forceinline__ bool better(double a, int da, double b, int db) {  // np.argmax order
+    const bool na = isnan(a), nb = isnan(b);
+    if (na || nb) return na && (!nb || da < db);
+    return a > b || (a == b && da < db);
+}
+
+// One (row, disparity) walk of the horizontal pass: running boxes of shift_d(VB),
+// shift_d(VB2) and V(A*shift_d(B)) along the row and the ZNCC score at every x
+// (stereo.py:113-117).  init() sums the first window; score(x, pab_new) advances
+// to x (x > 0) and returns the score, -2 where invalid.
+struct ScoreWalk {
+    const double *vb, *vb2, *mul, *exl, *pab;
+    int d, da;
+    bool active;
+    double t1, t2, t3;
+    const StereoDims* sd;
+
+    __device__ __forceinline__ int sh(int x) const {  // column of the shifted image's vertical box (nearest)
+        const int c = clampi(x, sd->w) - da;
         return c > 0 ? c : 0;
-    };
-    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
-    for (int j = -sd.r; j <= sd.r; ++j) {
-        const int c = sh(j);
-        t1 = dadd(t1, vb[c]);
-        t2 = dadd(t2, vb2[c]);
-        t3 = dadd(t3, pab[(int64_t)clampi(j, sd.w) * sd.nd]);
     }
-    for (int x = 0; x < sd.w; ++x) {
+    __device__ __forceinline__ double pv(int x) const { return pab[(int64_t)clampi(x, sd->w) * sd->nd]; }
+    __device__ __forceinline__ void init() {
+        t1 = t2 = t3 = 0.0;
+        for (int j = -sd->r; j <= sd->r; ++j) {
+            const int c = sh(j);
+            t1 = dadd(t1, vb[c]);
+            t2 = dadd(t2, vb2[c]);
+            t3 = dadd(t3, pv(j));
+        }
+    }
+    __device__ __forceinline__ double score(int x, double pnew) {
         if (x > 0) {
-            const int cn = sh(x + sd.r), co = sh(x - sd.r - 1);
+            const int cn = sh(x + sd->r), co = sh(x - sd->r - 1);
             t1 = dadd(t1, dsub(vb[cn], vb[co]));
             t2 = dadd(t2, dsub(vb2[cn], vb2[co]));
-            t3 = dadd(t3, dsub(pab[(int64_t)clampi(x + sd.r, sd.w) * sd.nd],
-                               pab[(int64_t)clampi(x - sd.r - 1, sd.w) * sd.nd]));
+            t3 = dadd(t3, dsub(pnew, pv(x - sd->r - 1)));
         }
-        const double mu_r = ddiv(t1, sd.size), ex_r2 = ddiv(t2, sd.size), ex_ab = ddiv(t3, sd.size);
+        const double mu_r = div_size(t1, sd->size, sd->inv), ex_r2 = div_size(t2, sd->size, sd->inv);
+        const double ex_ab = div_size(t3, sd->size, sd->inv);
         const double mu_l = mul[x];
         const double var_l = dsub(exl[x], dmul(mu_l, mu_l));
         const double var_r = dsub(ex_r2, dmul(mu_r, mu_r));
         const double cov = dsub(ex_ab, dmul(mu_l, mu_r));
-        const bool ok = var_l >= sd.floor_v && var_r >= sd.floor_v && x >= d;
+        if (!(active && var_l >= sd->floor_v && var_r >= sd->floor_v && x >= d)) return -2.0;
         const double p = dmul(var_l, var_r);
-        const double den = __dsqrt_rn(p < sd.floor_sq ? sd.floor_sq : p);  // np.maximum keeps a NaN
-        out[(int64_t)x * sd.nd] = ok ? ddiv(cov, den) : -2.0;
+        return ddiv(cov, __dsqrt_rn(p < sd->floor_sq ? sd->floor_sq : p));  // np.maximum keeps a NaN
     }
-}
+};
 
-// argmax over d (first maximum; np.argmax also stops at the first NaN) and the
-// parabolic refinement of stereo.py:121-139.  Entries d >= w are -2 (stereo.py:107-108).
-__device__ __forceinline__ double score_at(const double* s, int d, const StereoDims& sd) {
-    return d < sd.nde ? s[d] : -2.0;
-}
+// Horizontal pass + per-warp argmax epilogue.  A warp walks 32 consecutive
+// disparities of one row (lanes with d >= nde carry the reference's -2), so its
+// loads of the [y][x][d] volume are contiguous; the scores of 32 consecutive x
+// are staged in shared memory ([d][x], padded) and each lane then scans the 32
+// disparities of one pixel -- no per-step shuffles.  (Packing a lone last
+// disparity of 32 rows into one warp, lane = row, was tried: those warps walk
+// uncoalesced and became the critical path, 2.5x slower.)
+constexpr int kHsWarps = 4;
 
-__global__ void stereo_best_kernel(const double* __restrict__ scores, StereoDims sd, double* __restrict__ disp) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)sd.h * sd.w) return;
-    const double* s = scores + i * sd.nd;
-    int best = 0;
-    double s0 = score_at(s, 0, sd);
-    if (!isnan(s0)) {
-        for (int d = 1; d < sd.nd; ++d) {
-            const double v = score_at(s, d, sd);
-            if (isnan(v)) {
-                best = d;
-                s0 = v;
-                break;
-            }
-            if (v > s0) {
-                best = d;
-                s0 = v;
+__global__ void __launch_bounds__(32 * kHsWarps) stereo_hscore_kernel(const double* __restrict__ v4_all,
+                                                                      const double* __restrict__ mu_ex_all,
+                                                                      const double* __restrict__ vab_all, StereoDims sd,
+                                                                      ScorePart* __restrict__ parts_all) {
+    __shared__ double stage[kHsWarps][32][33];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t np = (int64_t)sd.h * sd.w;
+    const double* v4 = v4_all + 4 * blockIdx.y * np;
+    const double* mu_ex = mu_ex_all + 2 * blockIdx.y * np;
+    const double* vab = vab_all + blockIdx.y * np * sd.nd;
+    ScorePart* parts = parts_all + blockIdx.y * np * sd.nw;
+    ScoreWalk wk;
+    wk.sd = &sd;
+    if (gw >= (int64_t)sd.h * sd.nw) return;  // whole warps exit together
+    const int y = (int)(gw / sd.nw);
+    wk.d = (int)(gw - (int64_t)y * sd.nw) * 32 + lane;
+    wk.active = wk.d < sd.nde;
+    wk.da = wk.active ? wk.d : 0;  // inactive lanes read valid memory, results unused
+    wk.vb = v4 + 2 * np + (int64_t)y * sd.w;
+    wk.vb2 = v4 + 3 * np + (int64_t)y * sd.w;
+    wk.mul = mu_ex + (int64_t)y * sd.w;
+    wk.exl = mu_ex + np + (int64_t)y * sd.w;
+    wk.pab = vab + (int64_t)y * sd.w * sd.nd + wk.da;
+    wk.init();
+    const int wi = wk.d >> 5;
+    ScorePart* out = parts + (int64_t)y * sd.w * sd.nw + wi;
+    double(*st)[33] = stage[wl];
+    for (int x0 = 0; x0 < sd.w; x0 += 32) {
+#pragma unroll 1
+        for (int u0 = 0; u0 < 32; u0 += 8) {
+            double pn[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) pn[u] = wk.pv(x0 + u0 + u + sd.r);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int x = x0 + u0 + u;
+                st[lane][u0 + u] = x < sd.w ? wk.score(x, pn[u]) : -2.0;
             }
         }
+        __syncwarp();
+        const int x = x0 + lane;
+        if (x < sd.w) {  // lane = pixel: first maximum over this warp's 32 disparities
+            double bv = st[0][lane];
+            int bl = 0;
+            for (int k = 1; k < 32; ++k) {
+                const double v = st[k][lane];
+                if (better(v, k, bv, bl)) {
+                    bv = v;
+                    bl = k;
+                }
+            }
+            ScorePart pr;
+            pr.best_d = (double)(wi * 32 + bl);
+            pr.s_best = bv;
+            pr.s_prev = st[bl > 0 ? bl - 1 : 0][lane];
+            pr.s_next = st[bl < 31 ? bl + 1 : 31][lane];
+            pr.s_first = st[0][lane];
+            pr.s_last = st[31][lane];
+            out[(int64_t)x * sd.nw] = pr;
+        }
+        __syncwarp();
     }
-    double out = s0 <= -2.0 ? -1.0 : (double)best;
+}
+
+// Finish np.argmax over all disparities and the parabolic refinement of
+// stereo.py:121-139 from the per-warp parts.  Scores of d >= nde are -2
+// (stereo.py:107-108), as the lanes that produced them.
+__global__ void stereo_best_kernel(const ScorePart* __restrict__ parts, StereoDims sd, double* __restrict__ disp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t np = (int64_t)sd.h * sd.w;
+    if (i >= np) return;
+    const ScorePart* p = parts + (blockIdx.y * np + i) * sd.nw;
+    disp += blockIdx.y * np;
+    int wb = 0;
+    ScorePart b = p[0];
+    for (int k = 1; k < sd.nw; ++k) {
+        const ScorePart c = p[k];
+        if (better(c.s_best, (int)c.best_d, b.s_best, (int)b.best_d)) {
+            b = c;
+            wb = k;
+        }
+    }
+    int best = (int)b.best_d;
+    const double s0 = b.s_best;
+    if (best >= sd.nd) best = sd.nd - 1;  // cannot happen (-2 ties resolve to lower d); defensive
     const int dmax = sd.nd - 1;
-    const double sm = score_at(s, best - 1 > 0 ? best - 1 : 0, sd);
-    const double sp = score_at(s, best + 1 < dmax ? best + 1 : dmax, sd);
+    double out = s0 <= -2.0 ? -1.0 : (double)best;
+    const int lane = best - wb * 32;
+    const double sm = best == 0 ? s0 : (lane > 0 ? b.s_prev : p[wb - 1].s_last);
+    double sp;
+    if (best >= dmax) sp = s0;
+    else if (best + 1 >= sd.nde) sp = -2.0;
+    else sp = lane < 31 ? b.s_next : p[wb + 1].s_first;
     const bool refinable = best > 0 && best < dmax && sm > -2.0 && sp > -2.0 && s0 > -2.0;
     const double den = dsub(dadd(sm, sp), dmul(2.0, s0));
     if (refinable && den < -1e-12) {
@@ -211,6 +387,21 @@ __global__ void stereo_best_kernel(const double* __restrict__ scores, StereoDims
         out = dadd((double)best, delta);
     }
     disp[i] = out;
+}
+
+// Self-check of div_size against the IEEE division on pseudo-random operands.
+__global__ void stereo_div_check_kernel(double size, double inv, int64_t n, uint64_t seed,
+                                        unsigned long long* mismatches) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t z = seed + (uint64_t)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    // mantissa random, exponent in [2^-40, 2^24), sign random
+    const uint64_t e = 1023 - 40 + (z >> 58) % 64;
+    const double t = __longlong_as_double((long long)((z & 0x000FFFFFFFFFFFFFull) | (e << 52) | ((z >> 57) & 1) << 63));
+    if (div_size(t, size, inv) != ddiv(t, size)) atomicAdd(mismatches, 1ull);
 }
 
 // Left-right consistency (stereo.py:151-161) and the un-transpose to (H, W).
@@ -256,19 +447,23 @@ int stereo_match_impl(const void* left, const void* right, int height, int width
     sd.w = transpose ? height : width;
     sd.nd = max_disparity + 1;
     sd.nde = sd.nd < sd.w ? sd.nd : sd.w;
+    sd.nw = (sd.nde + 31) / 32;
     sd.r = radius;
     sd.size = (double)(2 * radius + 1);
+    sd.inv = 1.0 / sd.size;
     sd.floor_v = floor_v;
     sd.floor_sq = floor_sq;
     sd.lr_tol = lr_tol;
     const int64_t np = (int64_t)sd.h * sd.w;
     const int64_t nvol = np * sd.nd;
-    double *planes = nullptr, *v4 = nullptr, *muex = nullptr, *vab = nullptr, *scores = nullptr, *dl = nullptr,
-           *drm = nullptr;
+    // both passes (left/right and the mirrored right/left of the LR check) run in
+    // the same launches (blockIdx.y), so the sequential line walks have twice the
+    // independent lines in flight
+    double *planes = nullptr, *v4 = nullptr, *muex = nullptr, *vab = nullptr, *dd = nullptr;
+    ScorePart* parts = nullptr;
     int rc = RCGS_OK;
-    if ((rc = dalloc(&planes, 4 * np, s)) || (rc = dalloc(&v4, 4 * np, s)) || (rc = dalloc(&muex, 2 * np, s)) ||
-        (rc = dalloc(&vab, nvol, s)) || (rc = dalloc(&scores, nvol, s)) || (rc = dalloc(&dl, np, s)) ||
-        (rc = dalloc(&drm, np, s)))
+    if ((rc = dalloc(&planes, 4 * np, s)) || (rc = dalloc(&v4, 8 * np, s)) || (rc = dalloc(&muex, 4 * np, s)) ||
+        (rc = dalloc(&vab, 2 * nvol, s)) || (rc = dalloc(&parts, 2 * np * sd.nw, s)) || (rc = dalloc(&dd, 2 * np, s)))
         goto done;
     {
         const int T = 256;
@@ -278,16 +473,13 @@ int stereo_match_impl(const void* left, const void* right, int height, int width
         else
             stereo_gray_kernel<double><<<div_up(np, T), T, 0, s>>>((const double*)left, (const double*)right,
                                                                    ch_l, ch_r, transpose, sd, planes);
-        for (int pass = 0; pass < 2; ++pass) {  // pass 0: (left, right); pass 1: mirrored (right, left)
-            const double* A = planes + (2 * pass) * np;
-            const double* B = planes + (2 * pass + 1) * np;
-            stereo_vbox_planes_kernel<<<div_up(4 * sd.w, 128), 128, 0, s>>>(A, B, sd, v4);
-            stereo_hbox_left_kernel<<<div_up(2 * sd.h, 128), 128, 0, s>>>(v4, sd, muex);
-            stereo_vbox_products_kernel<<<div_up((int64_t)sd.w * sd.nde, T), T, 0, s>>>(A, B, sd, vab);
-            stereo_hscore_kernel<<<div_up((int64_t)sd.h * sd.nde, 128), 128, 0, s>>>(v4, muex, vab, sd, scores);
-            stereo_best_kernel<<<div_up(np, T), T, 0, s>>>(scores, sd, pass ? drm : dl);
-        }
-        stereo_lr_kernel<<<div_up(np, T), T, 0, s>>>(dl, drm, sd, transpose, disp);
+        stereo_vbox_planes_kernel<<<dim3(div_up(4 * sd.w, 64), 2), 64, 0, s>>>(planes, sd, v4);
+        stereo_hbox_left_kernel<<<dim3(div_up(2 * sd.h, 64), 2), 64, 0, s>>>(v4, sd, muex);
+        stereo_vbox_products_kernel<<<dim3(div_up((int64_t)sd.w * sd.nde, T), 2), T, 0, s>>>(planes, sd, vab);
+        stereo_hscore_kernel<<<dim3(div_up((int64_t)sd.h * sd.nw * 32, 32 * kHsWarps), 2), 32 * kHsWarps, 0, s>>>(
+            v4, muex, vab, sd, parts);
+        stereo_best_kernel<<<dim3(div_up(np, T), 2), T, 0, s>>>(parts, sd, dd);
+        stereo_lr_kernel<<<div_up(np, T), T, 0, s>>>(dd, dd + np, sd, transpose, disp);
         rc = cudaGetLastError() == cudaSuccess ? RCGS_OK : RCGS_ECUDA;
         if (rc) set_error("stereo kernels failed to launch");
     }
@@ -296,9 +488,8 @@ done:
     dfree(v4, s);
     dfree(muex, s);
     dfree(vab, s);
-    dfree(scores, s);
-    dfree(dl, s);
-    dfree(drm, s);
+    dfree(parts, s);
+    dfree(dd, s);
     return rc;
 }
 
@@ -318,6 +509,24 @@ extern "C" int rcgs_stereo_match(const void* d_left, const void* d_right, int32_
     return stereo_match_impl(d_left, d_right, height, width, channels_left, channels_right, elem_bytes, transpose != 0, max_disparity,
                              window_radius, variance_floor, variance_floor_sq, lr_tolerance, d_disparity,
                              as_stream(stream));
+}
+
+extern "C" int rcgs_stereo_div_check(int32_t size, int64_t n, uint64_t seed, int64_t* h_mismatches, void* stream) {
+    RCGS_CHECK_ARG(size >= 1 && n >= 0 && h_mismatches, "bad arguments");
+    cudaStream_t s = as_stream(stream);
+    unsigned long long* cnt = nullptr;
+    RCGS_TRY(dalloc(&cnt, 1, s));
+    RCGS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    if (n > 0) {
+        stereo_div_check_kernel<<<div_up(n, 256), 256, 0, s>>>((double)size, 1.0 / (double)size, n, seed, cnt);
+        RCGS_LAUNCH_CHECK();
+    }
+    unsigned long long h = 0;
+    RCGS_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    RCGS_CUDA(cudaStreamSynchronize(s));
+    dfree(cnt, s);
+    *h_mismatches = (int64_t)h;
+    return RCGS_OK;
 }
 
 extern "C" int rcgs_stereo_depth(const double* d_disp_h, const double* d_disp_v, int64_t n, double fx_baseline,

@@ -118,6 +118,14 @@ def test_match_disparity_properties():
     small = img[:24, :24]
     np.testing.assert_array_equal(P.match_disparity(small, small, P.StereoConfig(max_disparity=64)),
                                   P.match_disparity(small, small, P.StereoConfig(max_disparity=23)))
+    for wr in (0, 1, 11, 12):  # the streamed-ring line walk holds r <= 11; r = 12 takes the plain walk
+        right = np.roll(img, -2, axis=1)
+        np.testing.assert_array_equal(P.match_disparity(img, right, P.StereoConfig(max_disparity=8, window_radius=wr)),
+                                      OS.match(img, right, max_disp=8, r=wr), err_msg=f"window_radius={wr}")
+    for md in (0, 1, 31, 32, 33, 64):  # warp layouts: tail-only, padded, full + tail
+        right = np.roll(img, -3, axis=1)
+        np.testing.assert_array_equal(P.match_disparity(img, right, P.StereoConfig(max_disparity=md)),
+                                      OS.match(img, right, max_disp=md), err_msg=f"max_disparity={md}")
     for shift in (1, 4, 8):
         right = np.roll(img, -shift, axis=1)
         got = P.match_disparity(img, right, P.StereoConfig(max_disparity=16))
@@ -182,3 +190,18 @@ def test_render_stereo_pair_shifts_peak():
         lp = np.unravel_index(np.argmax(pair.left.sum(axis=2)), (64, 64))
         rp = np.unravel_index(np.argmax(pair.right.sum(axis=2)), (64, 64))
         assert lp[1 - axis] == rp[1 - axis] and lp[axis] - rp[axis] == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size", [3, 5, 7, 9, 11, 13, 21, 31])
+def test_fused_window_division_is_ieee(size):
+    """The matcher divides running sums by the window size with an fma-corrected
+    reciprocal product; it must equal IEEE division on every operand tried."""
+    import ctypes
+
+    from paper_2511_18441_b200 import _native as N
+    from paper_2511_18441_b200 import device as D
+
+    bad = ctypes.c_int64(-1)
+    N.call("rcgs_stereo_div_check", size, 1 << 25, 12345 + size, ctypes.byref(bad), D.stream_ptr())
+    assert bad.value == 0
