@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         const int64_t g0 = tile * kAG;
         const int ng = (int)(n - g0 < kAG ? n - g0 : kAG);
         mbar_wait(smem_addr(&bars[s]), (uint32_t)((it / kAStages) & 1));
+        float c12[12];  // this thread's 12 coefficients after the update (colour epilogue)
         if (upd && gi < ng) {
             const int64_t g = g0 + gi;
             const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
@@ -208,6 +209,48 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
                 P[q] = p4;
                 Mm[q] = m4;
                 V[q] = v4;
+                c12[4 * q] = p4.x;
+                c12[4 * q + 1] = p4.y;
+                c12[4 * q + 2] = p4.z;
+                c12[4 * q + 3] = p4.w;
+            }
+        } else if (gi < ng) {  // rejected step: the tile as loaded
+            const float* P = reinterpret_cast<const float*>(stage_buf(s, 0)) + gi * 48 + part * 12;
+#pragma unroll
+            for (int e = 0; e < 12; ++e) c12[e] = P[e];
+        }
+        if (next_color != nullptr) {
+            // fused colour pass of the next step's view (render.py:209-214) from the
+            // updated coefficients in registers: each of a gaussian's 4 threads
+            // evaluates its basis-row quarter (fp64, the order color_kernel uses,
+            // bit-identical) and lane part 0 combines and writes the colour
+            const int64_t g = g0 + gi;
+            const int32_t rs = gi < ng ? next_rank_of[g] : -1;
+            double qv[3] = {0.0, 0.0, 0.0};
+            if (rs >= 0) {
+                double x, y, z;
+                view_dir(pos, g, next_cen.c, x, y, z);
+                double b[16];
+                sh_basis16<double>(x, y, z, deg, b);
+                color_quarter(b, c12, part, qv);
+            }
+            double q1[3], q2[3], q3[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                q1[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 1);
+                q2[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 2);
+                q3[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 3);
+            }
+            if (rs >= 0 && part == 0) {  // colours are stored by scene index
+                float col[3];
+                int act = 0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const double val = color_combine(qv[ch], q1[ch], q2[ch], q3[ch]) + 0.5;
+                    act |= (val > 0.0) << ch;
+                    col[ch] = (float)fmax(0.0, val);
+                }
+                next_color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
             }
         }
         // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
@@ -218,34 +261,6 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
 #pragma unroll
             for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (next_color != nullptr) {
-            // fused colour pass of the next step's view (render.py:209-214) from the
-            // updated SH tile: thread `part` < 3 evaluates channel `part` with the same
-            // fp64 basis and summation order as color_kernel (bit-identical), lane
-            // part 0 gathers the channels and writes the depth-rank slot
-            const int64_t g = g0 + gi;
-            const int32_t rs = gi < ng ? next_rank_of[g] : -1;
-            double val = 0.0;
-            if (rs >= 0 && part < 3) {
-                double x, y, z;
-                view_dir(pos, g, next_cen.c, x, y, z);
-                double b[16];
-                sh_basis16<double>(x, y, z, deg, b);
-                const float* P = reinterpret_cast<const float*>(stage_buf(s, 0)) + gi * 48;
-                double raw = 0.0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) raw = fma(b[i], (double)P[3 * i + part], raw);
-                val = raw + 0.5;
-            }
-            const double v1 = __shfl_down_sync(0xffffffffu, val, 1);
-            const double v2 = __shfl_down_sync(0xffffffffu, val, 2);
-            if (rs >= 0 && part == 0) {  // colours are stored by scene index
-                const int act = (val > 0.0) | ((v1 > 0.0) << 1) | ((v2 > 0.0) << 2);
-                next_color[g] = make_float4((float)fmax(0.0, val), (float)fmax(0.0, v1), (float)fmax(0.0, v2),
-                                             __int_as_float(act));
-            }
-            __syncthreads();  // the tile is refilled below only after every reader is done
         }
         if (t == 0) {
             const int64_t next = tile + (int64_t)kAStages * gridDim.x;
@@ -353,7 +368,7 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem));
             RCGS_CUDA(cudaMalloc(&ticket, sizeof(unsigned)));
             RCGS_CUDA(cudaMemset(ticket, 0, sizeof(unsigned)));
-            grid = sms * (per_sm > 0 ? per_sm : 1);
+            grid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
         }
         const int64_t ntiles = (sc->n + kAG - 1) / kAG;
         Center nc = {{0.0, 0.0, 0.0}};

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -45,6 +46,18 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
     } while (0)
 
 inline unsigned div_up(int64_t a, int64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// CTAs per SM a persistent main-stream kernel (raster, record streaming, Adam)
+// launches: its occupancy limit minus RCGS_PERSIST_RESERVE (default 0), so that
+// the side-stream view build finds free CTA slots instead of queueing behind it.
+inline int persistent_ctas(int per_sm) {
+    static const int reserve = [] {
+        const char* e = getenv("RCGS_PERSIST_RESERVE");
+        return e ? atoi(e) : 0;
+    }();
+    const int c = per_sm - reserve;
+    return c > 0 ? c : 1;
+}
 
 // Keep freed blocks in the device's default pool across stream syncs (the
 // default release threshold of 0 returns memory to the driver at every sync,

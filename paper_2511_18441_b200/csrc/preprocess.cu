@@ -424,13 +424,12 @@ __global__ void color_kernel(const double* __restrict__ pos, const float4* __res
         c[4 * i + 2] = f.z;
         c[4 * i + 3] = f.w;
     }
-    double raw[3] = {0.0, 0.0, 0.0};
+    double qv[4][3];  // quarters in the order shared with the Adam colour epilogue
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {  // fused multiply-adds, as in the Adam colour epilogue
-        raw[0] = fma(b[i], (double)c[3 * i], raw[0]);
-        raw[1] = fma(b[i], (double)c[3 * i + 1], raw[1]);
-        raw[2] = fma(b[i], (double)c[3 * i + 2], raw[2]);
-    }
+    for (int part = 0; part < 4; ++part) color_quarter(b, c + 12 * part, part, qv[part]);
+    double raw[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) raw[ch] = color_combine(qv[0][ch], qv[1][ch], qv[2][ch], qv[3][ch]);
     int act = 0;
     float col[3];
 #pragma unroll

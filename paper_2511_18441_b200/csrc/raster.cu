@@ -50,6 +50,13 @@ constexpr int kCTA = 32 * kWarpsPerCTA;
 #define RCGS_RASTER_MIN_CTAS 4
 #endif
 constexpr int kMinCTAs = RCGS_RASTER_MIN_CTAS;  // resident CTAs per SM the register budget targets
+// raster_kernel CTA shape: warps are independent (persistent, barrier-free), so
+// the CTA size only sets how the per-warp staging buffer is addressed.
+#ifndef RCGS_RASTER_WARPS
+#define RCGS_RASTER_WARPS 8
+#endif
+constexpr int kRWarps = RCGS_RASTER_WARPS;
+constexpr int kRCTA = 32 * kRWarps;
 constexpr int kBlocksPerTile = 8;  // 2 x 4 blocks of 8x4 pixels
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kFixScale = 1125899906842624.0;  // 2^50
@@ -367,12 +374,13 @@ struct WarpStage {
 #define RCGS_FWDREC_MIN_CTAS 4
 #endif
 template <int M, bool kInstr>
-__global__ void __launch_bounds__(kCTA, M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMinCTAs) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMinCTAs) * 8 / kRWarps)
+    raster_kernel(RasterArgs a) {
     constexpr bool kFwd = (M == FWD || M == FWDREC || M == FWDRGBA);
     constexpr int kRow = (M == FWDREC || M == FWDRGBA) ? (int)FWD : M;  // counter row
-    __shared__ WarpStage stage_all[kWarpsPerCTA];
+    __shared__ WarpStage stage_all[kRWarps];
     const int lane = threadIdx.x & 31;
-    WarpStage& st = stage_all[threadIdx.x >> 5];
+    WarpStage& st = stage_all[kRWarps == 1 ? 0 : threadIdx.x >> 5];
     const uint32_t lt_mask = (1u << lane) - 1u;
 
     for (;;) {
@@ -714,7 +722,7 @@ static int launch_rec(RecArgs a, cudaStream_t s) {
         RCGS_CUDA(cudaGetDevice(&dev));
         RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<1>, kCTA, 0));
-        grid = sms * (per_sm > 0 ? per_sm : 1);
+        grid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
     }
     const int blocks = (int)min((int64_t)grid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
     if (blocks > 0) rec_kernel<kMode><<<blocks, kCTA, 0, s>>>(a);
@@ -829,17 +837,17 @@ static int launch(RasterArgs a, cudaStream_t s) {
         int dev = 0, sms = 0, per_sm = 0;
         RCGS_CUDA(cudaGetDevice(&dev));
         RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_kernel<M, false>, kCTA, 0));
-        grid[M] = sms * (per_sm > 0 ? per_sm : 1);
+        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_kernel<M, false>, kRCTA, 0));
+        grid[M] = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
     }
     a.counters = g_counters;
     a.trace = (g_trace && g_trace_items >= a.n_items) ? g_trace : nullptr;
-    const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
+    const int blocks = (int)min((int64_t)grid[M], ((int64_t)a.n_items + kRWarps - 1) / kRWarps);
     if (blocks > 0) {
         if (a.counters || a.trace)
-            raster_kernel<M, true><<<blocks, kCTA, 0, s>>>(a);
+            raster_kernel<M, true><<<blocks, kRCTA, 0, s>>>(a);
         else
-            raster_kernel<M, false><<<blocks, kCTA, 0, s>>>(a);
+            raster_kernel<M, false><<<blocks, kRCTA, 0, s>>>(a);
     }
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;

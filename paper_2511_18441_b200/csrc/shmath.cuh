@@ -78,4 +78,26 @@ __device__ __forceinline__ void view_dir(const double* __restrict__ pos, int64_t
     z = z / nrm;
 }
 
+// Colour of one channel-triplet quarter: basis rows 4 part .. 4 part + 3 against
+// this quarter's 12 coefficients (coefficient 12 part + e is row 4 part + e / 3,
+// channel e % 3), an fp64 fma chain per channel from 0.  The full colour is
+// ((q0 + q1) + q2) + q3 over the quarters -- the order color_kernel and the Adam
+// colour epilogue share, so both produce identical bits.
+__device__ __forceinline__ void color_quarter(const double b[16], const float c12[12], int part, double out[3]) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double bq = part == 0 ? b[q] : (part == 1 ? b[4 + q] : (part == 2 ? b[8 + q] : b[12 + q]));
+            acc = fma(bq, (double)c12[3 * q + ch], acc);
+        }
+        out[ch] = acc;
+    }
+}
+
+__device__ __forceinline__ double color_combine(double q0, double q1, double q2, double q3) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(q0, q1), q2), q3);
+}
+
 }  // namespace rcgs

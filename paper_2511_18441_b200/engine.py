@@ -22,6 +22,7 @@ floating-point all-reduce.
 from __future__ import annotations
 
 import collections
+import os
 import ctypes
 import threading
 import time
@@ -36,7 +37,7 @@ from .render import DEFAULT_CONFIG
 
 
 class ViewPrefetcher:
-    """Builds the views of upcoming steps on a side stream from a worker thread.
+    """Builds the views of upcoming steps on side streams from worker threads.
 
     A view build (K1 + depth sort + K2) synchronises its stream twice to size
     its buffers; running it one or two steps ahead on its own stream and host
@@ -44,15 +45,21 @@ class ViewPrefetcher:
     with the current step's raster / loss / backward / Adam.  Every step still
     builds its own view from scratch; only the timing moves.
 
-    Used views come back through `retire`: the worker frees them on ITS stream
-    after an event recorded on the consumer's stream.  Allocation and release of
-    view memory then happen on one stream, so the stream-ordered pool reuses
-    blocks without cross-stream dependencies and never grows in steady state.
-    Growing it (a driver-locked physical allocation) stalled both host threads
-    for 30-800 ms when views were freed on the consumer stream instead.
+    `workers` threads (RCGS_PREFETCH_WORKERS, default 2) take jobs in turn, each
+    on its own stream: a build's wall time (its two host syncs, and kernels that
+    only run between the main stream's CTAs) is about one step, so one worker
+    cannot stay ahead; two interleave.  The streams get the highest priority, so
+    the block scheduler starts build CTAs as soon as main-stream CTAs retire.
+
+    Used views come back through `retire`: the worker that built a view frees it
+    on ITS stream after an event recorded on the consumer's stream.  Allocation
+    and release of view memory then happen on one stream, so the stream-ordered
+    pool reuses blocks without cross-stream dependencies and never grows in
+    steady state.  Growing it (a driver-locked physical allocation) stalled both
+    host threads for 30-800 ms when views were freed on the consumer stream instead.
     """
 
-    def __init__(self, dscene, cameras, raster, device, profile=False, targets=None, depth=2):
+    def __init__(self, dscene, cameras, raster, device, profile=False, targets=None, depth=2, workers=None):
         self.dscene, self.cameras, self.raster, self.device = dscene, cameras, raster, device
         self.profile = profile
         # host-resident targets (streamed datasets): each upcoming step's target is
@@ -63,18 +70,26 @@ class ViewPrefetcher:
         self.ring = [None] * (depth + 4)
         self.ring_free = [None] * (depth + 4)
         self.copy_stream = torch.cuda.Stream(device=device) if self.targets is not None else None
-        self.events = []  # (start, end) of each view build on the side stream
+        self.events = []  # (start, end) of each view build on its side stream
         self.host_build_ms = []
         self.host_wait_ms = []
-        self.stream = torch.cuda.Stream(device=device)
+        if workers is None:
+            workers = int(os.environ.get("RCGS_PREFETCH_WORKERS", "2"))
+        workers = max(1, int(workers))
+        prio = os.environ.get("RCGS_PREFETCH_PRIORITY")
+        prio = int(prio) if prio is not None else torch.cuda.Stream.priority_range()[1]
+        self.streams = [torch.cuda.Stream(device=device, priority=prio) for _ in range(workers)]
         self.jobs = collections.deque()
-        self.retired = collections.deque()
+        self.retired = [collections.deque() for _ in range(workers)]
+        self.builder = {}  # id(view) -> index of the worker that built it
         self.ready = {}
         self.cv = threading.Condition()
         self.stop = False
         self.error = None
-        self.thread = threading.Thread(target=self._run, name="view-prefetch", daemon=True)
-        self.thread.start()
+        self.threads = [threading.Thread(target=self._run, args=(w,), name=f"view-prefetch-{w}", daemon=True)
+                        for w in range(workers)]
+        for t in self.threads:
+            t.start()
 
     def submit(self, key, index):
         with self.cv:
@@ -82,23 +97,24 @@ class ViewPrefetcher:
             self.cv.notify_all()
 
     def retire(self, view, key=None):
-        """Hand a used view back; it is freed on the side stream once the current
-        stream's work queued so far (which reads the view) has completed.  `key`
-        releases the step's target-ring slot at the same event."""
+        """Hand a used view back; it is freed on its builder's stream once the
+        current stream's work queued so far (which reads the view) has completed.
+        `key` releases the step's target-ring slot at the same event."""
         ev = torch.cuda.Event()
         ev.record()
         with self.cv:
-            self.retired.append((view, ev))
+            w = self.builder.pop(id(view), 0)
+            self.retired[w].append((view, ev))
             if key is not None and self.targets is not None:
                 self.ring_free[key % len(self.ring)] = ev
             self.cv.notify_all()
 
-    def _free_retired(self):
+    def _free_retired(self, w):
         with self.cv:
-            items = list(self.retired)
-            self.retired.clear()
+            items = list(self.retired[w])
+            self.retired[w].clear()
         for view, ev in items:
-            self.stream.wait_event(ev)
+            self.streams[w].wait_event(ev)
             view.close()
 
     def take(self, key):
@@ -112,18 +128,19 @@ class ViewPrefetcher:
                 raise self.error
             return self.ready.pop(key)
 
-    def _run(self):
+    def _run(self, w):
         torch.cuda.set_device(self.device)
-        with torch.cuda.stream(self.stream):
+        stream = self.streams[w]
+        with torch.cuda.stream(stream):
             while True:
                 with self.cv:
-                    while not self.jobs and not self.retired and not self.stop:
+                    while not self.jobs and not self.retired[w] and not self.stop:
                         self.cv.wait(timeout=1.0)
                     if self.stop:
                         return
                     job = self.jobs.popleft() if self.jobs else None
                 if job is None:
-                    self._free_retired()
+                    self._free_retired(w)
                     continue
                 key, index = job
                 try:
@@ -147,20 +164,21 @@ class ViewPrefetcher:
                     t0 = time.perf_counter()
                     if self.profile:
                         e0 = torch.cuda.Event(enable_timing=True)
-                        e0.record(self.stream)
+                        e0.record(stream)
                     view = D.View(self.dscene, intr, pose, self.raster)
                     if self.profile:
                         self.host_build_ms.append((time.perf_counter() - t0) * 1000.0)
                     if copied is not None:
-                        self.stream.wait_event(copied)  # one ready event covers view + target
+                        stream.wait_event(copied)  # one ready event covers view + target
                     ev = torch.cuda.Event(enable_timing=self.profile)
-                    ev.record(self.stream)
+                    ev.record(stream)
                     if self.profile:
                         self.events.append((e0, ev))
                     with self.cv:
+                        self.builder[id(view)] = w
                         self.ready[key] = (view, ev, tgt)
                         self.cv.notify_all()
-                    self._free_retired()
+                    self._free_retired(w)
                 except Exception as e:  # surfaced to the consumer
                     with self.cv:
                         self.error = e
@@ -171,10 +189,14 @@ class ViewPrefetcher:
         with self.cv:
             self.stop = True
             self.cv.notify_all()
-        self.thread.join(timeout=30)
-        with torch.cuda.stream(self.stream):
-            self._free_retired()
-            for view, _, _ in self.ready.values():
+        for t in self.threads:
+            t.join(timeout=30)
+        for w, stream in enumerate(self.streams):
+            with torch.cuda.stream(stream):
+                self._free_retired(w)
+        for view, _, _ in self.ready.values():
+            w = self.builder.pop(id(view), 0)
+            with torch.cuda.stream(self.streams[w]):
                 view.close()
         self.ready.clear()
 
@@ -226,7 +248,7 @@ class RefitEngine:
         self._prof = []
         self._build_ev = []  # inline view builds (no prefetcher)
         # with prefetching, Adam also colours the next step's view (rcgs_adam_fused_next)
-        self.fuse_color = fuse_color
+        self.fuse_color = fuse_color and os.environ.get("RCGS_FUSE_COLOR", "1") != "0"
         self._held = None
 
     def close(self):
