@@ -30,7 +30,10 @@ constexpr int kLT = 32;            // output tile edge
 constexpr int kLH = kLT + 2 * kR;  // 42
 constexpr int kRows = 4;           // output rows per thread in the vertical pass
 constexpr int kLNT = 256;          // = kLT * kLT / kRows
-constexpr int kHS = 4;             // adjacent outputs per thread in the horizontal passes
+#ifndef RCGS_LOSS_HS
+#define RCGS_LOSS_HS 4
+#endif
+constexpr int kHS = RCGS_LOSS_HS;  // adjacent outputs per thread in the horizontal passes
 #ifndef RCGS_LOSS_CTAS
 #define RCGS_LOSS_CTAS 3
 #endif

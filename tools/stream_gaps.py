@@ -56,6 +56,20 @@ def main():
     for e in ks:
         by[e["args"].get("stream", e.get("tid"))].append((e["ts"], e["ts"] + e["dur"], e["name"]))
     wall = t1 - t0
+    # launch slack: kernel start - end of its cudaLaunchKernel (via correlation id);
+    # near zero means the GPU was waiting for the host to enqueue it
+    api = {e["args"].get("correlation"): e for e in ev
+           if e.get("cat") == "cuda_runtime" and "dur" in e and "args" in e}
+    slack = collections.defaultdict(list)
+    for e in ks:
+        c = e["args"].get("correlation")
+        if c in api:
+            slack[e["args"].get("stream")].append(e["ts"] - (api[c]["ts"] + api[c]["dur"]))
+    for sid, v in slack.items():
+        v.sort()
+        n = len(v)
+        print(f"stream {sid}: launch slack p10 {v[n // 10]:.0f} p50 {v[n // 2]:.0f} us; "
+              f"{sum(1 for x in v if x < 15)} of {n} ops started < 15 us after their launch call")
     print(f"wall {wall:.0f} us over {a.steps} steps = {wall / a.steps:.1f} us/step")
     for sid, iv in sorted(by.items(), key=lambda kv: -sum(b - a_ for a_, b, _ in kv[1])):
         iv.sort()
