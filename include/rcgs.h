@@ -192,11 +192,13 @@ int rcgs_sh_grad(const rcgs_scene* scene, const float* d_acc, const double* h_ce
  * (1/G) sum_v basis(dir_{v,i}) (x) acc_v[i] for G views (G == 1 is the reference
  * iteration); d_accs points to G device pointers (host array).  If *d_reject != 0 the
  * update is skipped (non-finite gradient, optimize.py:72-74); otherwise the device
- * step counter *d_step is advanced. */
+ * step counter *d_step is advanced.  With d_reject_record non-null the flag is
+ * consumed for a pipelined caller: 1.0 / 0.0 (rejected or not) is written there
+ * and *d_reject is reset to 0 for the next step, on the device. */
 int rcgs_adam_fused(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
                     const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                    const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                    void* stream);
+                    const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                    double* d_reject_record, void* stream);
 /* rcgs_adam_fused + the colour pass of `next_view` (the view the next optimizer
  * step renders, render.py:209-214) evaluated from the updated SH tiles while they
  * are in shared memory: saves the colour kernel's full SH read.  Equivalent to
@@ -204,8 +206,8 @@ int rcgs_adam_fused(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v
  * including on a rejected step (SH unchanged, view still coloured). */
 int rcgs_adam_fused_next(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
                          const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                         const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                         rcgs_view* next_view, void* stream);
+                         const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                         double* d_reject_record, rcgs_view* next_view, void* stream);
 /* Dense Adam on an explicit gradient (N,16,3) (adam_step API). */
 int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
                     const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,

@@ -69,9 +69,9 @@ _SIGNATURES = {
     "rcgs_backward": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_sh_grad": [c_void_p, c_void_p, P(c_double), c_void_p, c_void_p],
     "rcgs_adam_fused": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
-                        P(AdamConfig), c_void_p, c_void_p, c_void_p],
+                        P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_adam_fused_next": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
-                             P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p],
+                             P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_adam_dense": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, P(AdamConfig), c_void_p,
                         c_void_p, c_void_p],
     "rcgs_nonfinite_check": [c_void_p, c_i64, c_void_p, c_void_p],

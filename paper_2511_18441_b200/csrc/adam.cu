@@ -124,8 +124,8 @@ constexpr size_t kASmem = (size_t)kAStages * 3 * kATileBytes + kAStages * sizeof
 __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
     float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
-    unsigned* __restrict__ ticket, const int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
-    Center next_cen, float4* __restrict__ next_color) {
+    unsigned* __restrict__ ticket, int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
+    Center next_cen, float4* __restrict__ next_color, double* __restrict__ reject_record) {
     // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
     // colour epilogue the next view is still coloured from the unchanged SH
     const bool upd = !(reject && *reject);
@@ -278,6 +278,10 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
             if (upd) *step += 1;
             *ticket = 0;
+            if (reject_record) {  // consume the flag: record it, re-arm it for the next step
+                *reject_record = upd ? 0.0 : 1.0;
+                if (reject) *reject = 0;
+            }
         }
     }
 }
@@ -298,8 +302,14 @@ __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m
     v[q] = vv;
 }
 
-__global__ void step_commit_kernel(const int32_t* __restrict__ reject, int64_t* __restrict__ step) {
-    if (!(reject && *reject)) *step += 1;
+__global__ void step_commit_kernel(int32_t* __restrict__ reject, int64_t* __restrict__ step,
+                                   double* __restrict__ reject_record) {
+    const bool rej = reject && *reject;
+    if (!rej) *step += 1;
+    if (reject_record) {
+        *reject_record = rej ? 1.0 : 0.0;
+        if (reject) *reject = 0;
+    }
 }
 
 __global__ void sh_grad_kernel(const double* __restrict__ pos, int64_t n, int deg,
@@ -344,8 +354,8 @@ using namespace rcgs;
 
 static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
                            const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                           const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                           rcgs_view* next_view, void* stream) {
+                           const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                           double* d_reject_record, rcgs_view* next_view, void* stream) {
     RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
     RCGS_CHECK_ARG(n_views >= 1 && n_views <= kMaxViews, "views per step must be in [1, %d]", kMaxViews);
     RCGS_CHECK_ARG(sc->n < (int64_t)357913941, "scene too large for 32-bit Adam indexing");
@@ -382,31 +392,31 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
         // bias corrections from and commit of the device step counter happen inside
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
             sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
-            d_reject, nrank, nc, ncolor);
+            d_reject, nrank, nc, ncolor, d_reject_record);
         RCGS_LAUNCH_CHECK();
         return RCGS_OK;
     }
-    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
+    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step, d_reject_record);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }
 
 extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
                                const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                               const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                               void* stream) {
-    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step, nullptr,
-                           stream);
+                               const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                               double* d_reject_record, void* stream) {
+    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
+                           d_reject_record, nullptr, stream);
 }
 
 extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
                                     const float* const* h_d_accs, const double* h_centers, int32_t n_views,
-                                    const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,
-                                    rcgs_view* next_view, void* stream) {
+                                    const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                                    double* d_reject_record, rcgs_view* next_view, void* stream) {
     RCGS_CHECK_ARG(next_view != nullptr, "null next view");
     RCGS_CHECK_ARG(next_view->scene == sc, "next view belongs to another scene");
-    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step, next_view,
-                           stream);
+    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
+                           d_reject_record, next_view, stream);
 }
 
 extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
@@ -425,7 +435,7 @@ extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const fl
         RCGS_LAUNCH_CHECK();
         dfree(bc, s);
     }
-    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step);
+    step_commit_kernel<<<1, 1, 0, s>>>(const_cast<int32_t*>(d_reject), d_step, nullptr);  // flag only read
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }

@@ -349,7 +349,7 @@ class RefitEngine:
         if ev:
             ev[2].record()
         D.loss_grad(img, target, self.config.lam, loss3=rec[:3], grad=grad)
-        self.reject.zero_()
+        # self.reject is 0 here: the previous step's Adam consumed and re-armed it
         if ev:
             ev[3].record()
         view.backward(grad, acc=self.acc, nonfinite=self.reject)
@@ -361,7 +361,7 @@ class RefitEngine:
         cen = np.concatenate([self._centers[p] for p in picks[:len(accs)]])
         args = (self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
                 (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
-                N.ptr(self.reject), N.ptr(self.step_dev))
+                N.ptr(self.reject), N.ptr(self.step_dev), N.ptr(rec[3:4]))
         if prefetched and self.fuse_color:
             # take the next step's view now (its build was submitted `prefetch`
             # steps ago; the stream waits for it before the Adam stage event) and
@@ -369,7 +369,7 @@ class RefitEngine:
             nxt_picks, nxt, nxt_key, nxt_tgt = self._take_prefetched()
             if ev:
                 ev[5].record()
-            N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())
+            N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())  # also records + re-arms reject
             nxt._colored = True
             self._held = (nxt_picks, nxt, True, nxt_key, nxt_tgt)
         else:
@@ -379,7 +379,6 @@ class RefitEngine:
         if ev:
             ev[6].record()
             self._prof.append((ev, coloured))
-        rec[3].copy_(self.reject[0], non_blocking=True)
         self.pending.append((picks, generation))
         if prefetched:
             self._pf.retire(view, key)
