@@ -7,7 +7,7 @@
 //   dSSIM/dy = [F(M1) + 2 y F(M2) + g F(M3)] / n,
 //   M1 = (d_mu1 - 2 d_var1 mu1 - d_cov mu2) / mass, M2 = d_var1 / mass,
 //   M3 = d_cov / mass.
-// Dirty: per 32x32 block, do image and target differ anywhere?  (+ global flag)
+// Dirty: per 32x32 block, do image and target differ anywhere?
 // Pass A: moments of y, g, y^2, g^2, y g (separable filter in shared memory)
 //         -> SSIM map, |y - g|, M1..M3 (fp64) and per-block partial sums, for
 //         blocks within two blocks of a difference (elsewhere SSIM == 1, L1 == 0).
@@ -100,8 +100,7 @@ __device__ __forceinline__ void vfilter(const double* __restrict__ h, int r0, in
 // exactly-1 SSIM map, zero L1 and a mathematically zero gradient.
 template <typename T>
 __global__ void __launch_bounds__(kLNT) loss_dirty_kernel(const T* __restrict__ y, const T* __restrict__ g,
-                                                          int H, int W, uint8_t* __restrict__ dirty,
-                                                          int32_t* __restrict__ differ) {
+                                                          int H, int W, uint8_t* __restrict__ dirty) {
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     int d = 0;
     // chunk by chunk with a block vote: a block that differs (every block, once the
@@ -119,10 +118,7 @@ __global__ void __launch_bounds__(kLNT) loss_dirty_kernel(const T* __restrict__ 
         }
         d = __syncthreads_or(di);
     }
-    if (threadIdx.x == 0) {
-        dirty[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)d;
-        if (d) atomicOr(differ, 1);
-    }
+    if (threadIdx.x == 0) dirty[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)d;
 }
 
 __device__ __forceinline__ bool near_dirty(const uint8_t* __restrict__ dirty, int r) {
@@ -309,7 +305,6 @@ template <bool SSIM, typename T, typename G, typename MT>
 __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
                                                     int W, Window win, double lam,
                                                     const MT* __restrict__ maps,
-                                                    const int32_t* __restrict__ differ,
                                                     const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* hs = reinterpret_cast<double*>(smem_raw);   // [3][42][32]
@@ -320,7 +315,8 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
     const double n = (double)(npix * 3);
     // exact zeros where the gradient is mathematically zero: everywhere when the
     // images are identical (losses.py:127-130), else outside one block of a difference
-    const bool any = *differ != 0 && near_dirty(dirty, SSIM ? 1 : 0);
+    // (identical images: no block is dirty, so this is false everywhere)
+    const bool any = near_dirty(dirty, SSIM ? 1 : 0);
     const int c = t % kLT, r0 = (t / kLT) * kRows;
     // the next channel's three map planes (with the 5-px halo, zero outside the
     // image) stream into the other buffer while this channel computes
@@ -455,13 +451,10 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     const int64_t npix = (int64_t)height * width;
     MT* maps = nullptr;
     double* part = nullptr;
-    int32_t* differ = nullptr;
     uint8_t* dirty = nullptr;
     RCGS_TRY(dalloc(&part, 2 * nb, s));
-    RCGS_TRY(dalloc(&differ, 1, s));
     RCGS_TRY(dalloc(&dirty, nb, s));
-    RCGS_CUDA(cudaMemsetAsync(differ, 0, sizeof(int32_t), s));
-    loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty, differ);
+    loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty);
     const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
     const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
     if (ssim_ok) {
@@ -474,23 +467,22 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
             loss_pass_b<true, T, G, MT><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                                   differ, dirty, d_grad);
+                                                                   dirty, d_grad);
         } else {
             loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
-                                                               differ, dirty, d_grad);
+                                                               dirty, d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
         loss_pass_a<false, T, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, dirty);
         loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr,
-                                                           differ, dirty, d_grad);
+                                                           dirty, d_grad);
         RCGS_LAUNCH_CHECK();
     }
     loss_pass_c<<<1, kLNT, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
     RCGS_LAUNCH_CHECK();
     dfree(maps, s);
     dfree(part, s);
-    dfree(differ, s);
     dfree(dirty, s);
     return RCGS_OK;
 }
