@@ -308,10 +308,12 @@ def run_gpu(args):
             rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                                "frac": round(ach / hbm, 4), "ms_per_launch": round(kk["ms"], 4),
                                "note": kk.get("note", "")}
-    # dominant kernel: longest main-stream stage.  With prefetching the view build
-    # runs concurrently on a side stream and its "ms" is a contended interval, not
-    # a kernel duration, so it is reported but not ranked.
-    ranked = [k for k in rooflines if not (k == "view_build" and args.prefetch > 0)]
+    # dominant kernel: the longest single-kernel main-stream stage (recording raster,
+    # Adam).  Multi-kernel stages (loss: dirty scan + 3 passes; backward: record
+    # stream + finish; view build on its side streams) are event intervals that
+    # also contain the concurrent view build's kernels, not one kernel's duration:
+    # reported in `rooflines`, not ranked.
+    ranked = [k for k in rooflines if k in ("raster_fwd", "adam")]
     dom = max(ranked, key=lambda k: rooflines[k]["ms_per_launch"]) if ranked else None
     traffic = measured_traffic().get(dom) if dom else None
     roof = None if dom is None else dict(rooflines[dom], kernel=dom, traffic=traffic,
@@ -320,6 +322,21 @@ def run_gpu(args):
     if roof is not None and roof["bound"] == "fp32":
         roof["note"] = ("FP32 FLOP roofline (algorithmic FLOPs / measured FFMA peak); the rasteriser is "
                         "warp-issue bound (see profiles/, ~80% issue-active), so the FLOP fraction is low")
+        # raster unit = evaluated (pixel, entry) pair at ~16 FP32-pipe
+        # instructions; roof = FP32-pipe issue rate (128 lanes/SM/clk) at the live clock
+        work = stages["kernels"][dom].get("work") or {}
+        if work.get("evals"):
+            sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            peak_gi = sms * 128 * sm_mhz * 1e6 / 1e9
+            ach_gi = work["evals"] * 16 / (roof["ms_per_launch"] / 1000.0) / 1e9
+            roof["issue_model"] = {"instr_per_eval": 16, "achieved_ginstr_s": round(ach_gi, 1),
+                                   "peak_ginstr_s": round(peak_gi, 1), "frac": round(ach_gi / peak_gi, 4)}
+        ncu = measured_stage_ncu().get(dom, {})
+        if "sm_throughput_pct" in ncu:
+            roof["ncu"] = {"kernel": ncu.get("top_kernel"), "sm_throughput_frac": round(ncu["sm_throughput_pct"] / 100, 4),
+                           "issue_active_frac": round(ncu["issue_active_pct"] / 100, 4),
+                           "source": "profiles/traffic.json (ncu --set full of one step)"}
     cpu = cpu_baseline_sample(args, cfg) if args.cpu_baseline else None
     value = world / (step_ms / 1000.0)
     line = {
@@ -374,15 +391,20 @@ def ctypes_fp32_peak():
     return out.value
 
 
-def measured_traffic():
-    """DRAM bytes (read + write) per launch of each stage's kernel from the committed
-    ncu --set full capture summary (profiles/traffic.json), or {}."""
+def measured_stage_ncu():
+    """Per-stage figures of the committed ncu --set full capture summary
+    (profiles/traffic.json): DRAM bytes (read + write) per launch, and the
+    SM-throughput / issue-active percentages of the stage's longest kernel, or {}."""
     p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["stages"].items()}
+            return json.load(f)["stages"]
     except (OSError, ValueError, KeyError):
         return {}
+
+
+def measured_traffic():
+    return {k: v["dram_bytes_per_launch"] for k, v in measured_stage_ncu().items() if "dram_bytes_per_launch" in v}
 
 
 def stage_model(eng, cams, npix, cfg, live, cnt):

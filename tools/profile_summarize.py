@@ -35,12 +35,13 @@ def stage_of(name):
 
 
 def traffic_from_table(md_path, out_path, tag):
-    """traffic.json from the step summary table (DRAM read / write columns)."""
+    """traffic.json from the step summary table: DRAM read + write per stage, and
+    the SM-throughput / issue-active percentages of each stage's longest kernel."""
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    agg = {}
+    agg, top = {}, {}
     for line in open(md_path):
         cells = [c.strip() for c in line.strip().strip("|").split("|")]
-        if len(cells) < 4 or cells[0] in ("kernel", "---") or cells[0].startswith("---"):
+        if len(cells) < 7 or cells[0] in ("kernel", "---") or cells[0].startswith("---"):
             continue
         b = 0.0
         for cell in cells[2:4]:
@@ -48,8 +49,17 @@ def traffic_from_table(md_path, out_path, tag):
             b += float(v) * scale.get(u, 1)
         st = stage_of(cells[0])
         agg[st] = agg.get(st, 0.0) + b
+        us = float(cells[1].split()[0])
+        if us > top.get(st, (0.0,))[0]:
+            top[st] = (us, cells[0], float(cells[5].split()[0]), float(cells[6].split()[0]))
+    stages = {}
+    for k, v in agg.items():
+        stages[k] = {"dram_bytes_per_launch": int(v)}
+        if k in top:
+            stages[k].update({"top_kernel": top[k][1], "sm_throughput_pct": top[k][2],
+                              "issue_active_pct": top[k][3]})
     out = {"source": f"ncu --set full (default cache control), one optimizer step of C3: profiles/{tag}_ncu_step.md",
-           "stages": {k: {"dram_bytes_per_launch": int(v)} for k, v in agg.items()}}
+           "stages": stages}
     with open(out_path, "w") as f:
         json.dump(out, f, indent=1)
     return out
@@ -59,25 +69,7 @@ def main(tag, outdir="profiles"):
     os.makedirs(outdir, exist_ok=True)
     launch_summary.main("gpurun_out/launches.csv", f"{outdir}/{tag}_launches.txt")
     ncu_summary.main("gpurun_out/step_full.ncu-rep", f"{outdir}/{tag}_ncu_step.md")
-    raw = subprocess.run(["ncu", "-i", "gpurun_out/step_full.ncu-rep", "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    agg = {}
-    for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")].split("(")[0]
-        st = stage_of(name)
-        b = 0.0
-        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            i = hdr.index(key)
-            b += float(r[i].replace(",", "")) * scale.get(units[i], 1)
-        agg.setdefault(st, 0.0)
-        agg[st] += b
-    out = {"source": f"ncu --set full (default cache control), one optimizer step of C3: profiles/{tag}_ncu_step.md",
-           "stages": {k: {"dram_bytes_per_launch": int(v)} for k, v in agg.items()}}
-    with open(f"{outdir}/traffic.json", "w") as f:
-        json.dump(out, f, indent=1)
+    out = traffic_from_table(f"{outdir}/{tag}_ncu_step.md", f"{outdir}/traffic.json", tag)
     print(json.dumps(out, indent=1))
 
 
