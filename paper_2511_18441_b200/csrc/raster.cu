@@ -622,6 +622,117 @@ struct RecArgs {
     int32_t* nonfinite;
 };
 
+// Backward over the recorded weights, latency-hidden.  Each warp walks a static
+// stride of the heavy-first block order (no work-counter round trip), and the next
+// block's metadata (tile, record range, pixel gradients) is loaded while the
+// current block's records stream; record batches are double-buffered.  The per-
+// block setup chain (order -> range -> gradients, each a dependent global load)
+// was comparable to the ~2-3 record batches a block holds.
+struct RecMeta {
+    uint32_t base, n;
+    float g0, g1, g2;
+};
+
+__device__ __forceinline__ RecMeta rec_meta(const RecArgs& a, unsigned item, int tile, int lane) {
+    RecMeta m;
+    const int blk = (int)(item % kBlocksPerTile);
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int u = tx * kTile + (blk & 1) * 8 + (lane & 7), v = ty * kTile + (blk >> 1) * 4 + (lane >> 3);
+    const bool inside = u < a.W && v < a.H;
+    const int64_t pix = (int64_t)v * a.W + u;
+    m.g0 = inside ? a.grad[3 * pix] : 0.f;
+    m.g1 = inside ? a.grad[3 * pix + 1] : 0.f;
+    m.g2 = inside ? a.grad[3 * pix + 2] : 0.f;
+    const uint2 range = a.ranges[tile];
+    m.base = a.wrec_off ? a.wrec_off[tile * kBlocksPerTile + blk]
+                        : kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x);
+    m.n = a.wrec_n[tile * kBlocksPerTile + blk];
+    return m;
+}
+
+#ifndef RCGS_REC_BWD_CTAS
+#define RCGS_REC_BWD_CTAS 4
+#endif
+__global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArgs a) {
+    const int lane = threadIdx.x & 31;
+    constexpr int kU = 8;  // records per batch (the 32-value reduce-scatter width)
+    const unsigned nw = gridDim.x * (blockDim.x >> 5);
+    const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    auto tile_of = [&](unsigned item) -> int {
+        return a.tile_order ? (int)a.tile_order[item / kBlocksPerTile] : (int)(item / kBlocksPerTile);
+    };
+    unsigned item = gw;
+    if (item >= (unsigned)a.n_items) return;
+    RecMeta m = rec_meta(a, item, tile_of(item), lane);
+    int ntile = item + nw < (unsigned)a.n_items ? tile_of(item + nw) : 0;
+    while (true) {
+        const unsigned nitem = item + nw;
+        const bool has_next = nitem < (unsigned)a.n_items;
+        // next block's metadata in flight while this block streams its records
+        RecMeta nm = {0u, 0u, 0.f, 0.f, 0.f};
+        if (has_next) nm = rec_meta(a, nitem, ntile, lane);
+        const int nntile = nitem + nw < (unsigned)a.n_items ? tile_of(nitem + nw) : 0;
+        // the gradient is local to the edited region: blocks whose gradients are all
+        // 0 have no term
+        if (m.n > 0 && !__all_sync(0xffffffffu, m.g0 == 0.f && m.g1 == 0.f && m.g2 == 0.f)) {
+            float w[kU], wn[kU];
+            uint32_t sl = 0u, sln = 0u;  // lane q < kU holds record q's scene index
+            auto load = [&](uint32_t r0, float* wd, uint32_t& sd) {
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const bool ok = r0 + q < m.n;
+                    wd[q] = ok ? __ldcs(a.wrec_w + (size_t)(m.base + r0 + q) * 32 + lane) : 0.f;
+                }
+                sd = (lane < kU && r0 + lane < m.n) ? a.wrec_s[m.base + r0 + lane] : 0u;
+            };
+            load(0, w, sl);
+            for (uint32_t r0 = 0; r0 < m.n; r0 += kU) {
+                if (r0 + kU < m.n) load(r0 + kU, wn, sln);
+                // the kU records' (w g) sums for 3 channels (+1 zero pad) = 32 values,
+                // halved across the warp: xor 16, 8, 4, 2, 1 -- the butterfly tree of a
+                // plain warp sum (bit-identical totals); lane L ends with record L >> 2,
+                // channel L & 3
+                float x[32];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const bool comp = w[q] != 0.f;
+                    x[4 * q] = comp ? w[q] * m.g0 : 0.f;
+                    x[4 * q + 1] = comp ? w[q] * m.g1 : 0.f;
+                    x[4 * q + 2] = comp ? w[q] * m.g2 : 0.f;
+                    x[4 * q + 3] = 0.f;
+                }
+#pragma unroll
+                for (int h = 16; h >= 1; h >>= 1) {
+                    const bool hi = lane & h;
+#pragma unroll
+                    for (int p = 0; p < h; ++p) {
+                        const float send = hi ? x[p] : x[p + h];
+                        const float keep = hi ? x[p + h] : x[p];
+                        x[p] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+                    }
+                }
+                const float val = x[0];
+                const int q = lane >> 2, c = lane & 3;
+                const uint32_t sq = __shfl_sync(0xffffffffu, sl, q);
+                if (c < 3 && val != 0.f && r0 + q < m.n) {
+                    if (isfinite(val)) {
+                        atomicAdd(&a.acc_fx[3 * (int64_t)sq + c], (unsigned long long)to_fixed(val));
+                    } else if (a.nonfinite) {
+                        atomicOr(a.nonfinite, 1);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) w[u] = wn[u];
+                sl = sln;
+            }
+        }
+        if (!has_next) break;
+        item = nitem;
+        m = nm;
+        ntile = nntile;
+    }
+}
+
 // kMode: 0 SpMV render into an image, 1 backward, 2 SpMV render into an RGBA8 frame
 template <int kMode>
 __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
@@ -723,6 +834,22 @@ static int launch_rec(RecArgs a, cudaStream_t s) {
         RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_kernel<1>, kCTA, 0));
         grid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
+    }
+    static const bool dynamic = getenv("RCGS_REC_BWD_DYNAMIC") != nullptr;
+    if (kMode == 1 && !dynamic) {
+        // static work striding: every launched CTA must be resident at once
+        static int bgrid = 0;
+        if (bgrid == 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            RCGS_CUDA(cudaGetDevice(&dev));
+            RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rec_bwd_kernel, kCTA, 0));
+            bgrid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
+        }
+        const int blocks = (int)min((int64_t)bgrid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
+        if (blocks > 0) rec_bwd_kernel<<<blocks, kCTA, 0, s>>>(a);
+        RCGS_LAUNCH_CHECK();
+        return RCGS_OK;
     }
     const int blocks = (int)min((int64_t)grid, ((int64_t)a.n_items + kWarpsPerCTA - 1) / kWarpsPerCTA);
     if (blocks > 0) rec_kernel<kMode><<<blocks, kCTA, 0, s>>>(a);
