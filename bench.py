@@ -624,35 +624,63 @@ def run_interactive(args, scene, cams, ds, sh0, sp, cloud, frames=60):
     from paper_2511_18441_b200.selection import project_cloud_device
     from paper_2511_18441_b200.synthetic import ring_cameras
 
+    import concurrent.futures
+
+    # training views are drawn from the optimizer's RNG, so they are built ahead
+    # (prefetch); the viewer's camera is only known when its frame starts, so its
+    # view is built during the frame -- on a side thread and stream, concurrently
+    # with the optimizer step it does not depend on (geometry is frozen; only its
+    # colour needs the updated SH)
     eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
-                      seed=11, cache_views=False)
+                      seed=11, cache_views=False, prefetch=2)
     intr = cams[0][0]
     orbit = ring_cameras(intr.width, intr.height, frames)
     pts = D.to_device(cloud.points, torch.float64)
+    dev = torch.cuda.current_device()
+    side = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
+    pool = concurrent.futures.ThreadPoolExecutor(1)
+    host = torch.empty((intr.height, intr.width, 4), dtype=torch.uint8, pin_memory=True)
+
+    def build(ci, cp):
+        torch.cuda.set_device(dev)
+        with torch.cuda.stream(side):
+            v = D.View(ds, ci, cp, P.DEFAULT_CONFIG)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        return v, ev
+
     lat = []
     for f in range(frames + 5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        eng.step()
         ci, cp = orbit[f % frames]
-        v = D.View(ds, ci, cp, P.DEFAULT_CONFIG)
+        fut = pool.submit(build, ci, cp)   # viewer frame's preprocess + binning
+        eng.step()                         # one optimizer step (main stream)
+        v, ev = fut.result()
+        torch.cuda.current_stream().wait_event(ev)
         v.color(eng.sh)
         depth = v.depth(0.5)
         mask = project_cloud_device(pts, ci, cp, depth, 5, 0.02)
         rgba = v.render_rgba(mask)  # render + selection overlay + RGBA8 in one pass
-        frame = rgba.cpu()
-        v.close()
+        host.copy_(rgba, non_blocking=True)
         torch.cuda.synchronize()
+        frame = host
+        with torch.cuda.stream(side):  # freed on the stream that allocated it
+            side.wait_stream(torch.cuda.current_stream())
+            v.close()
         if f >= 5:
             lat.append((time.perf_counter() - t0) * 1000.0)
+    pool.shutdown()
     eng.drain()
     eng.close()
     lat = np.array(lat)
     return {"frames": len(lat), "p50_ms": round(float(np.percentile(lat, 50)), 3),
             "p99_ms": round(float(np.percentile(lat, 99)), 3), "fps_p50": round(1000.0 / float(np.percentile(lat, 50)), 1),
             "frame_bytes_d2h": int(frame.numel()),
-            "note": "1 optimizer step + viewer frame (depth, cloud projection, render with the selection "
-                    "overlay and RGBA8 quantisation fused, rcgs_render_rgba) + RGBA8 readback per frame"}
+            "note": "1 optimizer step + viewer frame (preprocess + binning of the viewer camera, built "
+                    "concurrently with the step; colour, depth, cloud projection, render with the selection "
+                    "overlay and RGBA8 quantisation fused, rcgs_render_rgba) + pinned RGBA8 readback per frame; "
+                    "training views prefetched"}
 
 
 def run_selection_sweep(group, world, rank, dev):
