@@ -143,20 +143,45 @@ class SelectionPass:
         if stats and self.hits is None:
             self.hits = torch.zeros(self.dscene.n, dtype=torch.int32, device=dev)
             self.wsum = torch.zeros(self.dscene.n, dtype=torch.int64, device=dev)
-        for i in idx:
-            intr, pose = self.cameras[i]
-            self.masks[i].zero_()
-            if points_dev is not None and points_dev.shape[0] > 0:
-                view = self.view(i)
-                depth = view.depth(tau)
-                project_cloud_device(points_dev, intr, pose, depth, quad_size, depth_tolerance,
-                                     out=self.masks[i])
-                if stats:
-                    view.mask_hits(self.masks[i], self.hits, self.wsum)
-                if not self.keep_views:
-                    view.close()
-                    self.views[i] = None
-            apply_recolor_device(self.gt[i], self.masks[i], tint, out=self.edited[i])
+        idx = list(idx)
+        has_points = points_dev is not None and points_dev.shape[0] > 0
+        # views not kept are built ahead on side streams by worker threads (their
+        # two host syncs and latency-bound build kernels overlap this loop's
+        # depth / projection / hit passes); results are identical
+        pf = None
+        ahead = 3
+        if has_points and not self.keep_views and len(idx) > 1 and all(self.views[i] is None for i in idx):
+            from .engine import ViewPrefetcher  # engine imports this module's users, not this module
+            pf = ViewPrefetcher(self.dscene, self.cameras, self.raster, dev.index if dev.index is not None else 0,
+                                depth=ahead)
+            for k, i in enumerate(idx[:ahead]):
+                pf.submit(k, i)
+        try:
+            for k, i in enumerate(idx):
+                intr, pose = self.cameras[i]
+                self.masks[i].zero_()
+                if has_points:
+                    if pf is not None:
+                        view, ev, _ = pf.take(k)
+                        torch.cuda.current_stream().wait_event(ev)
+                        if k + ahead < len(idx):
+                            pf.submit(k + ahead, idx[k + ahead])
+                    else:
+                        view = self.view(i)
+                    depth = view.depth(tau)
+                    project_cloud_device(points_dev, intr, pose, depth, quad_size, depth_tolerance,
+                                         out=self.masks[i])
+                    if stats:
+                        view.mask_hits(self.masks[i], self.hits, self.wsum)
+                    if pf is not None:
+                        pf.retire(view)
+                    elif not self.keep_views:
+                        view.close()
+                        self.views[i] = None
+                apply_recolor_device(self.gt[i], self.masks[i], tint, out=self.edited[i])
+        finally:
+            if pf is not None:
+                pf.close()
         return self
 
     def wsum_float(self) -> torch.Tensor:
