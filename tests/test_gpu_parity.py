@@ -339,6 +339,24 @@ def test_selection_pass_mask_hits_exact(two_blobs):
                                atol=1e-7)
 
 
+def test_selection_pass_prefetched_equals_inline(orbit_room):
+    """SelectionPass builds upcoming views on worker streams when it does not keep
+    them; masks, edited targets, hit counts and weights equal the inline path's."""
+    import torch
+    from paper_2511_18441_b200 import device as D
+    scene = p_scene(orbit_room)
+    cams = [p_cam(orbit_room, f"v{v}_") for v in (0, 3)] * 4  # 8 views
+    ds = D.device_scene(scene)
+    gt = torch.stack([D.to_device(orbit_room[f"v{v}_image"]) for v in (0, 3)] * 4)
+    rng = np.random.default_rng(9)
+    pts = D.to_device(rng.uniform(-1.0, 1.0, (4000, 3)) * [1, 1, 0.6], torch.float64)
+    a = P.SelectionPass(ds, cams, gt).run(pts, (1.0, 0.2, 0.2))            # prefetched
+    b = P.SelectionPass(ds, cams, gt, keep_views=True).run(pts, (1.0, 0.2, 0.2))  # inline
+    assert torch.equal(a.masks, b.masks) and torch.equal(a.edited, b.edited)
+    assert torch.equal(a.hits, b.hits) and torch.equal(a.wsum, b.wsum)
+    assert int(a.masks.sum()) > 0
+
+
 # ---------------------------------------------------------------- optimizer trajectory
 def test_refit_trajectory_tracks_reference(two_blobs):
     """10 iterations of BackgroundOptimizer(seed=7) vs the reference run.  The
