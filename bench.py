@@ -340,16 +340,13 @@ def run_gpu(args):
     cpu = cpu_baseline_sample(args, cfg) if args.cpu_baseline else None
     value = world / (step_ms / 1000.0)
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "view-steps/s (opt steps/s x views per step)",
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
         "step_ms_p10_p50_p90_max": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90, 100)],
         "slowest_steps": [[int(i), round(float(per_step[i]), 3)] for i in np.argsort(per_step)[-3:][::-1]],
         "vs_baseline": None, "dtype": "f32 (fp64 decisions/keys/loss)", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg['n']} gaussians SH deg {cfg['deg']}, "
-                               f"{cfg['views']} views {cfg['width']}x{cfg['height']}, selection + recolor",
-                   "views_per_step": world, "l2": "inputs larger than L2 (SH + Adam state "
-                   f"{cfg['n'] * 48 * 4 * 3 / 1e6:.0f} MB touched per step)", "parallelism": f"views{world}"},
+        "config": workload_config(args, cfg, world),
         "opt_steps_per_s": round(1000.0 / step_ms, 3),
         "rendered_mpix_s": round(world * npix / (frame_ms / 1000.0) / 1e6, 1),
         "render_ms_per_frame": round(frame_ms, 4),
@@ -747,7 +744,7 @@ def run_e2e(args, scene, cams, sp, group, world):
     dt = sync_max(dt, world)
     opt.stop()
     h, w = edited.shape[1], edited.shape[2]
-    return {"value": round(world * args.steps / dt, 3), "unit": "view-steps/s",
+    return {"value": round(world * args.steps / dt, 3), "unit": UNIT,
             "h2d_bytes_per_step": int(h * w * 3 * 4), "d2h_bytes_per_step": 32,
             "api": "BackgroundOptimizer(stream_targets=True): target H2D every step on the prefetch stream, "
                    "metrics D2H every step (pipelined one step)"}
@@ -800,7 +797,7 @@ def cpu_reference(cfg, budget_s=20.0, workers=None):
     # forward (alpha + weights) dominates; the capture/colour/backward/loss add
     # ~35% (einsum 19% + nonzero 15% + loss/backward/adam ~3-4%)
     step_s = t_proj + wall / done * npix * 1.37
-    return {"value": 1.0 / step_s, "unit": "view-steps/s", "cores": workers, "kind": "port",
+    return {"value": 1.0 / step_s, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": f"{done} pixels of view 0 at {cfg['n']} gaussians ({p.count} kept), dense "
                       f"reference composite, extrapolated to {npix} px x 1.37 (capture+loss+backward+adam)",
             "rendered_mpix_s": npix / ((t_proj + wall / done * npix) * 1e6)}
@@ -811,6 +808,17 @@ def cpu_baseline_sample(args, cfg):
         return cpu_reference(cfg, budget_s=args.cpu_budget)
     except Exception as e:  # never fail the GPU line because of the baseline
         return {"value": None, "error": repr(e)}
+
+
+UNIT = "view-steps/s (opt steps/s x views per step)"
+
+
+def workload_config(args, cfg, world):
+    """The `config` object both arms report (same workload, same keys)."""
+    return {"workload": f"{args.config}: {cfg['n']} gaussians SH deg {cfg['deg']}, "
+                        f"{cfg['views']} views {cfg['width']}x{cfg['height']}, selection + recolor",
+            "views_per_step": world, "l2": "inputs larger than L2 (SH + Adam state "
+            f"{cfg['n'] * 48 * 4 * 3 / 1e6:.0f} MB touched per step)", "parallelism": f"views{world}"}
 
 
 def run_reference(args):
@@ -825,12 +833,12 @@ def run_reference(args):
     base = vals[args.warmup:]
     value = float(np.mean([b["value"] for b in base]))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "view-steps/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.config, **cfg},
-        "cpu_baseline": {**base[-1], "value": value},
-        "e2e": {"value": value, "unit": "view-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic", "config": workload_config(args, cfg, world),
+        "cpu_baseline": {**base[-1], "value": value, "unit": UNIT},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
