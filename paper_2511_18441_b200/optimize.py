@@ -291,7 +291,11 @@ class BackgroundOptimizer:
         with self._lock:
             self._version += 1
         if len(self._engine.pending) >= min(self._config.snapshot_every, self._engine.max_pending):
-            self._flush()
+            # non-blocking: starts the metrics read-back of the pending steps and
+            # delivers the ones already landed (every step's metrics still reach the
+            # sink, in order, one flush later) -- a blocking flush here drained the
+            # whole step pipeline every `snapshot_every` iterations
+            self._flush(wait=False)
 
     def _flush(self, wait: bool = True) -> None:
         recs = self._engine.drain(wait)
