@@ -20,7 +20,7 @@ STAGES = {  # bench stage -> kernel name prefixes (ncu "Kernel Name" without arg
     "raster_fwd": ["void rcgs::raster_kernel<0,", "rcgs::raster_kernel<0,", "void rcgs::raster_kernel<6,",
                    "rcgs::raster_kernel<6,", "void rcgs::rec_kernel<0>", "rcgs::rec_kernel<0>"],
     "raster_bwd": ["void rcgs::raster_kernel<2,", "rcgs::raster_kernel<2,", "void rcgs::rec_kernel<1>",
-                   "rcgs::rec_kernel<1>", "bwd_finish_kernel"],
+                   "rcgs::rec_kernel<1>", "rcgs::rec_bwd_kernel", "bwd_finish_kernel"],
     "adam": ["rcgs::adam_prep_kernel", "rcgs::adam_fused_kernel", "rcgs::step_commit_kernel"],
     "color": ["rcgs::color_kernel"],
     "loss_grad": ["void rcgs::loss_", "rcgs::loss_"],
