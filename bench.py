@@ -185,7 +185,7 @@ def run_gpu(args):
     pts = D.to_device(cloud.points, torch.float64)
     mine = parallel.shard_views(len(cams), rank, world)
     sp = P.SelectionPass(ds, cams, gt)
-    sp.run(pts, (1.0, 0.2, 0.2), indices=mine[:1])  # warm-up
+    sp.run(pts, (1.0, 0.2, 0.2), indices=mine[:2])  # warm-up (two views: also the prefetched path)
     sp = P.SelectionPass(ds, cams, gt)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
