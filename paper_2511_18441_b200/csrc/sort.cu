@@ -50,17 +50,29 @@ int pool_reserve(int64_t bytes, cudaStream_t s) {
     return RCGS_OK;
 }
 
-void* pinned_scratch(size_t bytes) {
-    static thread_local void* buf = nullptr;
-    static thread_local size_t cap = 0;
-    if (bytes > cap) {
-        if (buf) cudaFreeHost(buf);
-        buf = nullptr;
-        cap = 0;
-        if (cudaMallocHost(&buf, bytes) != cudaSuccess) return nullptr;
-        cap = bytes;
+// Per-thread pinned staging for small device->host reads.  Builder threads come
+// and go (one pair per prefetcher), so the buffer is released when its thread
+// exits instead of leaking one pinned page per thread.
+namespace {
+struct PinnedScratch {
+    void* buf = nullptr;
+    size_t cap = 0;
+    ~PinnedScratch() {
+        if (buf) cudaFreeHost(buf);  // errors at process teardown are irrelevant
     }
-    return buf;
+};
+}  // namespace
+
+void* pinned_scratch(size_t bytes) {
+    static thread_local PinnedScratch ps;
+    if (bytes > ps.cap) {
+        if (ps.buf) cudaFreeHost(ps.buf);
+        ps.buf = nullptr;
+        ps.cap = 0;
+        if (cudaMallocHost(&ps.buf, bytes) != cudaSuccess) return nullptr;
+        ps.cap = bytes;
+    }
+    return ps.buf;
 }
 
 // ---------------------------------------------------------------- block scan
