@@ -6,6 +6,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include <cstdlib>
 
 namespace rcgs {
 
@@ -28,6 +29,12 @@ void retain_pool_memory() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // blocks freed on one stream may be reused by another only once the free
+        // has completed: with internal dependencies the pool would make the main
+        // stream wait on a builder stream's queued work (or vice versa)
+        static const bool internal = getenv("RCGS_POOL_INTERNAL_DEPS") != nullptr;
+        int allow = internal ? 1 : 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &allow);
     }
     done_dev = dev;
 }

@@ -152,6 +152,8 @@ class SelectionPass:
         ahead = 3
         if has_points and not self.keep_views and len(idx) > 1 and all(self.views[i] is None for i in idx):
             from .engine import ViewPrefetcher  # engine imports this module's users, not this module
+            # the views in flight come from the retained pool (as RefitEngine reserves)
+            N.call("rcgs_pool_reserve", int((ahead + 2) * self.dscene.n * 400), D.stream_ptr())
             pf = ViewPrefetcher(self.dscene, self.cameras, self.raster, dev.index if dev.index is not None else 0,
                                 depth=ahead)
             for k, i in enumerate(idx[:ahead]):
