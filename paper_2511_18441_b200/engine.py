@@ -281,8 +281,40 @@ class RefitEngine:
         return self._bufs[key]
 
     def draw(self):
-        """View indices of the next step from the reference RNG stream (optimize.py:106)."""
+        """View indices of the next step from the reference RNG stream (optimize.py:106)
+        -- after any picks restored by `load_state` that were drawn before it."""
+        replay = getattr(self, "_replay", None)
+        if replay:
+            return replay.popleft()
         return parallel.draw_views(self.rng, len(self.cameras), self.world)
+
+    # -- optimizer state (checkpoint / resume) -------------------------------------
+    def state_dict(self) -> dict:
+        """Exact resume state: SH / Adam moments / step counter, the RNG, and the
+        picks already drawn for steps not yet executed (prefetch draws ahead).
+        Pending metrics are not included; drain() first."""
+        ahead = []
+        if self._held is not None:
+            ahead.append(list(self._held[0]))
+        ahead += [list(p) for _, p in self._future]
+        ahead += [list(p) for p in getattr(self, "_replay", ())]
+        return {"sh": self.sh.cpu().numpy(), "m": self.m.cpu().numpy(), "v": self.v.cpu().numpy(),
+                "step": int(self.step_dev.item()), "rng": self.rng.bit_generator.state, "ahead": ahead}
+
+    def load_state_dict(self, st: dict) -> None:
+        """Restore `state_dict()` into a fresh engine (same scene, views and world size)."""
+        if self._held is not None or self._future:
+            raise RuntimeError("load_state_dict needs an engine that has not stepped")
+        for name in ("sh", "m", "v"):
+            src = torch.as_tensor(np.ascontiguousarray(st[name], dtype=np.float32))
+            dst = getattr(self, name)
+            if tuple(src.shape) != tuple(dst.shape):
+                raise ValueError(f"state {name} has shape {tuple(src.shape)}, engine {tuple(dst.shape)}")
+            dst.copy_(src.to(dst.device))
+        self.step_dev.fill_(int(st["step"]))
+        self.rng.bit_generator.state = st["rng"]
+        self._replay = collections.deque([list(p) for p in st["ahead"]])
+        torch.cuda.current_stream().synchronize()
 
     # -- one step -----------------------------------------------------------------
     def _next_prefetched(self):

@@ -239,6 +239,39 @@ class BackgroundOptimizer:
                 self._sh_base = torch.from_numpy(np.ascontiguousarray(self._scene0.sh)).to(self._sh0.device)
             save_scene_ply_device(self._scene0, self._engine.sh, path, sh_base=(self._sh_base, self._sh0))
 
+    def save_state(self, path) -> None:
+        """Optimizer checkpoint for an exact resume (an extension; the reference
+        restarts Adam per session, session.py:355-358): SH, Adam moments and step,
+        the view-sampling RNG and the views already drawn ahead, the accepted-step
+        count.  Pending metrics are delivered to the sink first."""
+        import json
+        if self._thread is not None and not self.paused:
+            raise ValidationError("save_state needs a paused or synchronous optimizer")
+        with self._lock:
+            self._flush()
+            st = self._engine.state_dict()
+            meta = {"rng": st["rng"], "ahead": st["ahead"], "step": st["step"], "accepted": self._accepted,
+                    "n": int(st["sh"].shape[0])}
+        np.savez(path, sh=st["sh"], m=st["m"], v=st["v"], meta=np.array(json.dumps(meta)))
+
+    def load_state(self, path) -> None:
+        """Restore `save_state` into a fresh optimizer built on the same scene,
+        dataset cameras, config and world size; the next iterations then equal
+        the ones the saved optimizer would have run, bit for bit."""
+        import json
+        if self._thread is not None:
+            raise ValidationError("load_state must precede start()")
+        with np.load(path) as z:
+            meta = json.loads(str(z["meta"]))
+            st = {"sh": z["sh"], "m": z["m"], "v": z["v"], "step": meta["step"], "rng": meta["rng"],
+                  "ahead": meta["ahead"]}
+        with self._lock:
+            self._engine.load_state_dict(st)
+            self._accepted = int(meta["accepted"])
+            self._snapshot_sh.copy_(self._engine.sh)  # the published snapshot is the restored SH
+            self._snapshot_cache = (None, None)
+            self._version += 1
+
     def status(self) -> OptimizerStatus:
         with self._lock:
             return self._status

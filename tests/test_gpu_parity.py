@@ -382,6 +382,32 @@ def test_refit_trajectory_tracks_reference(two_blobs):
     np.testing.assert_array_equal(final.positions, scene.positions)
 
 
+@pytest.mark.parametrize("prefetch", [0, 2])
+def test_optimizer_state_resume_is_exact(two_blobs, tmp_path, prefetch):
+    """save_state after 6 iterations, then 5 more == a fresh optimizer that loads
+    the state and runs 5: same SH bits and the same metric lines (the views drawn
+    ahead by the prefetcher are replayed before new draws)."""
+    scene = p_scene(two_blobs)
+    views = []
+    for v in (0, 1):
+        intr, pose = p_cam(two_blobs, f"v{v}_")
+        views.append(P.TrainingView(v, intr, pose, P.render(scene, intr, pose)))
+    ds = P.build_edited_dataset(views, P.SelectionCloud(two_blobs["cloud"]), (1.0, 0.2, 0.2), scene)
+    kw = dict(seed=7, cache_views=prefetch == 0, prefetch=prefetch)
+    la, lb = [], []
+    a = P.BackgroundOptimizer(scene, ds, metrics_sink=lambda m: la.append(m.line()), **kw)
+    a.run_iterations(6)
+    a.save_state(tmp_path / "state.npz")
+    sha = a.run_iterations(5).sh
+    a.stop()
+    b = P.BackgroundOptimizer(scene, ds, metrics_sink=lambda m: lb.append(m.line()), **kw)
+    b.load_state(tmp_path / "state.npz")
+    shb = b.run_iterations(5).sh
+    b.stop()
+    np.testing.assert_array_equal(sha, shb)
+    assert lb == la[6:]
+
+
 def test_self_consistent_dataset_is_fixed_point(two_blobs):
     scene = p_scene(two_blobs)
     views = []
