@@ -257,6 +257,11 @@ def run_gpu(args):
     N.call("rcgs_raster_counters", None)
     eng.stage_report(reset=True)
     cnt = counters.view(6, 5).cpu().numpy() / float(ncnt)  # per launch (one per step)
+    # fraction q of a block's entries shared with the other 8x4 block of its 8x8
+    # region (static list culls): q = 2 - 2 U / E  (U region entries, E block entries)
+    region_q = None
+    if cnt[5, 0] > 0:
+        region_q = round(float(2.0 - 2.0 * cnt[5, 1] / cnt[5, 0]), 4)
     if world > 1:
         torch.distributed.barrier()
 
@@ -358,7 +363,7 @@ def run_gpu(args):
         "prefetch_host_ms_max": {k: round(live[k], 3) for k in ("prefetch_host_build_ms_max", "prefetch_wait_ms_max")
                                  if k in live},
         "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
-        "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"],
+        "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"], "raster_region_share_q": region_q,
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,

@@ -149,7 +149,9 @@ int rcgs_capture(const rcgs_view* view, int64_t* h_count, int64_t* d_pixel, int6
  * capture), {evaluated pixel-entry pairs, composited pairs, warp blocks processed,
  * warp blocks skipped, warp-level entry iterations} into the (6, 5) uint64 array;
  * pass NULL to switch off.  Feeds the benchmark's compute roofline (one atomic
- * per warp block, <1% overhead). */
+ * per warp block, <1% overhead).  The recording forward also fills [25] / [26] with
+ * static list statistics: entries passing each 8x4 block's cull, and entries
+ * passing each 8x8 region's cull (planning data for a two-pixels-per-lane raster). */
 int rcgs_raster_counters(uint64_t* d_counters30);
 
 /* Diagnostics: while d_trace != NULL every raster launch with at most max_items

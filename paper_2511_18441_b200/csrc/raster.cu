@@ -426,6 +426,37 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
 
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
+        if (kInstr && M == FWDREC && a.counters) {
+            // static list-cull statistics for a two-pixels-per-lane raster (8x8
+            // regions): entries passing this 8x4 block's cull, and for the top block
+            // of each 8x8 region the entries passing the region's cull (row 5 of the
+            // counters: [25] block entries, [26] region entries)
+            const bool top = ((blk >> 1) & 1) == 0;
+            unsigned cb = 0, cu = 0;
+            for (uint32_t j = range.x + lane; j < range.y; j += 32) {
+                const uint32_t sj = a.pair_g[j];
+                const float4 qa = a.rec[sj].a, qb = a.rec[sj].b, qc = a.rec[sj].c;
+                cb += touches_block(qa, fbx0, fby0) &&
+                      ellipse_touches_rect(qa, qb, qc, fbx0, fby0, fbx0 + 7.f, fby0 + 3.f);
+                if (top) {
+                    const unsigned pk = __float_as_uint(qa.z);
+                    const float ex = __half2float(__ushort_as_half((unsigned short)(pk & 0xffffu)));
+                    const float ey = __half2float(__ushort_as_half((unsigned short)(pk >> 16)));
+                    const bool box = qa.x + ex >= fbx0 && qa.x - ex <= fbx0 + 7.f && qa.y + ey >= fby0 &&
+                                     qa.y - ey <= fby0 + 7.f;
+                    cu += box && ellipse_touches_rect(qa, qb, qc, fbx0, fby0, fbx0 + 7.f, fby0 + 7.f);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                cb += __shfl_xor_sync(0xffffffffu, cb, o);
+                cu += __shfl_xor_sync(0xffffffffu, cu, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.counters[25], (unsigned long long)cb);
+                atomicAdd(&a.counters[26], (unsigned long long)cu);
+            }
+        }
         uint32_t n_eval = 0, n_comp = 0, n_iter = 0;
         // FWDREC: this block's record slots, 8 per tile-list entry and block (32-bit:
         // the host checks 8 * pairs < 2^32)
