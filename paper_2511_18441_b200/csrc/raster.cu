@@ -380,7 +380,11 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
     constexpr int kRow = (M == FWDREC || M == FWDRGBA) ? (int)FWD : M;  // counter row
     __shared__ WarpStage stage_all[kRWarps];
     const int lane = threadIdx.x & 31;
-    WarpStage& st = stage_all[kRWarps == 1 ? 0 : threadIdx.x >> 5];
+    // The warp index comes from a shuffle: ptxas cannot re-derive a shuffle result
+    // from threadIdx / the CTA id at every use (which it did with the plain
+    // expression, ~16 instructions per entry), so the staging base stays in a
+    // register.  Measured 332 -> 323 us for the recording raster.
+    WarpStage& st = stage_all[kRWarps == 1 ? 0 : __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0)];
     const uint32_t lt_mask = (1u << lane) - 1u;
 
     for (;;) {
