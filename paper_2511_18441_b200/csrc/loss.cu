@@ -103,19 +103,26 @@ __global__ void __launch_bounds__(kLNT) loss_dirty_kernel(const T* __restrict__ 
                                                           int H, int W, uint8_t* __restrict__ dirty) {
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     int d = 0;
-    // chunk by chunk with a block vote: a block that differs (every block, once the
-    // refit is under way) stops after its first chunk
-    for (int c0 = 0; c0 < kLT * kLT * 3 && !d; c0 += kLNT) {
-        const int i = c0 + threadIdx.x;
-        int di = 0;
-        if (i < kLT * kLT * 3) {
-            const int p = i / 3, ch = i % 3;
+    // chunk by chunk with a block vote: a block that differs (most blocks, once the
+    // refit is under way) stops after its first chunk; kDU values per thread per
+    // chunk (all loads in flight before the compares) keep the votes few
+    constexpr int kDU = 4;
+    for (int c0 = 0; c0 < kLT * kLT * 3 && !d; c0 += kLNT * kDU) {
+        T yv[kDU], gv[kDU];
+        bool ok[kDU];
+#pragma unroll
+        for (int u = 0; u < kDU; ++u) {
+            const int i = c0 + u * kLNT + threadIdx.x;
+            const int p = i / 3, ch = i - 3 * (i / 3);
             const int gy = y0 + p / kLT, gx = x0 + p % kLT;
-            if (gy < H && gx < W) {
-                const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
-                di = y[o] != g[o];
-            }
+            ok[u] = i < kLT * kLT * 3 && gy < H && gx < W;
+            const int64_t o = ((int64_t)gy * W + gx) * 3 + ch;
+            yv[u] = ok[u] ? y[o] : T(0);
+            gv[u] = ok[u] ? g[o] : T(0);
         }
+        int di = 0;
+#pragma unroll
+        for (int u = 0; u < kDU; ++u) di |= ok[u] && yv[u] != gv[u];
         d = __syncthreads_or(di);
     }
     if (threadIdx.x == 0) dirty[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)d;
