@@ -14,11 +14,15 @@
 // Pass B: separable filter of M1..M3 -> gradient within one block of a
 //         difference; exact zeros elsewhere and when the images are identical
 //         (losses.py:127-130).
-// Pass C: fixed-order final reduction -> {l1, ssim, total} (deterministic).
+// Tail of pass A: the last block to finish reduces the per-block partials in a
+//         fixed order -> {l1, ssim, total} (deterministic; formerly a pass C kernel).
 // Both filter passes work on 32x32 output tiles (42x42 with the 5-pixel halo),
 // one channel at a time; the vertical pass is a register sliding window (each
 // thread produces 4 rows of one column from 14 shared-memory rows).
 #include <math.h>
+
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -136,12 +140,46 @@ __device__ __forceinline__ bool near_dirty(const uint8_t* __restrict__ dirty, in
     return false;
 }
 
+// Final reduction of the per-block partials (formerly pass C), run by the last
+// pass-A block to finish: a fixed assignment of blocks to threads and a fixed
+// reduction tree, so the result is deterministic regardless of which block it is.
+struct LossTail {
+    unsigned* ticket;  // per-stream counter, zero between launches (the last block resets it)
+    double n, lam;
+    bool ssim_valid;
+    double* out3;
+};
+
+__device__ void loss_tail(const double* __restrict__ part, int nb, const LossTail& lt, double* red) {
+    __shared__ unsigned s_last;
+    __threadfence();  // this block's partial is visible before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(lt.ticket, 1u) == (unsigned)nb - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nb; i += kLNT) {
+        a += __ldcg(&part[2 * i]);
+        b += __ldcg(&part[2 * i + 1]);
+    }
+    block_sum2(a, b, red);
+    if (threadIdx.x == 0) {
+        const double l1 = a / lt.n;
+        const double ss = lt.ssim_valid ? b / lt.n : __longlong_as_double(0x7ff8000000000000ll);
+        lt.out3[0] = l1;
+        lt.out3[1] = ss;
+        lt.out3[2] = lt.lam == 0.0 ? l1 : (1.0 - lt.lam) * l1 + lt.lam * (1.0 - ss);
+        *lt.ticket = 0u;
+    }
+}
+
 // ---------------------------------------------------------------- pass A
 template <bool SSIM, typename T, typename MT>
 __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
                                                     int W, Window win, MT* __restrict__ maps,
                                                     double* __restrict__ block_part,
-                                                    const uint8_t* __restrict__ dirty) {
+                                                    const uint8_t* __restrict__ dirty, LossTail lt) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // input planes in the input type (exact), horizontal sums in fp64
     double* hs = reinterpret_cast<double*>(smem_raw);  // [5][42][32]
@@ -167,6 +205,7 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
             block_part[2 * b] = 0.0;
             block_part[2 * b + 1] = SSIM ? (double)(vw * vh * 3) : 0.0;
         }
+        loss_tail(block_part, gridDim.x * gridDim.y, lt, red);
         return;
     }
 
@@ -296,6 +335,8 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
         block_part[2 * b] = l1;
         block_part[2 * b + 1] = ss;
     }
+    __syncthreads();  // red[] is reused by the tail
+    loss_tail(block_part, gridDim.x * gridDim.y, lt, red);
 }
 
 // 4- or 8-byte asynchronous global -> shared copy (LDGSTS); `in` false zero-fills
@@ -405,25 +446,6 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
     }
 }
 
-__global__ void loss_pass_c(const double* __restrict__ part, int nb, double n, double lam, bool ssim_valid,
-                            double* __restrict__ out3) {
-    __shared__ double red[2 * kLNT / 32];
-    double a = 0.0, b = 0.0;
-    // fixed assignment of blocks to threads and a fixed reduction tree: deterministic
-    for (int i = threadIdx.x; i < nb; i += kLNT) {
-        a += part[2 * i];
-        b += part[2 * i + 1];
-    }
-    block_sum2(a, b, red);
-    if (threadIdx.x == 0) {
-        const double l1 = a / n;
-        const double ss = ssim_valid ? b / n : __longlong_as_double(0x7ff8000000000000ll);
-        out3[0] = l1;
-        out3[1] = ss;
-        out3[2] = lam == 0.0 ? l1 : (1.0 - lam) * l1 + lam * (1.0 - ss);
-    }
-}
-
 static Window make_window() {
     Window w;
     double sum = 0.0;
@@ -439,6 +461,22 @@ static Window make_window() {
 }  // namespace rcgs
 
 using namespace rcgs;
+
+// Per-stream zeroed ticket for pass A's tail reduction (the last block resets it, so
+// it is zero again for the next launch on that stream; launches on one stream are
+// ordered, on different streams they use different tickets).
+static unsigned* stream_ticket(cudaStream_t s) {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, unsigned*> tickets;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = tickets.find(s);
+    if (it != tickets.end()) return it->second;
+    unsigned* t = nullptr;
+    if (cudaMalloc(&t, sizeof(unsigned)) != cudaSuccess || cudaMemset(t, 0, sizeof(unsigned)) != cudaSuccess)
+        return nullptr;
+    tickets.emplace(s, t);
+    return t;
+}
 
 // MT: storage type of the three gradient maps between the passes -- fp64 for the
 // fp64 entry point, fp32 when the gradient itself is fp32 (halves the maps'
@@ -461,6 +499,13 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     uint8_t* dirty = nullptr;
     RCGS_TRY(dalloc(&part, 2 * nb, s));
     RCGS_TRY(dalloc(&dirty, nb, s));
+    LossTail lt;
+    lt.ticket = stream_ticket(s);
+    RCGS_CHECK_ARG(lt.ticket != nullptr, "loss ticket allocation failed");
+    lt.n = (double)(npix * 3);
+    lt.lam = lam;
+    lt.ssim_valid = ssim_ok;
+    lt.out3 = d_loss3;
     loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty);
     const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
     const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
@@ -470,7 +515,8 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
                                        (int)smem_a));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_b<true, T, G, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_b));
-        loss_pass_a<true, T, MT><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, dirty);
+        loss_pass_a<true, T, MT><<<grid, kLNT, smem_a, s>>>(d_image, d_target, height, width, win, maps, part, dirty,
+                                                            lt);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
             loss_pass_b<true, T, G, MT><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
@@ -481,13 +527,12 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
         }
         RCGS_LAUNCH_CHECK();
     } else {
-        loss_pass_a<false, T, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part, dirty);
+        loss_pass_a<false, T, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part,
+                                                         dirty, lt);
         loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr,
                                                            dirty, d_grad);
         RCGS_LAUNCH_CHECK();
     }
-    loss_pass_c<<<1, kLNT, 0, s>>>(part, nb, (double)(npix * 3), lam, ssim_ok, d_loss3);
-    RCGS_LAUNCH_CHECK();
     dfree(maps, s);
     dfree(part, s);
     dfree(dirty, s);
