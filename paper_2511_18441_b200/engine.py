@@ -69,7 +69,7 @@ class ViewPrefetcher:
         self.targets = targets if targets is not None and any(not t.is_cuda for t in targets) else None
         self.ring = [None] * (depth + 4)
         self.ring_free = [None] * (depth + 4)
-        self.copy_stream = torch.cuda.Stream(device=device) if self.targets is not None else None
+        self.copy_stream = None  # one copy stream per worker (below): uploads of two steps run concurrently
         self.events = []  # (start, end) of each view build on its side stream
         self.host_build_ms = []
         self.host_wait_ms = []
@@ -79,6 +79,11 @@ class ViewPrefetcher:
         prio = os.environ.get("RCGS_PREFETCH_PRIORITY")
         prio = int(prio) if prio is not None else torch.cuda.Stream.priority_range()[1]
         self.streams = [torch.cuda.Stream(device=device, priority=prio) for _ in range(workers)]
+        # per-worker copy streams: with one, the ~25 MB target uploads (one per step,
+        # ~21 GB/s from pinned host memory) were serialised at about the step rate
+        nc = int(os.environ.get("RCGS_UPLOAD_STREAMS", str(workers)))
+        self.copy_streams = ([torch.cuda.Stream(device=device) for _ in range(max(1, nc))]
+                             if self.targets is not None else [])
         self.jobs = collections.deque()
         self.retired = [collections.deque() for _ in range(workers)]
         self.builder = {}  # id(view) -> index of the worker that built it
@@ -152,15 +157,16 @@ class ViewPrefetcher:
                         slot = key % len(self.ring)
                         with self.cv:
                             free = self.ring_free[slot]
-                        with torch.cuda.stream(self.copy_stream):
+                        cs = self.copy_streams[w % len(self.copy_streams)]
+                        with torch.cuda.stream(cs):
                             if free is not None:
-                                self.copy_stream.wait_event(free)
+                                cs.wait_event(free)
                             if self.ring[slot] is None or self.ring[slot].shape != src.shape:
                                 self.ring[slot] = torch.empty(src.shape, dtype=torch.float32, device=self.device)
                             tgt = self.ring[slot]
                             tgt.copy_(src, non_blocking=True)
                             copied = torch.cuda.Event()
-                            copied.record(self.copy_stream)
+                            copied.record(cs)
                     t0 = time.perf_counter()
                     if self.profile:
                         e0 = torch.cuda.Event(enable_timing=True)

@@ -28,13 +28,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--prefetch", type=int, default=2)
+    ap.add_argument("--stream-targets", action="store_true", help="targets in pinned host memory (e2e path)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(bench.CONFIGS["c3"], 0, torch.device("cuda", 0))
     pts = D.to_device(cloud.points, torch.float64)
     sp = P.SelectionPass(ds, cams, gt)
     sp.run(pts, (1.0, 0.2, 0.2))
-    eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
+    targets = [sp.edited[i] for i in range(len(cams))]
+    if a.stream_targets:
+        targets = [t.cpu().pin_memory() for t in targets]
+    eng = RefitEngine(ds, sh0.clone(), cams, targets, P.OptimizerConfig(),
                       seed=7, cache_views=False, prefetch=a.prefetch)
     for _ in range(8):
         eng.step()
