@@ -1,3 +1,9 @@
+"""Selection-pass wall time per config, prefetched (views built ahead on worker
+streams) vs inline (views kept), twice each: the first prefetched run in a
+process pays a one-time thread/stream setup.
+
+    python tools/selection_timing.py
+"""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import torch, bench
