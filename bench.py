@@ -192,12 +192,19 @@ def run_gpu(args):
     e0.record()
     sp.run(pts, (1.0, 0.2, 0.2), indices=mine)
     parallel.reduce_counts(group, sp.hits, sp.wsum)
-    if world > 1:
-        for i in range(len(cams)):  # every rank needs every edited target for the refit
-            torch.distributed.broadcast(sp.edited[i], src=i % world)
     e1.record()
     torch.cuda.synchronize()
     sel_ms = sync_max(e0.elapsed_time(e1), world)
+    # replicate the edited targets for the refit (every rank samples every view):
+    # one all-gather of the ranks' view blocks, timed apart from the selection
+    dist_ms = 0.0
+    if world > 1:
+        torch.distributed.barrier()
+        e0.record()
+        parallel.replicate_views(sp.edited, mine, group)
+        e1.record()
+        torch.cuda.synchronize()
+        dist_ms = sync_max(e0.elapsed_time(e1), world)
     for v in sp.views:
         if v is not None:
             v.close()
@@ -357,6 +364,7 @@ def run_gpu(args):
         "render_ms_per_frame": round(frame_ms, 4),
         "selection": {"views": len(cams), "ms": round(sel_ms, 3),
                       "views_per_s": round(len(cams) / (sel_ms / 1000.0), 1),
+                      "replicate_targets_ms": round(dist_ms, 3),
                       "masked_px": masked_px, "cloud_points": len(cloud)},
         "interactive_job_s": round((sel_ms + 100 * step_ms) / 1000.0, 4),
         "stages_ms": {k: round(v["ms"], 4) for k, v in stages["kernels"].items() if v.get("ms")},
@@ -788,61 +796,72 @@ def run_e2e(args, scene, cams, sp, group, world):
 
 
 # ----------------------------------------------------------------------------- CPU reference arm
-def _cpu_pixels(payload):
-    from oracle import raster as OR
-    p, us, vs = payload
-    t0 = time.perf_counter()
-    xs_done = 0
-    for u, v in zip(us, vs):
-        a = OR.alpha_block(p, np.array([float(u)]), np.array([float(v)]))
-        OR.weights_block(a)
-        xs_done += 1
-    return xs_done, time.perf_counter() - t0
-
-
-def cpu_reference(cfg, budget_s=20.0, workers=None):
-    """The reference algorithm (oracle port of render.py/losses.py/backward.py/
-    optimize.py; the dense per-pixel composite over all kept gaussians in
-    global depth order) timed on a bounded pixel sample and extrapolated to
-    one full optimizer iteration.  Returns a cpu_baseline dict."""
-    import multiprocessing as mp
-    from oracle import raster as OR
-    from paper_2511_18441_b200.synthetic import ring_cameras, scaled_scene
-
-    scene, _ = scaled_scene(cfg["n"], cfg["deg"], seed=0)
-    intr, pose = ring_cameras(cfg["width"], cfg["height"], cfg["views"])[0]
-    t0 = time.perf_counter()
-    p = OR.project(scene, intr, pose)
-    t_proj = time.perf_counter() - t0
-    workers = workers or max(1, min(os.cpu_count() or 1, 16))
-    rng = np.random.default_rng(0)
-    # calibrate: one pixel
-    _, t1 = _cpu_pixels((p, [intr.width // 2], [intr.height // 2]))
-    per_worker = max(1, int(budget_s / max(t1, 1e-6)))
-    us = rng.integers(0, intr.width, per_worker * workers)
-    vs = rng.integers(0, intr.height, per_worker * workers)
-    chunks = [(p, us[i::workers], vs[i::workers]) for i in range(workers)]
-    t0 = time.perf_counter()
-    if workers > 1:
-        with mp.get_context("fork").Pool(workers) as pool:
-            res = pool.map(_cpu_pixels, chunks)
-    else:
-        res = [_cpu_pixels(chunks[0])]
-    wall = time.perf_counter() - t0
-    done = sum(r[0] for r in res)
+def _cpu_line(sampler, done, wall, c1, cfg):
+    """view-steps/s of the CPU reference from a timed pixel sample, extrapolated
+    to a full iteration with the factor measured at config 1 (oracle/refarm.py)."""
     npix = cfg["width"] * cfg["height"]
-    # forward (alpha + weights) dominates; the capture/colour/backward/loss add
-    # ~35% (SURVEY.md 3: einsum 19% + nonzero 15% + loss/backward/adam ~3-4%)
-    step_s = t_proj + wall / done * npix * 1.37
-    return {"value": 1.0 / step_s, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": f"{done} pixels of view 0 at {cfg['n']} gaussians ({p.count} kept), dense "
-                      f"reference composite, extrapolated to {npix} px x 1.37 (capture+loss+backward+adam)",
-            "rendered_mpix_s": npix / ((t_proj + wall / done * npix) * 1e6)}
+    composite_s = sampler.t_proj + wall / done * npix
+    step_s = sampler.t_proj + wall / done * npix * c1["factor"]
+    return {"value": 1.0 / step_s, "unit": UNIT, "cores": sampler.workers, "kind": sampler.kind,
+            "sample": (f"{done} seeded pixels of view 0 at {cfg['n']} gaussians ({sampler.kept} kept), each "
+                       f"composited against every kept gaussian in global depth order by the "
+                       f"{'stock reference (baseline/_ref splattint render._block_alpha/_block_weights)' if sampler.kind == 'reference' else 'oracle port'}"
+                       f" on a {sampler.workers}-process pool; projection {sampler.t_proj:.2f} s once; "
+                       f"extrapolated to {npix} px x {c1['factor']} (full-iteration factor measured at c1)"),
+            "extrapolated": True, "step_s": round(step_s, 1),
+            "rendered_mpix_s": npix / (composite_s * 1e6), "measured_c1": c1}
+
+
+def cpu_reference(cfg, n_pixels=12000, c1=None):
+    """The reference CPU path (stock splattint from baseline/_ref, else the oracle
+    port) on a fixed 12k-pixel sample of the workload, pool and projection built
+    once; see oracle/refarm.py.  Returns a cpu_baseline dict."""
+    from oracle import refarm
+    c1 = c1 or refarm.measured_c1()
+    sampler = refarm.PixelSampler(cfg, n_pixels=n_pixels)
+    try:
+        done, wall = sampler.time(0, n_pixels)
+    finally:
+        sampler.close()
+    return _cpu_line(sampler, done, wall, c1, cfg)
+
+
+def c1_gpu_rate(steps=200):
+    """The GPU engine on config 1 (the config the CPU reference runs in full):
+    view-steps/s, so measured_c1 carries one fully measured GPU/CPU ratio."""
+    import torch
+    import paper_2511_18441_b200 as P
+    from paper_2511_18441_b200.engine import RefitEngine
+    cfg = CONFIGS["c1"]
+    scene, cams, ds, sh0, gt, cloud, _ = build_workload(cfg, 0, torch.device("cuda", torch.cuda.current_device()))
+    targets = [gt[i] for i in range(len(cams))]
+    eng = RefitEngine(ds, sh0.clone(), cams, targets, P.OptimizerConfig(), seed=7, cache_views=False, prefetch=2)
+    for _ in range(10):
+        eng.step()
+    eng.drain()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        eng.step()
+    e1.record()
+    torch.cuda.synchronize()
+    eng.drain()
+    eng.close()
+    return steps / (e0.elapsed_time(e1) / 1000.0)
 
 
 def cpu_baseline_sample(args, cfg):
     try:
-        return cpu_reference(cfg, budget_s=args.cpu_budget)
+        out = cpu_reference(cfg)
+        try:
+            g = c1_gpu_rate()
+            c1 = out["measured_c1"]
+            c1["gpu_view_steps_s"] = round(g, 1)
+            c1["gpu_over_cpu_measured"] = round(g * c1["full_iteration_s"], 1)
+        except Exception as e:  # the GPU c1 rate is an extra
+            out["measured_c1"]["gpu_error"] = repr(e)
+        return out
     except Exception as e:  # never fail the GPU line because of the baseline
         return {"value": None, "error": repr(e)}
 
@@ -859,23 +878,50 @@ def workload_config(args, cfg, world):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path (stock splattint from
+    baseline/_ref) on the host cores, on this arm's workload.  The scene is
+    generated and projected once and the process pool created once; a fixed
+    12k-pixel sample is split over the W + K steps (each step composites its
+    share of the sample); the K timed steps' per-pixel rate is extrapolated to a
+    full iteration with the factor measured at config 1 (one full stock
+    optimize_iteration, timed)."""
+    from oracle import refarm
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        vals.append(cpu_reference(cfg, budget_s=args.cpu_budget / max(1, args.steps + args.warmup)))
-    base = vals[args.warmup:]
-    value = float(np.mean([b["value"] for b in base]))
+    n_steps = args.warmup + args.steps
+    n_pixels = max(12000, 32 * n_steps)
+    c1 = refarm.measured_c1()
+    sampler = refarm.PixelSampler(cfg, n_pixels=n_pixels)
+    bounds = np.linspace(0, n_pixels, n_steps + 1).astype(int)
+    t_start = time.perf_counter()
+    timed = []
+    try:
+        for i in range(n_steps):
+            done, wall = sampler.time(int(bounds[i]), int(bounds[i + 1]))
+            if i >= args.warmup:
+                timed.append((done, wall))
+    finally:
+        sampler.close()
+    timed_s = time.perf_counter() - t_start
+    done = sum(d for d, _ in timed)
+    wall = sum(w for _, w in timed)
+    base = _cpu_line(sampler, done, wall, c1, cfg)
+    value = base["value"]
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args, cfg, world),
-        "cpu_baseline": {**base[-1], "value": value, "unit": UNIT},
+        "cpu_baseline": base,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "timing": {"extrapolated": True, "sample_pixels_timed": done,
+                   "sample_ms_per_step": round(1000.0 * wall / max(1, len(timed)), 1),
+                   "wall_s_all_steps": round(timed_s, 1),
+                   "note": "each step composites 1/(W+K) of a fixed pixel sample; ms_per_step is the "
+                           "extrapolated full-iteration time (not executed in full: hours of CPU)"},
     }))
 
 
@@ -886,7 +932,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-clocks", dest="clocks", action="store_false", help="skip NVML clock sampling")
     ap.add_argument("--no-extras", dest="extras", action="store_false",
@@ -897,10 +942,34 @@ def main():
     ap.add_argument("--no-profile", dest="profile", action="store_false",
                     help="skip the per-stage CUDA events inside the timed steps")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus, need_gpus=args.impl == "ours"))
     if args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
+
+
+def relaunch(n, need_gpus=True):
+    """`bench.py --gpus N` (N > 1) outside a launcher: re-run this command as N
+    ranks, one process per GPU over NCCL (torch.distributed.run on 127.0.0.1,
+    NCCL_DEBUG=INFO so the communicator setup is logged on stderr).  Rank 0
+    prints the JSON line."""
+    import socket
+    import subprocess
+    import torch
+    if need_gpus and os.environ.get("RCGS_DIST_BACKEND", "nccl") == "nccl" and torch.cuda.device_count() < n:
+        print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, found {torch.cuda.device_count()}"}))
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,COLL")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

@@ -97,6 +97,15 @@ int rcgs_view_kept(const rcgs_view* view, int64_t* d_index, double* d_depth, voi
 /* Tile bins: [start, end) into the pair list per 16x16 tile, row-major (tiles_y,
  * tiles_x, 2) uint32 (the reference's per-tile index lists, render.py binning). */
 int rcgs_view_ranges(const rcgs_view* view, uint32_t* d_ranges, void* stream);
+/* The binned pair list (n_pairs,) uint32: scene indices, sorted by (tile, depth
+ * rank); tile t's list is d_pair_g[ranges[t].start, ranges[t].end) -- the
+ * reference's global depth order (render.py:216) restricted to the gaussians
+ * whose opacity-aware footprint touches the tile (render.py:263-272). */
+int rcgs_view_pairs(const rcgs_view* view, uint32_t* d_pair_g, void* stream);
+/* Per kept gaussian in depth order, the fp64 operands of every exact decision
+ * (K,6): mean2d x, y, conic a, b, c and opacity (render.py:181-223), bit-identical
+ * to the reference's numpy values. */
+int rcgs_view_exact(const rcgs_view* view, double* d_out, void* stream);
 
 /* SH basis (K,16) fp64 along each kept gaussian's view direction and the channel
  * activation flags (K,3) uint8 from the last rcgs_view_color (ForwardCapture.basis /
@@ -210,6 +219,23 @@ int rcgs_adam_fused_next(const rcgs_scene* scene, float* d_sh, float* d_m, float
                          const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                          const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                          double* d_reject_record, rcgs_view* next_view, void* stream);
+/* Snapshot publication (optimize.py:221-238): when the step commits with a step
+ * count that is a multiple of `every`, the updated SH tiles are also written to
+ * d_snapshot (bulk stores from the same shared-memory tiles, no extra read) and
+ * the step count to *d_snapshot_step -- in stream order, exactly the
+ * post-step-k scene the reference publishes, with no host round trip. */
+typedef struct {
+    float* d_snapshot;          /* (N,16,3) fp32 published copy                  */
+    int64_t* d_snapshot_step;   /* step count of the published copy (may be NULL) */
+    int64_t every;              /* snapshot_every (> 0)                           */
+} rcgs_adam_publish;
+/* rcgs_adam_fused / rcgs_adam_fused_next (next_view may be NULL) with optional
+ * snapshot publication (publish may be NULL). */
+int rcgs_adam_fused_ex(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
+                       const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                       const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                       double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* publish,
+                       void* stream);
 /* Dense Adam on an explicit gradient (N,16,3) (adam_step API). */
 int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
                     const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,

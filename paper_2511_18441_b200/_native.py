@@ -42,6 +42,10 @@ class AdamConfig(ctypes.Structure):
                 ("beta2", c_double), ("eps", c_double)]
 
 
+class AdamPublish(ctypes.Structure):
+    _fields_ = [("d_snapshot", c_void_p), ("d_snapshot_step", c_void_p), ("every", c_i64)]
+
+
 class ViewInfo(ctypes.Structure):
     _fields_ = [("n_gaussians", c_i64), ("n_kept", c_i64), ("n_pairs", c_i64),
                 ("tiles_x", c_i32), ("tiles_y", c_i32), ("tile_size", c_i32), ("sort_bits", c_i32)]
@@ -57,6 +61,8 @@ _SIGNATURES = {
     "rcgs_view_destroy": [c_void_p, c_void_p],
     "rcgs_view_kept": [c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_view_ranges": [c_void_p, c_void_p, c_void_p],
+    "rcgs_view_pairs": [c_void_p, c_void_p, c_void_p],
+    "rcgs_view_exact": [c_void_p, c_void_p, c_void_p],
     "rcgs_view_color": [c_void_p, c_void_p, c_void_p],
     "rcgs_render": [c_void_p, P(ctypes.c_float), c_int, c_void_p, c_void_p, c_void_p],
     "rcgs_view_keep_records": [c_void_p, c_void_p],
@@ -72,6 +78,8 @@ _SIGNATURES = {
                         P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_adam_fused_next": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
                              P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "rcgs_adam_fused_ex": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
+                           P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, P(AdamPublish), c_void_p],
     "rcgs_adam_dense": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, P(AdamConfig), c_void_p,
                         c_void_p, c_void_p],
     "rcgs_nonfinite_check": [c_void_p, c_i64, c_void_p, c_void_p],

@@ -10,6 +10,8 @@
 // sequence of steps needs no host synchronisation.
 #include <math.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "shmath.cuh"
 
@@ -104,6 +106,23 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t byt
                  : "memory");
 }
 
+// The last block to finish (every block has read *step and *reject by then)
+// commits the step: advances the counter unless rejected, records the outcome and
+// re-arms the flag.  One thread per block.
+__device__ __forceinline__ void commit_step(unsigned* ticket, bool upd, int64_t* step, int32_t* reject,
+                                            double* reject_record, int64_t* snapshot_step, int64_t new_step) {
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+        if (upd) *step += 1;
+        if (snapshot_step) *snapshot_step = new_step;
+        *ticket = 0;
+        if (reject_record) {  // consume the flag: record it, re-arm it for the next step
+            *reject_record = upd ? 0.0 : 1.0;
+            if (reject) *reject = 0;
+        }
+    }
+}
+
 constexpr int kAG = 64;                     // gaussians per tile
 constexpr int kAThreads = 4 * kAG;          // 4 threads per gaussian, 12 coefficients each
 constexpr int kAStages = 2;                 // tiles in flight per CTA
@@ -125,11 +144,21 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
     float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
     unsigned* __restrict__ ticket, int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
-    Center next_cen, float4* __restrict__ next_color, double* __restrict__ reject_record) {
+    Center next_cen, float4* __restrict__ next_color, double* __restrict__ reject_record,
+    float* __restrict__ snapshot, int64_t* __restrict__ snapshot_step, int64_t snapshot_every) {
     // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
-    // colour epilogue the next view is still coloured from the unchanged SH
+    // colour epilogue the next view is still coloured from the unchanged SH.
+    // Every block still takes the last-block ticket, so the step commit (reject
+    // record + re-arming the flag) happens exactly once, after every block has
+    // read the flag.
     const bool upd = !(reject && *reject);
-    if (!upd && next_color == nullptr) return;
+    if (!upd && next_color == nullptr) {
+        if (threadIdx.x == 0) commit_step(ticket, upd, step, reject, reject_record, nullptr, 0);
+        return;
+    }
+    // publish: this step commits step count *step + 1; a multiple of the cadence
+    // also writes the updated tiles to the snapshot (optimize.py:221-222)
+    const bool snap = upd && snapshot != nullptr && snapshot_every > 0 && (*step + 1) % snapshot_every == 0;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kAStages * 3 * kATileBytes);
     const int t = threadIdx.x;
@@ -260,6 +289,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
             const uint32_t bytes = (uint32_t)ng * kARow;
 #pragma unroll
             for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
+            if (snap) bulk_store(snapshot + g0 * 48, smem_addr(stage_buf(s, 0)), bytes);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (t == 0) {
@@ -273,16 +303,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     }
     if (t == 0) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        // the last block to finish (every block has read *step by then) commits the step
-        __threadfence();
-        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
-            if (upd) *step += 1;
-            *ticket = 0;
-            if (reject_record) {  // consume the flag: record it, re-arm it for the next step
-                *reject_record = upd ? 0.0 : 1.0;
-                if (reject) *reject = 0;
-            }
-        }
+        commit_step(ticket, upd, step, reject, reject_record, snap ? snapshot_step : nullptr, *step + 1);
     }
 }
 
@@ -303,9 +324,13 @@ __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m
 }
 
 __global__ void step_commit_kernel(int32_t* __restrict__ reject, int64_t* __restrict__ step,
-                                   double* __restrict__ reject_record) {
+                                   double* __restrict__ reject_record, int64_t* __restrict__ snapshot_step = nullptr,
+                                   int64_t every = 0) {
     const bool rej = reject && *reject;
-    if (!rej) *step += 1;
+    if (!rej) {
+        *step += 1;
+        if (snapshot_step && every > 0 && *step % every == 0) *snapshot_step = *step;  // empty scene
+    }
     if (reject_record) {
         *reject_record = rej ? 1.0 : 0.0;
         if (reject) *reject = 0;
@@ -355,8 +380,12 @@ using namespace rcgs;
 static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
                            const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                            const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
-                           double* d_reject_record, rcgs_view* next_view, void* stream) {
+                           double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* pub,
+                           void* stream) {
     RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
+    RCGS_CHECK_ARG(pub == nullptr || (pub->d_snapshot != nullptr && pub->every > 0),
+                   "snapshot publication needs a buffer and a positive cadence");
+    RCGS_CHECK_ARG(next_view == nullptr || next_view->scene == sc, "next view belongs to another scene");
     RCGS_CHECK_ARG(n_views >= 1 && n_views <= kMaxViews, "views per step must be in [1, %d]", kMaxViews);
     RCGS_CHECK_ARG(sc->n < (int64_t)357913941, "scene too large for 32-bit Adam indexing");
     cudaStream_t s = as_stream(stream);
@@ -368,18 +397,26 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
         }
         static int grid = 0;
-        static unsigned* ticket = nullptr;  // last-block ticket (reset by the last block)
-        if (grid == 0) {
+        static std::once_flag once;
+        static int once_err = RCGS_OK;
+        std::call_once(once, [] {
             int dev = 0, sms = 0, per_sm = 0;
-            RCGS_CUDA(cudaGetDevice(&dev));
-            RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            RCGS_CUDA(cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kASmem));
-            RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem));
-            RCGS_CUDA(cudaMalloc(&ticket, sizeof(unsigned)));
-            RCGS_CUDA(cudaMemset(ticket, 0, sizeof(unsigned)));
+            if (cudaGetDevice(&dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kASmem) !=
+                    cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem) !=
+                    cudaSuccess) {
+                once_err = RCGS_ECUDA;
+                return;
+            }
             grid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
-        }
+        });
+        RCGS_CHECK_ARG(once_err == RCGS_OK && grid > 0, "adam launch setup failed");
+        // last-block ticket, one per stream: concurrent launches on different streams
+        // must not mix their counts (reset by the last block of each launch)
+        unsigned* ticket = stream_ticket(s);
+        RCGS_CHECK_ARG(ticket != nullptr, "adam ticket allocation failed");
         const int64_t ntiles = (sc->n + kAG - 1) / kAG;
         Center nc = {{0.0, 0.0, 0.0}};
         const int32_t* nrank = nullptr;
@@ -392,11 +429,13 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
         // bias corrections from and commit of the device step counter happen inside
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
             sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
-            d_reject, nrank, nc, ncolor, d_reject_record);
+            d_reject, nrank, nc, ncolor, d_reject_record, pub ? pub->d_snapshot : nullptr,
+            pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0);
         RCGS_LAUNCH_CHECK();
         return RCGS_OK;
     }
-    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step, d_reject_record);
+    step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step, d_reject_record, pub ? pub->d_snapshot_step : nullptr,
+                                       pub ? pub->every : 0);
     RCGS_LAUNCH_CHECK();
     return RCGS_OK;
 }
@@ -406,7 +445,16 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
                                const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                                double* d_reject_record, void* stream) {
     return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
-                           d_reject_record, nullptr, stream);
+                           d_reject_record, nullptr, nullptr, stream);
+}
+
+extern "C" int rcgs_adam_fused_ex(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
+                                  const float* const* h_d_accs, const double* h_centers, int32_t n_views,
+                                  const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
+                                  double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* publish,
+                                  void* stream) {
+    return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
+                           d_reject_record, next_view, publish, stream);
 }
 
 extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
@@ -416,7 +464,7 @@ extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_
     RCGS_CHECK_ARG(next_view != nullptr, "null next view");
     RCGS_CHECK_ARG(next_view->scene == sc, "next view belongs to another scene");
     return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
-                           d_reject_record, next_view, stream);
+                           d_reject_record, next_view, nullptr, stream);
 }
 
 extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,

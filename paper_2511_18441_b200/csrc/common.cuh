@@ -88,6 +88,10 @@ void dfree(T*& p, cudaStream_t s) {
 // allocations do not map new physical memory on the timed path.
 int pool_reserve(int64_t bytes, cudaStream_t s);
 
+// A zeroed device counter owned by stream `s` (created on first use, never freed),
+// for last-block tickets: launches on different streams never share one.
+unsigned* stream_ticket(cudaStream_t s);
+
 // Pinned scratch for small device->host readbacks (per thread).
 void* pinned_scratch(size_t bytes);
 

@@ -437,7 +437,10 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                 continue;
             }
             const T fy = fyv[i], fg = fgv[i];
-            const double sgn = fy > fg ? 1.0 : (fy < fg ? -1.0 : 0.0);
+            // np.sign(y - gt): NaN propagates (a NaN image or target makes the
+            // gradient non-finite, so the step is rejected, optimize.py:72-74)
+            const double d = (double)fy - (double)fg;
+            const double sgn = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == 0.0 ? 0.0 : d));
             double out = (1.0 - lam) * sgn / n;
             if (SSIM) out -= lam * ((f[0][i] + 2.0 * (double)fy * f[1][i] + (double)fg * f[2][i]) / n);
             grad[o] = (G)out;
@@ -465,7 +468,7 @@ using namespace rcgs;
 // Per-stream zeroed ticket for pass A's tail reduction (the last block resets it, so
 // it is zero again for the next launch on that stream; launches on one stream are
 // ordered, on different streams they use different tickets).
-static unsigned* stream_ticket(cudaStream_t s) {
+unsigned* rcgs::stream_ticket(cudaStream_t s) {
     static std::mutex mu;
     static std::unordered_map<cudaStream_t, unsigned*> tickets;
     std::lock_guard<std::mutex> lock(mu);

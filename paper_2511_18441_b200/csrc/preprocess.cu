@@ -54,7 +54,14 @@ __device__ __forceinline__ ProjF64 project_one(const double* __restrict__ pos,
     // mean2d = fx * x / z + cx (render.py:182), evaluated left to right, unfused
     p.mx = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fx, x), z), cam.cx);
     p.my = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fy, y), z), cam.cy);
-    // EWA Jacobian and cov2d = (J W) Sigma (J W)^T + dilation (render.py:184-194)
+    // EWA Jacobian and cov2d = (J W) Sigma (J W)^T + dilation (render.py:184-194),
+    // with numpy's exact operation sequence (every op explicitly rounded: nvcc
+    // would otherwise contract * + into FMAs), restated in oracle/c/rcgs_oracle.c:
+    //   jac entries: plain ops;
+    //   t = jac @ R: the stacked matmul runs through OpenBLAS dgemm, the fused chain
+    //     fma(a2, b2, fma(a1, b1, a0 * b0)) with jac's structural zeros multiplied in;
+    //   cov2 = einsum("nij,njk,nlk->nil", t, S, t): sum over j (outer), k (inner)
+    //     of (t_ij * S_jk) * t_lk, accumulated left to right.
     const double zz = __dmul_rn(z, z);
     const double j00 = __ddiv_rn(cam.fx, z);
     const double j02 = __ddiv_rn(__dmul_rn(-cam.fx, x), zz);
@@ -64,21 +71,22 @@ __device__ __forceinline__ ProjF64 project_one(const double* __restrict__ pos,
     double t0[3], t1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        t0[k] = j00 * R[0 * 3 + k] + j02 * R[2 * 3 + k];
-        t1[k] = j11 * R[1 * 3 + k] + j12 * R[2 * 3 + k];
+        t0[k] = __fma_rn(j02, R[6 + k], __fma_rn(0.0, R[3 + k], __dmul_rn(j00, R[k])));
+        t1[k] = __fma_rn(j12, R[6 + k], __fma_rn(j11, R[3 + k], __dmul_rn(0.0, R[k])));
     }
-    const double* S = cov3d + 6 * g;  // xx xy xz yy yz zz
-    const double s00 = S[0], s01 = S[1], s02 = S[2], s11 = S[3], s12 = S[4], s22 = S[5];
-    double u0[3], u1[3];  // Sigma t^T rows
-    u0[0] = s00 * t0[0] + s01 * t0[1] + s02 * t0[2];
-    u0[1] = s01 * t0[0] + s11 * t0[1] + s12 * t0[2];
-    u0[2] = s02 * t0[0] + s12 * t0[1] + s22 * t0[2];
-    u1[0] = s00 * t1[0] + s01 * t1[1] + s02 * t1[2];
-    u1[1] = s01 * t1[0] + s11 * t1[1] + s12 * t1[2];
-    u1[2] = s02 * t1[0] + s12 * t1[1] + s22 * t1[2];
-    const double a = t0[0] * u0[0] + t0[1] * u0[1] + t0[2] * u0[2] + cfg.covariance_dilation;
-    const double b = t0[0] * u1[0] + t0[1] * u1[1] + t0[2] * u1[2];
-    const double c = t1[0] * u1[0] + t1[1] * u1[1] + t1[2] * u1[2] + cfg.covariance_dilation;
+    const double* S6 = cov3d + 6 * g;  // xx xy xz yy yz zz
+    const double S[3][3] = {{S6[0], S6[1], S6[2]}, {S6[1], S6[3], S6[4]}, {S6[2], S6[4], S6[5]}};
+    auto quad = [&](const double* ti, const double* tl) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(ti[j], S[j][k]), tl[k]));
+        return acc;
+    };
+    const double a = __dadd_rn(quad(t0, t0), cfg.covariance_dilation);
+    const double b = quad(t0, t1);
+    const double c = __dadd_rn(quad(t1, t1), cfg.covariance_dilation);
     // det, lambda_max, 3-sigma radius and viewport test (render.py:196-205), unfused
     const double det = __dsub_rn(__dmul_rn(a, c), __dmul_rn(b, b));
     const double mid = __dmul_rn(0.5, __dadd_rn(a, c));
@@ -100,27 +108,31 @@ __global__ void cov3d_kernel(const double* __restrict__ rot, const double* __res
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const double w = rot[4 * g], x = rot[4 * g + 1], y = rot[4 * g + 2], z = rot[4 * g + 3];
-    // quaternion_to_rotation (scene.py:98-112)
+    // quaternion_to_rotation (scene.py:98-112) and m = R diag(s): elementwise numpy
+    // ops, each explicitly rounded (no FMA contraction); then m @ m^T, which numpy
+    // runs through OpenBLAS dgemm: the fused chain (oracle/c/rcgs_oracle.c)
+    auto sq2 = [](double p, double q) { return __dadd_rn(__dmul_rn(p, p), __dmul_rn(q, q)); };
     double r[3][3];
-    r[0][0] = 1 - 2 * (y * y + z * z);
-    r[0][1] = 2 * (x * y - w * z);
-    r[0][2] = 2 * (x * z + w * y);
-    r[1][0] = 2 * (x * y + w * z);
-    r[1][1] = 1 - 2 * (x * x + z * z);
-    r[1][2] = 2 * (y * z - w * x);
-    r[2][0] = 2 * (x * z - w * y);
-    r[2][1] = 2 * (y * z + w * x);
-    r[2][2] = 1 - 2 * (x * x + y * y);
+    r[0][0] = __dsub_rn(1.0, __dmul_rn(2.0, sq2(y, z)));
+    r[0][1] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+    r[0][2] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+    r[1][0] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+    r[1][1] = __dsub_rn(1.0, __dmul_rn(2.0, sq2(x, z)));
+    r[1][2] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+    r[2][0] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+    r[2][1] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+    r[2][2] = __dsub_rn(1.0, __dmul_rn(2.0, sq2(x, y)));
     double m[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) m[i][j] = r[i][j] * scale[3 * g + j];
+        for (int j = 0; j < 3; ++j) m[i][j] = __dmul_rn(r[i][j], scale[3 * g + j]);
     double s[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) s[i][j] = m[i][0] * m[j][0] + m[i][1] * m[j][1] + m[i][2] * m[j][2];
+        for (int j = 0; j < 3; ++j)
+            s[i][j] = __fma_rn(m[i][2], m[j][2], __fma_rn(m[i][1], m[j][1], __dmul_rn(m[i][0], m[j][0])));
     double* o = cov + 6 * g;
     o[0] = s[0][0];
     o[1] = s[0][1];
@@ -745,6 +757,36 @@ extern "C" int rcgs_view_kept(const rcgs_view* v, int64_t* d_index, double* d_de
     if (v->k == 0) return RCGS_OK;
     kept_export_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->gid, v->z, v->k, d_index, d_depth);
     RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+__global__ void exact_export_kernel(const uint32_t* __restrict__ gid, const ExactRec* __restrict__ exact, int64_t k,
+                                    double* __restrict__ out) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    const ExactRec e = exact[gid[s]];
+    double* o = out + 6 * s;
+    o[0] = e.mx;
+    o[1] = e.my;
+    o[2] = e.ca;
+    o[3] = e.cb;
+    o[4] = e.cc;
+    o[5] = e.op;
+}
+
+extern "C" int rcgs_view_exact(const rcgs_view* v, double* d_out, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_out != nullptr, "null argument");
+    if (v->k == 0) return RCGS_OK;
+    exact_export_kernel<<<div_up(v->k, 256), 256, 0, as_stream(stream)>>>(v->gid, v->exact, v->k, d_out);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+}
+
+extern "C" int rcgs_view_pairs(const rcgs_view* v, uint32_t* d_pair_g, void* stream) {
+    RCGS_CHECK_ARG(v != nullptr && d_pair_g != nullptr, "null argument");
+    if (v->pairs == 0) return RCGS_OK;
+    RCGS_CUDA(cudaMemcpyAsync(d_pair_g, v->pair_g, sizeof(uint32_t) * (size_t)v->pairs, cudaMemcpyDeviceToDevice,
+                              as_stream(stream)));
     return RCGS_OK;
 }
 

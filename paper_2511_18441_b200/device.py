@@ -246,6 +246,20 @@ class View:
             N.call("rcgs_view_ranges", self.handle, N.ptr(out), stream_ptr())
         return out
 
+    def pairs(self) -> torch.Tensor:
+        """The binned pair list: scene indices sorted by (tile, depth rank)."""
+        out = torch.zeros(max(self.n_pairs, 1), dtype=torch.int32, device=device())
+        if self.n_pairs:
+            N.call("rcgs_view_pairs", self.handle, N.ptr(out), stream_ptr())
+        return out[:self.n_pairs]
+
+    def exact(self) -> torch.Tensor:
+        """(K, 6) fp64 mean2d x, y, conic a, b, c, opacity of the kept gaussians in depth order."""
+        out = torch.zeros((max(self.n_kept, 1), 6), dtype=torch.float64, device=device())
+        if self.n_kept:
+            N.call("rcgs_view_exact", self.handle, N.ptr(out), stream_ptr())
+        return out[:self.n_kept]
+
     def backward(self, grad_image: torch.Tensor, acc=None, nonfinite=None) -> torch.Tensor:
         self._need_color()
         if tuple(grad_image.shape) != (self.height, self.width, 3):

@@ -36,6 +36,20 @@ from . import parallel
 from .render import DEFAULT_CONFIG
 
 
+def cameras_equal(a, b) -> bool:
+    """Value equality of [(intrinsics, pose)] lists (poses hold numpy arrays, whose
+    dataclass __eq__ would raise)."""
+    if len(a) != len(b):
+        return False
+    for (ia, pa), (ib, pb) in zip(a, b):
+        if (ia.fx, ia.fy, ia.cx, ia.cy, ia.width, ia.height) != (ib.fx, ib.fy, ib.cx, ib.cy, ib.width, ib.height):
+            return False
+        if not (np.array_equal(np.asarray(pa.rotation), np.asarray(pb.rotation))
+                and np.array_equal(np.asarray(pa.translation), np.asarray(pb.translation))):
+            return False
+    return True
+
+
 class ViewPrefetcher:
     """Builds the views of upcoming steps on side streams from worker threads.
 
@@ -96,6 +110,16 @@ class ViewPrefetcher:
         for t in self.threads:
             t.start()
 
+    def set_dataset(self, cameras, targets) -> None:
+        """New cameras / targets for builds submitted from now on (no job may be
+        in flight: the engine takes every prefetched step first)."""
+        host = targets if targets is not None and any(not t.is_cuda for t in targets) else None
+        with self.cv:
+            self.cameras = cameras
+            if host is not None and not self.copy_streams:
+                self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in range(len(self.streams))]
+            self.targets = host
+
     def submit(self, key, index):
         with self.cv:
             self.jobs.append((key, index))
@@ -149,11 +173,13 @@ class ViewPrefetcher:
                     continue
                 key, index = job
                 try:
-                    intr, pose = self.cameras[index]
+                    with self.cv:
+                        intr, pose = self.cameras[index]
+                        targets = self.targets
                     tgt, copied = None, None
-                    if self.targets is not None:
+                    if targets is not None:
                         # the upload runs on its own stream, concurrently with the build
-                        src = self.targets[index]
+                        src = targets[index]
                         slot = key % len(self.ring)
                         with self.cv:
                             free = self.ring_free[slot]
@@ -256,6 +282,28 @@ class RefitEngine:
         # with prefetching, Adam also colours the next step's view (rcgs_adam_fused_next)
         self.fuse_color = fuse_color and os.environ.get("RCGS_FUSE_COLOR", "1") != "0"
         self._held = None
+        self._undo = {}  # key -> how to undo the draw of a step taken ahead (reset_ahead)
+        # snapshot publication inside Adam (enable_snapshots): the post-step SH of
+        # every step whose count is a multiple of `every`, written in stream order
+        self._publish = None
+        self.snapshot_sh = None
+        self.snapshot_step = None
+
+    def enable_snapshots(self, every: int) -> None:
+        """Have every Adam step whose committed count is a multiple of `every`
+        also write the updated SH to `snapshot_sh` (and the count to
+        `snapshot_step`) in stream order: the reference's publication of the
+        post-step scene (optimize.py:221-222, 226-238) with no host round trip."""
+        if every <= 0:
+            raise ValueError("snapshot cadence must be positive")
+        self.snapshot_sh = self.sh.clone()
+        self.snapshot_step = self.step_dev.clone()
+        self._publish = N.AdamPublish(self.snapshot_sh.data_ptr(), self.snapshot_step.data_ptr(), int(every))
+
+    def publish_now(self) -> None:
+        """Copy the current SH and step count into the snapshot (on the current stream)."""
+        self.snapshot_sh.copy_(self.sh)
+        self.snapshot_step.copy_(self.step_dev)
 
     def close(self):
         if self._held is not None:
@@ -289,10 +337,63 @@ class RefitEngine:
     def draw(self):
         """View indices of the next step from the reference RNG stream (optimize.py:106)
         -- after any picks restored by `load_state` that were drawn before it."""
+        return self._draw()[0]
+
+    def _draw(self):
+        """(picks, undo): undo restores the RNG / replay queue to before this draw."""
         replay = getattr(self, "_replay", None)
         if replay:
-            return replay.popleft()
-        return parallel.draw_views(self.rng, len(self.cameras), self.world)
+            return replay.popleft(), ("replay", None)
+        state = self.rng.bit_generator.state
+        return parallel.draw_views(self.rng, len(self.cameras), self.world), ("rng", state)
+
+    def reset_ahead(self) -> None:
+        """Discard the steps drawn ahead by the prefetcher (their views are built,
+        not executed) and undo their draws, so the next step draws again from the
+        RNG state after the last executed step.  Used by dataset swaps, which the
+        reference applies from the next iteration on (optimize.py:173-175, 211-214)."""
+        if self._pf is None:
+            return
+        taken = []
+        if self._held is not None:
+            picks, view, _, key, _ = self._held
+            self._held = None
+            self._pf.retire(view, key)
+            taken.append((key, picks))
+        while self._future:
+            key, picks = self._future.popleft()
+            view, ev, _ = self._pf.take(key)
+            torch.cuda.current_stream().wait_event(ev)
+            self._pf.retire(view, key)
+            taken.append((key, picks))
+        taken.sort()
+        replayed = []
+        first_rng = None
+        for key, picks in taken:
+            kind, state = self._undo.pop(key)
+            if kind == "replay":
+                replayed.append(list(picks))
+            elif first_rng is None:
+                first_rng = state
+        if first_rng is not None:
+            self.rng.bit_generator.state = first_rng
+        if replayed:
+            self._replay = collections.deque(replayed + list(getattr(self, "_replay", ())))
+
+    def set_dataset(self, cameras, targets) -> None:
+        """Swap the views' targets (and cameras, if they differ) from the next step on."""
+        self.reset_ahead()
+        cameras = list(cameras)
+        if not cameras_equal(cameras, self.cameras):
+            for v in self.views:
+                if v is not None:
+                    v.close()
+            self.cameras = cameras
+            self.views = [None] * len(cameras)
+            self._centers = [D.camera_center(p) for _, p in cameras]
+        self.targets = targets
+        if self._pf is not None:
+            self._pf.set_dataset(self.cameras, targets)
 
     # -- optimizer state (checkpoint / resume) -------------------------------------
     def state_dict(self) -> dict:
@@ -335,8 +436,9 @@ class RefitEngine:
 
     def _take_prefetched(self):
         while len(self._future) < self.prefetch:
-            picks = self.draw()
+            picks, undo = self._draw()
             key = self._seq
+            self._undo[key] = undo
             self._seq += 1
             self._pf.submit(key, picks[self.rank] if self.world > 1 else picks[0])
             self._future.append((key, picks))
@@ -400,6 +502,7 @@ class RefitEngine:
         args = (self.dscene.handle, N.ptr(self.sh), N.ptr(self.m), N.ptr(self.v), ptrs,
                 (ctypes.c_double * len(cen))(*cen), len(accs), ctypes.byref(self._adam_cfg),
                 N.ptr(self.reject), N.ptr(self.step_dev), N.ptr(rec[3:4]))
+        pub = ctypes.byref(self._publish) if self._publish is not None else None
         if prefetched and self.fuse_color:
             # take the next step's view now (its build was submitted `prefetch`
             # steps ago; the stream waits for it before the Adam stage event) and
@@ -407,18 +510,20 @@ class RefitEngine:
             nxt_picks, nxt, nxt_key, nxt_tgt = self._take_prefetched()
             if ev:
                 ev[5].record()
-            N.call("rcgs_adam_fused_next", *args, nxt.handle, D.stream_ptr())  # also records + re-arms reject
+            # also records + re-arms the reject flag, and publishes snapshots
+            N.call("rcgs_adam_fused_ex", *args, nxt.handle, pub, D.stream_ptr())
             nxt._colored = True
             self._held = (nxt_picks, nxt, True, nxt_key, nxt_tgt)
         else:
             if ev:
                 ev[5].record()
-            N.call("rcgs_adam_fused", *args, D.stream_ptr())
+            N.call("rcgs_adam_fused_ex", *args, None, pub, D.stream_ptr())
         if ev:
             ev[6].record()
             self._prof.append((ev, coloured))
         self.pending.append((picks, generation))
         if prefetched:
+            self._undo.pop(key, None)
             self._pf.retire(view, key)
         elif not self.cache_views:
             view.close()

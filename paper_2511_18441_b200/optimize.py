@@ -32,6 +32,14 @@ from .render import DEFAULT_CONFIG
 log = logging.getLogger(__name__)
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 @dataclass(frozen=True)
 class OptimizerConfig:
     lr_dc: float = 0.0025
@@ -152,7 +160,15 @@ class BackgroundOptimizer:
         self._config = config
         self._scene0 = scene
         self._metrics_sink = metrics_sink
-        self._lock = threading.Lock()
+        # _lock guards the published state (re-entrant: _flush publishes under it);
+        # _flush_lock serialises metric drains (worker and save_state); _step_lock is
+        # held by whoever is enqueueing a step, so save_state / load_state / swaps
+        # see the engine at a step boundary
+        self._lock = threading.RLock()
+        self._flush_lock = threading.RLock()
+        self._step_lock = threading.Lock()
+        self._cache_lock = threading.Lock()  # materialised snapshot / current scene caches
+        self._exec_stream = None  # the stream the steps run on (worker or caller)
         self._dataset = dataset
         self._stream_targets = stream_targets
         self._raster = raster
@@ -165,13 +181,14 @@ class BackgroundOptimizer:
                                    self._targets(dataset), config, seed=seed,
                                    cache_views=cache_views, group=group, raster=raster,
                                    prefetch=prefetch)
+        # Adam publishes the post-step SH of every snapshot_every-th step into the
+        # engine's snapshot buffer, in stream order (optimize.py:221-222)
+        self._engine.enable_snapshots(config.snapshot_every)
         self._pending_dataset = None
         self._accepted = 0
-        self._snapshot_sh = self._sh0.clone()
         self._sh_base = None  # fp64 host SH on the device, uploaded on the first save_ply
-        self._snapshot_cache = (None, None)
-        self._current_cache = (None, None)
-        self._version = 0
+        self._snapshot_cache = (None, None)  # (published step count, Scene)
+        self._current_cache = (None, None)   # (step count, Scene)
         self._status = OptimizerStatus(0, 0.0, 0.0, dataset.generation)
         self._run_event = threading.Event()
         self._run_event.set()
@@ -183,6 +200,17 @@ class BackgroundOptimizer:
 
     # -- dataset plumbing -------------------------------------------------------
     @staticmethod
+    def _view_ids(dataset):
+        ids = getattr(dataset, "_rcgs_view_ids", None)
+        if ids is None:
+            ids = tuple(ev.view.view_id for ev in dataset.views)
+            try:  # cached on the (frozen) dataset object
+                object.__setattr__(dataset, "_rcgs_view_ids", ids)
+            except Exception:
+                pass
+        return ids
+
+    @staticmethod
     def _cameras(dataset):
         return [(ev.view.intrinsics, ev.view.pose) for ev in dataset.views]
 
@@ -193,40 +221,53 @@ class BackgroundOptimizer:
         return [D.to_device(ev.image) for ev in dataset.views]
 
     def _apply_pending_dataset(self):
+        """Swap in the dataset passed to swap_dataset (the reference reads it at
+        the start of the next iteration, optimize.py:211-214).  Steps the
+        prefetcher drew ahead are discarded and redrawn, so the next step samples
+        the new dataset from the RNG state after the last executed step and
+        fits its targets."""
         with self._lock:
             ds, self._pending_dataset = self._pending_dataset, None
         if ds is None:
             return
         if len(ds) == 0:
             raise ValidationError("dataset has no views")
-        eng = self._engine
-        same = self._cameras(ds) == eng.cameras
-        eng.targets = self._targets(ds)
-        if not same:
-            if eng._pf is not None:
-                raise ValidationError("swap_dataset with different cameras needs prefetch=0")
-            eng.cameras = self._cameras(ds)
-            eng.views = [None] * len(eng.cameras)
-            eng._centers = [D.camera_center(p) for _, p in eng.cameras]
+        self._engine.set_dataset(self._cameras(ds), self._targets(ds))
         with self._lock:
             self._dataset = ds
 
     # -- state shared with other threads ------------------------------------------
-    def _materialise(self, sh_dev, cache_name):
-        ver, sc = getattr(self, cache_name)
-        if ver == self._version and sc is not None:
+    def _read_device(self, sh_dev, step_dev):
+        """Consistent copy of (SH, step count) at a step boundary: one copy each,
+        enqueued on the stream the steps run on (Adam is the only writer and is a
+        single kernel on that stream), then waited for."""
+        stream = self._exec_stream or torch.cuda.current_stream()
+        with self._step_lock, torch.cuda.stream(stream):  # no Adam enqueued between the two copies
+            sh = sh_dev.clone()
+            step = step_dev.clone()
+            done = torch.cuda.Event()
+            done.record(stream)
+        done.synchronize()
+        return sh, int(step.item())
+
+    def _materialise(self, sh_dev, step_dev, cache_name):
+        # lock order: _step_lock (in _read_device) is never taken under _lock
+        sh, step = self._read_device(sh_dev, step_dev)
+        with self._cache_lock:
+            ver, sc = getattr(self, cache_name)
+            if ver == step and sc is not None:
+                return sc
+            sc = self._scene0.with_sh(_delta_to_host(self._scene0.sh, self._sh0, sh))
+            setattr(self, cache_name, (step, sc))
             return sc
-        sc = self._scene0.with_sh(_delta_to_host(self._scene0.sh, self._sh0, sh_dev))
-        setattr(self, cache_name, (self._version, sc))
-        return sc
 
     def snapshot(self):
-        with self._lock:
-            return self._materialise(self._snapshot_sh, "_snapshot_cache")
+        """The scene published after the last step whose count is a multiple of
+        snapshot_every (optimize.py:164-166, 226-230)."""
+        return self._materialise(self._engine.snapshot_sh, self._engine.snapshot_step, "_snapshot_cache")
 
     def current_scene(self):
-        with self._lock:
-            return self._materialise(self._engine.sh, "_current_cache")
+        return self._materialise(self._engine.sh, self._engine.step_dev, "_current_cache")
 
     def save_ply(self, path) -> None:
         """Checkpoint of the current SH (session.py:328-333 saves current_scene()
@@ -234,10 +275,11 @@ class BackgroundOptimizer:
         byte-identical to save_scene_ply(self.current_scene())."""
         from .scene_io import save_scene_ply_device
 
-        with self._lock:
+        sh, _ = self._read_device(self._engine.sh, self._engine.step_dev)
+        with self._cache_lock:
             if self._sh_base is None:
                 self._sh_base = torch.from_numpy(np.ascontiguousarray(self._scene0.sh)).to(self._sh0.device)
-            save_scene_ply_device(self._scene0, self._engine.sh, path, sh_base=(self._sh_base, self._sh0))
+            save_scene_ply_device(self._scene0, sh, path, sh_base=(self._sh_base, self._sh0))
 
     def save_state(self, path) -> None:
         """Optimizer checkpoint for an exact resume (an extension; the reference
@@ -247,11 +289,13 @@ class BackgroundOptimizer:
         import json
         if self._thread is not None and not self.paused:
             raise ValidationError("save_state needs a paused or synchronous optimizer")
-        with self._lock:
-            self._flush()
-            st = self._engine.state_dict()
-            meta = {"rng": st["rng"], "ahead": st["ahead"], "step": st["step"], "accepted": self._accepted,
-                    "n": int(st["sh"].shape[0])}
+        with self._step_lock:  # waits for a step the worker was enqueueing at pause()
+            with self._exec_ctx():
+                self._flush()
+                st = self._engine.state_dict()
+            with self._lock:
+                meta = {"rng": st["rng"], "ahead": st["ahead"], "step": st["step"], "accepted": self._accepted,
+                        "n": int(st["sh"].shape[0])}
         np.savez(path, sh=st["sh"], m=st["m"], v=st["v"], meta=np.array(json.dumps(meta)))
 
     def load_state(self, path) -> None:
@@ -265,12 +309,13 @@ class BackgroundOptimizer:
             meta = json.loads(str(z["meta"]))
             st = {"sh": z["sh"], "m": z["m"], "v": z["v"], "step": meta["step"], "rng": meta["rng"],
                   "ahead": meta["ahead"]}
-        with self._lock:
+        with self._step_lock, self._lock, self._cache_lock:
             self._engine.load_state_dict(st)
             self._accepted = int(meta["accepted"])
-            self._snapshot_sh.copy_(self._engine.sh)  # the published snapshot is the restored SH
+            self._engine.publish_now()  # the published snapshot is the restored SH
+            torch.cuda.current_stream().synchronize()
             self._snapshot_cache = (None, None)
-            self._version += 1
+            self._current_cache = (None, None)
 
     def status(self) -> OptimizerStatus:
         with self._lock:
@@ -315,54 +360,65 @@ class BackgroundOptimizer:
         return self._stop_event.is_set()
 
     # -- the loop -----------------------------------------------------------------------
+    def _exec_ctx(self):
+        return torch.cuda.stream(self._exec_stream) if self._exec_stream is not None else _nullctx()
+
     def _step(self) -> None:
-        self._apply_pending_dataset()
-        with self._lock:
-            gen = self._dataset.generation
-        self._engine.step(generation=gen)
+        with self._step_lock:
+            self._apply_pending_dataset()
+            with self._lock:
+                # the step's generation and the dataset's view ids travel with its
+                # metrics (drained later, possibly after a swap)
+                tag = (self._dataset.generation, self._view_ids(self._dataset))
+            self._engine.step(generation=tag)
         self._window_iters += 1
-        with self._lock:
-            self._version += 1
         if len(self._engine.pending) >= min(self._config.snapshot_every, self._engine.max_pending):
             # non-blocking: starts the metrics read-back of the pending steps and
             # delivers the ones already landed (every step's metrics still reach the
             # sink, in order, one flush later) -- a blocking flush here drained the
-            # whole step pipeline every `snapshot_every` iterations
+            # whole step pipeline every `snapshot_every` iterations.  The snapshot
+            # itself is published by the step's own Adam on the device.
             self._flush(wait=False)
 
     def _flush(self, wait: bool = True) -> None:
-        recs = self._engine.drain(wait)
-        lines = []
-        for picks, gen, l1, ss, total, rejected in recs:
-            it = self._accepted + 1
-            if rejected:
-                log.warning("non-finite gradient; Adam iteration %d rejected", it)
-            else:
-                self._accepted += 1
-            self._last_loss = total
-            vid = self._dataset.views[picks[self._engine.rank]].view.view_id
-            lines.append(IterationMetrics(iteration=it, view_id=vid, generation=gen,
-                                          loss=LossBreakdown(l1, ss, total, self._config.lam)))
-            if not rejected and self._accepted % self._config.snapshot_every == 0:
-                self._publish()
-        if self._metrics_sink is not None:
-            for m in lines:
-                self._metrics_sink(m)
+        with self._flush_lock:
+            recs = self._engine.drain(wait)
+            lines = []
+            for picks, (gen, ids), l1, ss, total, rejected in recs:
+                it = self._accepted + 1
+                if rejected:
+                    log.warning("non-finite gradient; Adam iteration %d rejected", it)
+                else:
+                    self._accepted += 1
+                self._last_loss = total
+                vid = ids[picks[self._engine.rank]]
+                lines.append(IterationMetrics(iteration=it, view_id=vid, generation=gen,
+                                              loss=LossBreakdown(l1, ss, total, self._config.lam)))
+                if not rejected and self._accepted % self._config.snapshot_every == 0:
+                    self._publish_status()
+            if self._metrics_sink is not None:
+                for m in lines:
+                    self._metrics_sink(m)
 
-    def _publish(self) -> None:
+    def _publish_status(self) -> None:
         now = time.perf_counter()
         elapsed = max(now - self._window_start, 1e-9)
         with self._lock:
-            self._snapshot_sh.copy_(self._engine.sh)
-            self._snapshot_cache = (None, None)
             self._status = OptimizerStatus(iteration=self._accepted, loss=self._last_loss,
                                            ips=self._window_iters / elapsed,
                                            generation=self._dataset.generation)
         self._window_start = now
         self._window_iters = 0
 
+    def _publish(self) -> None:
+        """Publish the current scene now (run_iterations' final publish)."""
+        with self._lock:
+            self._engine.publish_now()
+        self._publish_status()
+
     def _loop(self) -> None:
         stream = torch.cuda.Stream()
+        self._exec_stream = stream
         with torch.cuda.stream(stream):
             while not self._stop_event.is_set():
                 if not self._run_event.wait(timeout=0.1):
@@ -381,6 +437,7 @@ class BackgroundOptimizer:
         """Deterministic synchronous mode; returns the final scene."""
         if self._thread is not None:
             raise ValidationError("run_iterations cannot be mixed with a started worker")
+        self._exec_stream = torch.cuda.current_stream()
         for _ in range(count):
             self._step()
         self._flush()

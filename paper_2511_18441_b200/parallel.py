@@ -75,8 +75,34 @@ def any_rank(flag: torch.Tensor, group) -> torch.Tensor:
 
 
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:
-    """Round-robin static view shard of this rank (selection pass)."""
-    return list(range(rank, n_views, world))
+    """Static contiguous view block of this rank (selection pass): rank r gets
+    views [r V / G, (r + 1) V / G) (rounded), so the blocks can be all-gathered."""
+    lo = (rank * n_views) // world
+    hi = ((rank + 1) * n_views) // world
+    return list(range(lo, hi))
+
+
+def replicate_views(stack: torch.Tensor, mine: list[int], group) -> None:
+    """Every rank ends with every row of `stack` (V, ...) when each rank computed
+    the rows of its `shard_views` block: one all-gather when the blocks are equal
+    (V divisible by the world size), else one broadcast per row from its owner."""
+    world, rank = world_of(group)
+    if world == 1:
+        return
+    n = stack.shape[0]
+    owners = [r for r in range(world) for _ in shard_views(n, r, world)]
+    if n % world == 0 and stack.is_cuda and not _host_staged(group):
+        blk = n // world
+        src = stack[rank * blk:(rank + 1) * blk].clone()
+        dist.all_gather_into_tensor(stack, src, group=group)
+        return
+    for i in range(n):
+        if stack.is_cuda and _host_staged(group):
+            h = stack[i].cpu()
+            dist.broadcast(h, src=owners[i], group=group)
+            stack[i].copy_(h)
+        else:
+            dist.broadcast(stack[i], src=owners[i], group=group)
 
 
 def reduce_counts(group, *tensors: torch.Tensor) -> None:

@@ -69,8 +69,14 @@ def _worker(rank, world, port, queue):
         hits = torch.tensor([rank + 1, 10 * (rank + 1), 0], dtype=torch.int32)
         wsum = torch.tensor([2 ** 40 + rank, 3], dtype=torch.int64)
         parallel.reduce_counts(dist.group.WORLD, hits, wsum)
-        queue.put((rank, scene.sh, picks_log, hits.tolist(), wsum.tolist(),
-                   parallel.shard_views(5, rank, world)))
+        # replicate_views: each rank fills its contiguous view block, then every
+        # rank holds every row
+        mine = parallel.shard_views(5, rank, world)
+        stack = torch.full((5, 3), -1.0)
+        for i in mine:
+            stack[i] = torch.arange(3.0) + 3 * i
+        parallel.replicate_views(stack, mine, dist.group.WORLD)
+        queue.put((rank, scene.sh, picks_log, hits.tolist(), wsum.tolist(), mine, stack.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -89,7 +95,7 @@ def test_two_rank_view_sharded_refit_matches_schedule_oracle():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, sh0, picks0, hits0, wsum0, shard0), (_, sh1, picks1, hits1, wsum1, shard1) = results
+    (_, sh0, picks0, hits0, wsum0, shard0, rep0), (_, sh1, picks1, hits1, wsum1, shard1, rep1) = results
     # both replicas hold the bit-identical scene and drew the same schedule
     np.testing.assert_array_equal(sh0, sh1)
     assert picks0 == picks1
@@ -101,7 +107,9 @@ def test_two_rank_view_sharded_refit_matches_schedule_oracle():
     np.testing.assert_allclose(sh0, ref.sh, rtol=0, atol=1e-12)
     assert hits0 == hits1 == [3, 30, 0]
     assert wsum0 == wsum1 == [2 * 2 ** 40 + 1, 6]
-    assert shard0 == [0, 2, 4] and shard1 == [1, 3]
+    assert shard0 == [0, 1] and shard1 == [2, 3, 4]
+    np.testing.assert_array_equal(rep0, np.arange(15.0).reshape(5, 3))
+    np.testing.assert_array_equal(rep1, rep0)
 
 
 def test_single_process_helpers():
