@@ -14,7 +14,9 @@ import time
 from .errors import SplattintError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librcgs.so")
+# RCGS_LIB_PATH: an alternate in-tree build for A/B measurements (tools/); the
+# default is the library __graft_entry__.build() makes
+LIB_PATH = os.environ.get("RCGS_LIB_PATH") or os.path.join(_HERE, "_lib", "librcgs.so")
 
 RCGS_OK, RCGS_EINVAL, RCGS_ECUDA, RCGS_ENOMEM = 0, 1, 2, 3
 

@@ -130,12 +130,14 @@ struct rcgs_scene {
 
 // Raster record of one kept gaussian (rank s), fp32, 48 bytes.  `a` alone is the
 // 16-byte cull record (mean + footprint half extents) the raster tests first.
+// Powers are in log2 units: power2 = log2(e) * power (render.py:265-269), so
+// alpha = op * 2^power2 = 2^(power2 + log2 op).
 struct __align__(16) RasterRec {
-    float4 a;  // mx_hi, my_hi, half2(ex, ey) bits, opacity
-    float4 b;  // mx_lo, my_lo, p_lo, p_hi     (mean2d = hi + lo; skip if power < p_lo,
-               //                               exact fp64 check in [p_lo, p_hi))
-    float4 c;  // -a/2, -b, -c/2, kappa + 2e-7  (power = nha dx^2 + nb dx dy + nhc dy^2;
-               //                                kappa = relative power-error coefficient)
+    float4 a;  // mx_hi, my_hi, half2(ex, ey) bits, log2(opacity)
+    float4 b;  // mx_lo, my_lo, p_lo, p_hi     (mean2d = hi + lo; alpha is exactly 0 in fp64 if
+               //                               the fp32 power2 < p_lo; [p_lo, p_hi) brackets the gate)
+    float4 c;  // nA, nB, nC, 0                 (power2 = nA dx^2 + nB dx dy + nC dy^2 with
+               //                                nA = -a/2 log2 e, nB = -b log2 e, nC = -c/2 log2 e)
 };
 
 // Exact (fp64) record for guarded decisions: the reference's own operands.

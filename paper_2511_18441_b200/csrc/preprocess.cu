@@ -189,13 +189,14 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
             const __half hx = __float2half_ru((float)fmin(ex_ + 0.01, 60000.0));
             const __half hy = __float2half_ru((float)fmin(ey_ + 0.01, 60000.0));
             const unsigned packed = (unsigned)__half_as_ushort(hx) | ((unsigned)__half_as_ushort(hy) << 16);
+            // raster record in log2 units (power2 = log2(e) * power, so alpha = op * 2^power2)
+            constexpr double kL = 1.4426950408889634;
             RasterRec r;
             const float mxh = (float)p.mx, myh = (float)p.my;
-            r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)op);
-            r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)(P - margin),
-                              (float)(P + margin));
-            // c.w = kappa + 2e-7: the raster's per-composite error term |power| c.w + 6e-7
-            r.c = make_float4((float)(-0.5 * ca), (float)(-cb), (float)(-0.5 * cc), (float)(kappa + 2e-7));
+            r.a = make_float4(mxh, myh, __uint_as_float(packed), (float)log2(op));
+            r.b = make_float4((float)(p.mx - (double)mxh), (float)(p.my - (double)myh), (float)((P - margin) * kL),
+                              (float)((P + margin) * kL));
+            r.c = make_float4((float)(-0.5 * ca * kL), (float)(-cb * kL), (float)(-0.5 * cc * kL), 0.f);
             rec[g] = r;
 
             Rect rc;

@@ -126,6 +126,7 @@ struct RasterArgs {
     int W, H, tiles_x, n_items;
     double alpha_clamp, alpha_skip, t_floor, tau;
     float f_alpha_clamp, f_floor, f_tau;
+    float f_gate2;  // log2(alpha_skip): the alpha gate in log2 units
     // FWD
     PixelOut out;
     // DEPTH
@@ -266,67 +267,6 @@ __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair
     return T;
 }
 
-struct Pix {
-    float uf, vf;
-    float T, A;  // fp32 transmittance and its absolute error bound vs the fp64 product
-};
-
-enum StepKind { SKIP = 0, COMPOSITE = 1, STOP = 2, CROSS = 3, AMBIG = 4 };
-
-// One (pixel, entry) step.  On COMPOSITE *w = alpha * T_before and the pixel
-// advances.  DEPTH returns CROSS at the first composited entry with T_inc < tau
-// (which is never after the stop entry, render.py:389-397).  When the fp32
-// transmittance and its error band straddle a threshold the step returns AMBIG
-// with *w set; the warp then resolves it with the exact transmittance (resolve).
-template <int M>
-__device__ __forceinline__ int step(const float4 ra, const float4 rb, const float4 rc, uint32_t s,
-                                    Pix& px, const RasterArgs& a, float* w) {
-    const float power = cull_power(ra, rb, rc, px.uf, px.vf);
-    if (power < rb.z) return SKIP;
-    float alpha;
-    if (power < rb.w) {
-        const double al = exact_alpha_at(a.exact, s, (double)px.uf, (double)px.vf, a.alpha_clamp, a.alpha_skip);
-        if (al == 0.0) return SKIP;
-        alpha = (float)al;
-    } else {
-        alpha = fminf(a.f_alpha_clamp, ra.w * ex2_approx(power * kLog2e));
-    }
-    const float oma = 1.0f - alpha;  // >= 0.01 (alpha clamp)
-    // relative error of (1 - alpha): q * delta with q = alpha / (1 - alpha) and
-    // delta = |power| (kappa + 2e-7) + 6e-7 (rc.w holds kappa + 2e-7).  Tracked as
-    // the absolute bound A = E * T: E' = E + q delta + 2.4e-7 becomes
-    // A' = A (1 - alpha) + w delta + 2.4e-7 T'  (q T' = alpha T = w), no reciprocal;
-    // its own fp32 rounding is absorbed by the 2x band below.
-    const float delta = fmaf(fabsf(power), rc.w, 6e-7f);
-    const float Tkeep = px.T * oma;
-    const float wgt = alpha * px.T;
-    const float Akeep = fmaf(px.A, oma, fmaf(wgt, delta, 2.4e-7f * Tkeep));
-    *w = wgt;
-    // is the exact inclusive T below a threshold?  fp32 with its error band; the
-    // common case (clearly above) first
-    if (M == DEPTH) {
-        if (fmaf(2.0f, Akeep, Tkeep) < a.f_tau) return CROSS;
-        if (!(fmaf(-2.0f, Akeep, Tkeep) >= a.f_tau)) return AMBIG;
-    }
-    if (fmaf(-2.0f, Akeep, Tkeep) >= a.f_floor) {
-        px.T = Tkeep;
-        px.A = Akeep;
-        return COMPOSITE;
-    }
-    if (fmaf(2.0f, Akeep, Tkeep) < a.f_floor) return STOP;
-    return AMBIG;
-}
-
-// Exact decision for an AMBIG step given the exact inclusive transmittance.
-template <int M>
-__device__ __forceinline__ int resolve(double T64, Pix& px, const RasterArgs& a) {
-    if (M == DEPTH && T64 < a.tau) return CROSS;
-    if (T64 < a.t_floor) return STOP;
-    px.T = (float)T64;
-    px.A = 1.2e-7f * px.T;
-    return COMPOSITE;
-}
-
 // Does the cull record's footprint box touch the 8x4 block at (bx0, by0)?
 __device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float by0) {
     const unsigned packed = __float_as_uint(ra.z);
@@ -335,14 +275,14 @@ __device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float 
     return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 3.f;
 }
 
-// Can the footprint {power >= p_lo} reach any point of the rectangle
-// [x0, x1] x [y0, y1]?  Q = -power is a PSD quadratic of the offset from the mean;
-// its minimum over the box is 0 when the mean is inside, else it lies on an edge,
-// where the 1-D minimiser is a clamp.  The candidates' fp32 values are lowered by
-// their evaluation error bound (2e-6 of the absolute term sum, plus 1e-4), so the
-// test only drops entries whose power stays below the gate at every pixel of the
-// rectangle -- exactly those the per-pixel step would SKIP (alpha exactly 0 in
-// fp64) -- and the results do not change.  NaN keeps the entry.
+// Can the footprint {power2 >= p_lo} reach any point of the rectangle
+// [x0, x1] x [y0, y1]?  Q = -power2 is a PSD quadratic of the offset from the
+// mean; its minimum over the box is 0 when the mean is inside, else it lies on
+// an edge, where the 1-D minimiser is a clamp.  The candidates' fp32 values are
+// lowered by their evaluation error bound (2e-6 of the absolute term sum, plus
+// 1.5e-4 = 1e-4 natural-log units), so the test only drops entries whose power
+// stays below the gate at every pixel of the rectangle -- alpha exactly 0 in
+// fp64 there -- and the results do not change.  NaN keeps the entry.
 __device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const float4 rb, const float4 rc, float x0,
                                                      float y0, float x1, float y1) {
     const float X0 = (x0 - ra.x) - rb.x, X1 = (x1 - ra.x) - rb.x;
@@ -352,7 +292,7 @@ __device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const floa
     const float hA = __fdividef(-0.5f * B, A), hC = __fdividef(-0.5f * B, C);
     auto lower = [&](float dx, float dy) {  // lower bound of Q(dx, dy)
         const float xx = A * dx * dx, yy = C * dy * dy, xy = B * dx * dy;
-        return (xx + yy + xy) - fmaf(2e-6f, xx + yy + fabsf(xy), 1e-4f);
+        return (xx + yy + xy) - fmaf(2e-6f, xx + yy + fabsf(xy), 1.5e-4f);
     };
     auto clampf = [](float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); };
     float m = lower(X0, clampf(hC * X0, Y0, Y1));
@@ -362,14 +302,141 @@ __device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const floa
     return !(m > -rb.z);
 }
 
+// One staged (entry, 8x4 block) pair.  The entry's log2 alpha over the block is
+// a quadratic in the pixel's offset (lx, ly) from the block centre:
+//   P2 = log2(op) + power2 = qA lx^2 + qB lx ly + qC ly^2 + qD lx + qE ly + qF,
+// five FMAs per pixel against per-lane constants, with a rigorous absolute
+// error bound eps for this block (staging): the alpha >= 1/255 gate is decided
+// in fp32 outside [G2 - eps, G2 + eps) (G2 = log2(1/255)) and in fp64 inside;
+// delta = relative error bound of the fp32 alpha.
+//
+// The raw records of the next 32 list entries (and the pair ids of the chunk
+// after) stream into per-lane shared slots with cp.async while the warp
+// composites the current chunk, so the dependent gathers pair_g -> rec[s] ->
+// colour[s] are off the critical path.
 struct WarpStage {
-    float4 a[32], b[32], c[32];
-    float4 col[32];
+    float4 q0[32];  // qA, qB, qC, qD
+    float4 q1[32];  // qE, qF, G2 - eps, G2 + eps
+    float4 q2[32];  // colour rgb (fwd modes), delta
     uint32_t g[32], j[32];  // entry: scene index, tile-list position
+    float4 ra[32], rb[32], rc[32], rcol[32];  // raw records of the next chunk (lane = entry)
+    uint32_t pg[2][32];                       // pair ids (scene indices), double-buffered
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One composite step of a pixel (render.py:265-292, 389-397): w = alpha T_before;
+// fp32 T with its absolute error bound A (A' = A (1 - alpha) + w delta + 2.4e-7 T';
+// delta = relative alpha error); the band tests decide stop (and the tau
+// crossing for DEPTH) exactly unless ambiguous.  The outcome is carried as
+// values: the composited weight (0 if not composited), next T (-T_final once
+// stopped: skipped entries keep it, composited ones stop again), next A, and
+// the crossing.  `amb`: the fp32 band straddles a threshold.
+struct StepOut {
+    float wc, Tn, An;
+    bool amb, xc;
+};
+
+template <int M>
+__device__ __forceinline__ StepOut composite_step(float T, float A, bool live, bool pass, float al, float dl,
+                                                  float f_floor, float f_tau) {
+    // A skipped entry (alpha 0) gives w = 0 and Tk = T exactly; finished lanes
+    // (T <= 0) give w = 0 when skipped and otherwise "stop" again (hi <= 0), so
+    // one select per output covers every case.
+    StepOut o;
+    const float oma = 1.f - al;  // >= 0.01 (alpha clamp)
+    const float w = al * T, Tk = T * oma;
+    const float Ak = fmaf(A, oma, fmaf(w, dl, 2.4e-7f * Tk));
+    const float lo = fmaf(-2.f, Ak, Tk), hi = fmaf(2.f, Ak, Tk);
+    const bool stop = pass && hi < f_floor;
+    bool amb = pass && !stop && !(lo >= f_floor), xcross = false;
+    if (M == DEPTH) {
+        xcross = live && pass && hi < f_tau;
+        amb = amb || (live && pass && !xcross && !(lo >= f_tau));
+    }
+    o.wc = stop ? 0.f : w;  // finished lanes: w = 0 (skip) or they stop again
+    o.Tn = stop ? fminf(T, -T) : (xcross ? 0.f : Tk);
+    o.An = (stop || xcross) ? 0.f : Ak;
+    o.amb = amb;
+    o.xc = xcross;
+    return o;
+}
+
+// The slow path of one entry, called by the whole warp (out of line, so the
+// fast loop keeps its registers and stays convergent): the exact fp64 alpha for
+// the lanes whose fp32 log2 alpha fell in the gate band, then the exact
+// transmittance (warp re-walk of the tile list prefix) for every lane whose
+// threshold test is ambiguous.  Returns the lane's final outcome; *resync
+// counts the re-walks.
+struct SlowOut {
+    StepOut o;
+    uint32_t resync;
+};
+
+template <int M>
+__device__ __noinline__ SlowOut slow_entry(const uint32_t* __restrict__ pair_g, const RasterRec* __restrict__ rec,
+                                           const ExactRec* __restrict__ exact, double clamp, double skip,
+                                           double t_floor, double tau, float f_floor, float f_tau, uint32_t g,
+                                           uint32_t j, uint32_t j0, float uf, float vf, int lane, float T, float A,
+                                           bool live, bool pass, bool gamb, float al, float dl, StepOut cur) {
+    uint32_t resync = 0;
+    if (gamb) {
+        const double a64 = exact_alpha_at(exact, g, (double)uf, (double)vf, clamp, skip);
+        pass = a64 != 0.0;
+        al = (float)a64;
+        dl = 1.2e-7f;  // the fp32 rounding of an exact alpha
+        cur = composite_step<M>(T, A, live, pass, al, dl, f_floor, f_tau);
+    }
+    for (unsigned m = __ballot_sync(0xffffffffu, cur.amb); m; m &= m - 1) {
+        const int L = __ffs(m) - 1;
+        const float lu = __shfl_sync(0xffffffffu, uf, L), lv = __shfl_sync(0xffffffffu, vf, L);
+        const double T64 = warp_exact_T(pair_g, rec, exact, clamp, skip, j0, j, lu, lv, lane);
+        if (lane == L) {  // the exact decision (render.py:278-291, 389-397)
+            const float w = al * T;
+            cur.amb = false;
+            if (M == DEPTH && T64 < tau) {
+                cur.wc = w;
+                cur.Tn = 0.f;
+                cur.An = 0.f;
+                cur.xc = true;
+            } else if (T64 < t_floor) {
+                cur.wc = 0.f;
+                cur.Tn = fminf(T, -T);
+                cur.An = 0.f;
+            } else {
+                cur.wc = w;
+                cur.Tn = (float)T64;
+                cur.An = 1.2e-7f * cur.Tn;
+            }
+        }
+        ++resync;
+    }
+    return SlowOut{cur, resync};
+}
 
 // kInstr: the instrumented variant (work counters / per-item trace); production
 // launches carry no counter registers or checks in the entry loop.
+//
+// Per (pixel, entry) the fast path is branch-free: skipped entries (alpha 0)
+// leave T and the colour exactly unchanged, finished pixels carry T = 0 (their
+// output T is kept in Tout), and everything that needs the exact fp64 answer --
+// an alpha inside the gate band, or an fp32 transmittance whose error band
+// straddles the stop floor (or tau) -- raises one warp vote per entry that sends
+// the warp to the slow path for that entry.
 #ifndef RCGS_FWDREC_MIN_CTAS
 #define RCGS_FWDREC_MIN_CTAS 4
 #endif
@@ -381,11 +448,13 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
     __shared__ WarpStage stage_all[kRWarps];
     const int lane = threadIdx.x & 31;
     // The warp index comes from a shuffle: ptxas cannot re-derive a shuffle result
-    // from threadIdx / the CTA id at every use (which it did with the plain
-    // expression, ~16 instructions per entry), so the staging base stays in a
-    // register.  Measured 332 -> 323 us for the recording raster.
+    // from threadIdx / the CTA id at every use, so the staging base stays in a
+    // register.
     WarpStage& st = stage_all[kRWarps == 1 ? 0 : __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0)];
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // pixel offset from the 8x4 block centre (exact small fp32 values)
+    const float lxf = (float)(lane & 7) - 3.5f, lyf = (float)(lane >> 3) - 1.5f;
+    const float G2 = a.f_gate2;
 
     for (;;) {
         unsigned item = 0;
@@ -400,13 +469,11 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         const bool inside = u < a.W && v < a.H;
         const int64_t pix = (int64_t)v * a.W + u;
 
-        Pix px;
-        px.uf = (float)u;
-        px.vf = (float)v;
-        px.T = 1.0f;
-        px.A = 0.0f;
+        // T: fp32 transmittance while the pixel composites (T > 0); once it stops,
+        // -T_final (T before the stop entry), and 0 for pixels that never composite.
+        // A: the absolute error bound of T vs the fp64 product.
+        float T = inside ? 1.f : 0.f, A = 0.f;
         uint32_t n_resync = 0;  // warp-uniform (trace launches)
-        bool done = !inside;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
         int32_t cross = -1;
         uint32_t ncap = 0, cap_base = 0;
@@ -425,11 +492,12 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             }
         }
         if (kInstr && a.trace && lane == 0) a.trace[8 * (int64_t)item] = globaltimer_lo();
-        if (M == HITS && inside) done = a.mask[pix] == 0;
+        if (M == HITS && inside && a.mask[pix] == 0) T = 0.f;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
         const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
+        const float cxf = fbx0 + 3.5f, cyf = fby0 + 1.5f;
         if (kInstr && M == FWDREC && a.counters) {
             // static list-cull statistics for a two-pixels-per-lane raster (8x8
             // regions): entries passing this 8x4 block's cull, and for the top block
@@ -463,81 +531,130 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         }
         uint32_t n_eval = 0, n_comp = 0, n_iter = 0;
         // FWDREC: this block's record slots, 8 per tile-list entry and block (32-bit:
-        // the host checks 8 * pairs < 2^32)
-        // a shuffle result, so ptxas keeps it in a register instead of re-deriving it
-        // from the range and block index at every record (measured 323 -> 318 us)
+        // the host checks 8 * pairs < 2^32); every entry the warp composites gets a
+        // record (the pixels' weights, 0 where a pixel did not composite).  A shuffle
+        // result, so ptxas keeps it in a register.
         const uint32_t rbase =
             __shfl_sync(0xffffffffu, kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x), 0);
+        // FWDREC: nrec records so far; wp = this lane's weight slot of the next one
         uint32_t nrec = 0;
-        for (uint32_t c0 = range.x; c0 < range.y; c0 += 32) {
-            if (__all_sync(0xffffffffu, done)) break;
+        float* wp = M == FWDREC ? a.wrec_w + (size_t)rbase * 32 + lane : nullptr;
+        // chunk pipeline: pair ids two chunks ahead, raw records one chunk ahead (each
+        // lane copies and later reads only its own slots)
+        auto issue_pg = [&](uint32_t cn, int buf) {
+            if (cn + lane < range.y) cp_async4(&st.pg[buf][lane], a.pair_g + cn + lane);
+            cp_async_commit();
+        };
+        auto issue_raw = [&](uint32_t cn, int buf) {
+            if (cn + lane < range.y) {
+                const uint32_t sn = st.pg[buf][lane];
+                cp_async16(&st.ra[lane], &a.rec[sn].a);
+                cp_async16(&st.rb[lane], &a.rec[sn].b);
+                cp_async16(&st.rc[lane], &a.rec[sn].c);
+                if (kFwd) cp_async16(&st.rcol[lane], &a.color[sn]);
+            }
+            cp_async_commit();
+        };
+        if (range.x < range.y) {
+            issue_pg(range.x, 0);
+            issue_pg(range.x + 32, 1);
+            cp_async_wait<1>();
+            issue_raw(range.x, 0);
+        }
+        int buf = 0;
+        for (uint32_t c0 = range.x; c0 < range.y; c0 += 32, buf ^= 1) {
+            if (__all_sync(0xffffffffu, !(T > 0.f))) break;
+            cp_async_wait<0>();  // this chunk's records (and the next chunk's ids)
             const uint32_t j = c0 + lane;
             bool keep = false;
             uint32_t s = 0;
-            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
+            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra, rcol = ra;
             if (j < range.y) {
-                s = a.pair_g[j];
-                ra = a.rec[s].a;
+                s = st.pg[buf][lane];
+                ra = st.ra[lane];
                 keep = touches_block(ra, fbx0, fby0);
                 if (keep) {
-                    rb = a.rec[s].b;
-                    rc = a.rec[s].c;
+                    rb = st.rb[lane];
+                    rc = st.rc[lane];
                     keep = ellipse_touches_rect(ra, rb, rc, fbx0, fby0, fbx0 + 7.f, fby0 + 3.f);
                 }
+                if (kFwd && keep) rcol = st.rcol[lane];
+            }
+            // the slots are consumed: start the next chunk's records and the ids after
+            if (c0 + 32 < range.y) {
+                issue_raw(c0 + 32, buf ^ 1);
+                if (c0 + 64 < range.y) issue_pg(c0 + 64, buf);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = __popc(bal & lt_mask);
-                st.a[slot] = ra;
-                st.b[slot] = rb;
-                st.c[slot] = rc;
+                // the entry's quadratic about the block centre and its error bound
+                const float mxr = (ra.x - cxf) + rb.x, myr = (ra.y - cyf) + rb.y;
+                const float nA = rc.x, nB = rc.y, nC = rc.z, l2op = ra.w;
+                const float qD = -fmaf(2.f * nA, mxr, nB * myr);
+                const float qE = -fmaf(2.f * nC, myr, nB * mxr);
+                const float qF = fmaf(nA * mxr, mxr, fmaf(nB * mxr, myr, fmaf(nC * myr, myr, l2op)));
+                // |P2_fp32 - P2| <= 18 u M over the block (u = 2^-24; coefficient
+                // rounding, the centred mean, the expansion and the 5-FMA evaluation),
+                // M = |qA| X^2 + |qB| X Y + |qC| Y^2 + |log2 op| with X = 3.5 + |mxr|,
+                // Y = 1.5 + |myr| bounding every monomial; taken as 2e-6 M + 2e-6
+                const float X = 3.5f + fabsf(mxr), Y = 1.5f + fabsf(myr);
+                const float Mb = fmaf(fabsf(nA), X * X, fmaf(fabsf(nB), X * Y, fmaf(fabsf(nC), Y * Y, fabsf(l2op))));
+                const float eps = fmaf(2e-6f, Mb, 2e-6f);
+                st.q0[slot] = make_float4(nA, nB, nC, qD);
+                st.q1[slot] = make_float4(qE, qF, G2 - eps, G2 + eps);
+                // relative alpha error: ln 2 eps (log2 error) + ex2.approx (< 3e-7)
+                const float delta = fmaf(0.6932f, eps, 4e-7f);
+                if (kFwd) {
+                    st.q2[slot] = make_float4(rcol.x, rcol.y, rcol.z, delta);
+                } else {
+                    st.q2[slot] = make_float4(0.f, 0.f, 0.f, delta);
+                }
                 st.g[slot] = s;
                 st.j[slot] = j;
-                if (kFwd) st.col[slot] = a.color[s];
+                if (M == FWDREC) a.wrec_s[rbase + nrec + slot] = s;  // record ids, one per staged entry
             }
             __syncwarp();
             const int n = __popc(bal);
-            for (int k = 0; k < n; ++k) {
-                float w = 0.f;
-                int r = SKIP;
+            // one (pixel, entry) step of staged entry k for this lane
+            auto entry = [&](int k) {
+                const float4 q0 = st.q0[k], q1 = st.q1[k], q2 = st.q2[k];
+                // P2 = lx (qA lx + qB ly + qD) + (ly (qC ly + qE) + qF): five FMAs, two
+                // lane constants (each rounding is bounded by the monomial sum M)
+                const float P2 = fmaf(lxf, fmaf(q0.x, lxf, fmaf(q0.y, lyf, q0.w)), fmaf(lyf, fmaf(q0.z, lyf, q1.x), q1.y));
+                const bool live = T > 0.f;
+                const bool pass = P2 >= q1.z;  // false: alpha is certainly 0 (skipped, T x 1 exactly)
+                // gate band (finished lanes included: a spurious slow call is harmless)
+                const bool gamb = pass && P2 < q1.w;
+                const float al = pass ? fminf(a.f_alpha_clamp, ex2_approx(P2)) : 0.f;
                 if (kInstr) {
-                    n_eval += !done;
+                    n_eval += live;
                     ++n_iter;
                 }
-                if (!done) r = step<M>(st.a[k], st.b[k], st.c[k], st.g[k], px, a, &w);
-                // ambiguous threshold tests: exact transmittance, one pixel at a time, by the warp
-                for (unsigned amb = __ballot_sync(0xffffffffu, r == AMBIG); amb; amb &= amb - 1) {
-                    const int L = __ffs(amb) - 1;
-                    const float lu = __shfl_sync(0xffffffffu, px.uf, L), lv = __shfl_sync(0xffffffffu, px.vf, L);
-                    const double T64 = warp_exact_T(a.pair_g, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, range.x,
-                                                    st.j[k], lu, lv, lane);
-                    if (lane == L) r = resolve<M>(T64, px, a);
-                    ++n_resync;
+                StepOut o = composite_step<M>(T, A, live, pass, al, q2.w, a.f_floor, a.f_tau);
+                if (__any_sync(0xffffffffu, gamb || o.amb)) {
+                    const SlowOut so =
+                        slow_entry<M>(a.pair_g, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, a.t_floor, a.tau, a.f_floor,
+                                      a.f_tau, st.g[k], st.j[k], range.x, cxf + lxf, cyf + lyf, lane, T, A, live, pass,
+                                      gamb, al, q2.w, o);
+                    o = so.o;
+                    n_resync += so.resync;
                 }
-                if (!done) {
-                    if (r == STOP) done = true;
-                    if (r == CROSS) {
-                        cross = (int32_t)st.g[k];
-                        done = true;
-                    }
-                }
-                const bool comp = (r == COMPOSITE);
+                const float wc = o.wc;
+                const bool xc = o.xc;
+                const float Tn = o.Tn, An = o.An;
+                const bool comp = wc != 0.f;
                 if (kInstr) n_comp += comp;
+                T = Tn;
+                A = An;
+                if (M == DEPTH && xc) cross = (int32_t)st.g[k];
                 if (kFwd) {
-                    if (comp) {
-                        const float4 c = st.col[k];
-                        acc0 = fmaf(c.x, w, acc0);
-                        acc1 = fmaf(c.y, w, acc1);
-                        acc2 = fmaf(c.z, w, acc2);
-                    }
-                    if (M == FWDREC && __ballot_sync(0xffffffffu, comp)) {
-                        // record: the entry + all 32 pixel weights (0 where a pixel did not
-                        // composite): one coalesced 128-byte store.  (Packing only the
-                        // composited weights measured slower both ways: partial-sector
-                        // writes here, offset-dependent loads in the readers.)
-                        const uint32_t slot = rbase + nrec++;
-                        a.wrec_w[(size_t)slot * 32 + lane] = comp ? w : 0.f;
-                        if (lane == 0) a.wrec_s[slot] = st.g[k];
+                    acc0 = fmaf(q2.x, wc, acc0);
+                    acc1 = fmaf(q2.y, wc, acc1);
+                    acc2 = fmaf(q2.z, wc, acc2);
+                    if (M == FWDREC) {
+                        *wp = wc;
+                        wp += 32;
                     }
                 } else if (M == CAP_COUNT) {
                     ncap += comp;
@@ -546,17 +663,17 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                         const uint32_t o = cap_base + ncap++;
                         a.cap_pixel[o] = pix;
                         a.cap_kept[o] = a.rank_of[st.g[k]];  // the API reports depth ranks
-                        a.cap_weight[o] = (double)w;
+                        a.cap_weight[o] = (double)wc;
                     }
                 } else if (M == BWD) {
-                    float v0 = comp ? w * g0 : 0.f, v1 = comp ? w * g1 : 0.f, v2 = comp ? w * g2 : 0.f;
+                    float v0 = wc * g0, v1 = wc * g1, v2 = wc * g2;
                     if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
                         // transposed reduce-scatter of (v0, v1, v2, 0) over the warp: 6
                         // shuffles instead of 15; channel c ends summed in lanes 8c..8c+7
                         const bool h16 = lane & 16, h8 = lane & 8;
-                        const float ra = __shfl_xor_sync(0xffffffffu, h16 ? v0 : v2, 16);
-                        const float rb = __shfl_xor_sync(0xffffffffu, h16 ? v1 : 0.f, 16);
-                        const float ka = (h16 ? v2 : v0) + ra, kb = (h16 ? 0.f : v1) + rb;
+                        const float ra_ = __shfl_xor_sync(0xffffffffu, h16 ? v0 : v2, 16);
+                        const float rb_ = __shfl_xor_sync(0xffffffffu, h16 ? v1 : 0.f, 16);
+                        const float ka = (h16 ? v2 : v0) + ra_, kb = (h16 ? 0.f : v1) + rb_;
                         float val = (h8 ? kb : ka) + __shfl_xor_sync(0xffffffffu, h8 ? ka : kb, 8);
                         val += __shfl_xor_sync(0xffffffffu, val, 4);
                         val += __shfl_xor_sync(0xffffffffu, val, 2);
@@ -573,7 +690,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 } else if (M == HITS) {
                     const unsigned hb = __ballot_sync(0xffffffffu, comp);
                     if (hb) {
-                        float ws = comp ? w : 0.f;
+                        float ws = wc;
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
                         if (lane == 0) {
@@ -583,10 +700,17 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                         }
                     }
                 }
-                if ((k & 7) == 7 && __all_sync(0xffffffffu, done)) break;
+            };
+            bool all_done = false;
+            int k = 0;
+            for (; k < n && !all_done; ++k) {
+                entry(k);
+                all_done = __all_sync(0xffffffffu, !(T > 0.f));  // one vote: cheaper than a cadence test
             }
+            nrec += (uint32_t)k;  // entries processed (one record each in FWDREC)
             __syncwarp();
         }
+        cp_async_wait<0>();  // no copy may land in the slots once the next item uses them
 
         if (kInstr && a.counters) {
 #pragma unroll
@@ -622,7 +746,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         }
         if (!inside) continue;
         if (kFwd) {
-            write_pixel<M == FWDRGBA>(a.out, a.W, a.H, pix, acc0, acc1, acc2, px.T);
+            write_pixel<M == FWDRGBA>(a.out, a.W, a.H, pix, acc0, acc1, acc2, fabsf(T));
         } else if (M == DEPTH) {
             if (a.cross) a.cross[pix] = cross;
             if (a.depth) a.depth[pix] = cross >= 0 ? a.z[cross] : __longlong_as_double(0x7ff0000000000000ll);
@@ -988,6 +1112,7 @@ static RasterArgs base_args(const rcgs_view* v) {
     a.t_floor = v->cfg.transmittance_floor;
     a.f_alpha_clamp = (float)v->cfg.alpha_clamp;
     a.f_floor = (float)v->cfg.transmittance_floor;
+    a.f_gate2 = (float)log2(v->cfg.alpha_skip);
     a.tau = 0.5;
     a.f_tau = 0.5f;
     return a;
