@@ -274,6 +274,7 @@ def run_gpu(args):
 
     # ---- per-kernel algorithmic work (live stage times above) + view statistics
     stages = stage_model(eng, cams, npix, cfg, live, cnt)
+    adam_active = (round(float(eng.tile_state.float().mean()), 4) if eng.tile_state is not None else None)
     # ---- rendered Mpix/s: full forward (preprocess + bin + colour + raster) per frame
     frames = max(8, args.steps)
     torch.cuda.synchronize()
@@ -373,6 +374,7 @@ def run_gpu(args):
         "pairs_per_view": stages["pairs"], "kept_per_view": stages["kept"],
         "roofline": roof, "rooflines": rooflines, "raster_work_per_launch": stages["raster_work"], "raster_region_share_q": region_q,
         "gpu_launches": gpu_launches, "setup_s": round(setup_s, 1),
+        "adam_tiles_active_frac": adam_active,
         "final_loss": recs[-1][4] if recs else None,
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         "interactive_c5": interactive, "selection_sweep_c4": sweep, "resident_views": resident,

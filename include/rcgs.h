@@ -230,12 +230,17 @@ typedef struct {
     int64_t every;              /* snapshot_every (> 0)                           */
 } rcgs_adam_publish;
 /* rcgs_adam_fused / rcgs_adam_fused_next (next_view may be NULL) with optional
- * snapshot publication (publish may be NULL). */
+ * snapshot publication (publish may be NULL) and optional exact tile skipping:
+ * d_tile_state (ceil(N/64) uint32, caller-owned, zero-initialised together with
+ * m = v = 0; set to all-ones whenever m/v/SH are written from outside) marks the
+ * 64-gaussian tiles whose Adam state may be nonzero.  A tile whose state is 0
+ * and whose acc is 0 in every view is left untouched -- bit-identical to the
+ * dense update, which maps (theta, 0, 0, g = 0) to itself.  NULL = dense. */
 int rcgs_adam_fused_ex(const rcgs_scene* scene, float* d_sh, float* d_m, float* d_v,
                        const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                        const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                        double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* publish,
-                       void* stream);
+                       uint32_t* d_tile_state, void* stream);
 /* Dense Adam on an explicit gradient (N,16,3) (adam_step API). */
 int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,
                     const rcgs_adam_config* cfg, const int32_t* d_reject, int64_t* d_step,

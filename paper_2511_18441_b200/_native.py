@@ -81,7 +81,8 @@ _SIGNATURES = {
     "rcgs_adam_fused_next": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
                              P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "rcgs_adam_fused_ex": [c_void_p, c_void_p, c_void_p, c_void_p, P(c_void_p), P(c_double), c_i32,
-                           P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, P(AdamPublish), c_void_p],
+                           P(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p, P(AdamPublish), c_void_p,
+                           c_void_p],
     "rcgs_adam_dense": [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, P(AdamConfig), c_void_p,
                         c_void_p, c_void_p],
     "rcgs_nonfinite_check": [c_void_p, c_i64, c_void_p, c_void_p],

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
     unsigned* __restrict__ ticket, int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
     Center next_cen, float4* __restrict__ next_color, double* __restrict__ reject_record,
-    float* __restrict__ snapshot, int64_t* __restrict__ snapshot_step, int64_t snapshot_every) {
+    float* __restrict__ snapshot, int64_t* __restrict__ snapshot_step, int64_t snapshot_every,
+    const uint32_t* __restrict__ tile_state) {
     // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
     // colour epilogue the next view is still coloured from the unchanged SH.
     // Every block still takes the last-block ticket, so the step commit (reject
@@ -167,13 +168,23 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     auto stage_buf = [&](int s, int arr) -> float4* {
         return reinterpret_cast<float4*>(smem + ((size_t)s * 3 + arr) * kATileBytes);
     };
+    // per tile: 2 = full update (SH, m, v in and out), 1 = SH in only (an inactive
+    // tile whose SH the fused colour epilogue needs), 0 = nothing.  A tile is
+    // inactive when its Adam state is exactly 0 and every view's acc is 0 there
+    // (tile_state, adam_active_kernel): Adam then leaves all of it bit-identical
+    // (m' = v' = 0, theta' = theta - lr * 0 / (0 + eps)), so the skip is exact.
+    auto mode_of = [&](int64_t tile) -> int {
+        const bool active = tile_state == nullptr || tile_state[tile] != 0u;
+        return (upd && active) ? 2 : (next_color != nullptr ? 1 : 0);
+    };
     auto issue = [&](int64_t tile, int s) {  // one thread
         const int64_t g0 = tile * kAG;
         const uint32_t bytes = (uint32_t)(n - g0 < kAG ? n - g0 : kAG) * kARow;
         const uint32_t bar = smem_addr(&bars[s]);
-        mbar_expect_tx(bar, 3 * bytes);
-#pragma unroll
-        for (int arr = 0; arr < 3; ++arr)
+        const int md = mode_of(tile);
+        const int na = md == 2 ? 3 : md;
+        mbar_expect_tx(bar, (uint32_t)na * bytes);  // 0 bytes: the phase completes at once
+        for (int arr = 0; arr < na; ++arr)
             bulk_load(smem_addr(stage_buf(s, arr)), arrays[arr] + g0 * 48, bytes, bar);
     };
     __shared__ float2 s_bc;
@@ -198,8 +209,9 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         const int64_t g0 = tile * kAG;
         const int ng = (int)(n - g0 < kAG ? n - g0 : kAG);
         mbar_wait(smem_addr(&bars[s]), (uint32_t)((it / kAStages) & 1));
+        const int md = mode_of(tile);
         float c12[12];  // this thread's 12 coefficients after the update (colour epilogue)
-        if (upd && gi < ng) {
+        if (md == 2 && gi < ng) {
             const int64_t g = g0 + gi;
             const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
             float gr[12];
@@ -243,7 +255,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
                 c12[4 * q + 2] = p4.z;
                 c12[4 * q + 3] = p4.w;
             }
-        } else if (gi < ng) {  // rejected step: the tile as loaded
+        } else if (md == 1 && gi < ng) {  // rejected step or inactive tile: the SH as loaded
             const float* P = reinterpret_cast<const float*>(stage_buf(s, 0)) + gi * 48 + part * 12;
 #pragma unroll
             for (int e = 0; e < 12; ++e) c12[e] = P[e];
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        if (t == 0 && upd) {
+        if (t == 0 && md == 2) {
             const uint32_t bytes = (uint32_t)ng * kARow;
 #pragma unroll
             for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
@@ -305,6 +317,22 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         commit_step(ticket, upd, step, reject, reject_record, snap ? snapshot_step : nullptr, *step + 1);
     }
+}
+
+// tile_state[t] |= any view's acc != 0 in tile t (NaN counts as nonzero).  Run
+// before the fused Adam of the step, on its stream; state only ever grows, so a
+// flag set by a step that is then rejected is merely conservative.
+__global__ void adam_active_kernel(AccViews views, int64_t n, uint32_t* __restrict__ state) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool nz = false;
+    if (g < n) {
+        for (int vi = 0; vi < views.n; ++vi) {
+            const float* acc = views.acc[vi] + 3 * g;
+            nz = nz || !(acc[0] == 0.f && acc[1] == 0.f && acc[2] == 0.f);
+        }
+    }
+    // a warp covers 32 gaussians of one 64-gaussian tile
+    if (__ballot_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) state[g / kAG] = 1u;
 }
 
 __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
@@ -381,7 +409,7 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
                            const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                            const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                            double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* pub,
-                           void* stream) {
+                           uint32_t* d_tile_state, void* stream) {
     RCGS_CHECK_ARG(sc && d_sh && d_m && d_v && h_d_accs && h_centers && cfg && d_step, "null argument");
     RCGS_CHECK_ARG(pub == nullptr || (pub->d_snapshot != nullptr && pub->every > 0),
                    "snapshot publication needs a buffer and a positive cadence");
@@ -426,11 +454,15 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             nrank = next_view->rank_of;
             ncolor = next_view->color;
         }
+        if (d_tile_state != nullptr) {
+            adam_active_kernel<<<div_up(sc->n, 256), 256, 0, s>>>(av, sc->n, d_tile_state);
+            RCGS_LAUNCH_CHECK();
+        }
         // bias corrections from and commit of the device step counter happen inside
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
             sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
             d_reject, nrank, nc, ncolor, d_reject_record, pub ? pub->d_snapshot : nullptr,
-            pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0);
+            pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0, d_tile_state);
         RCGS_LAUNCH_CHECK();
         return RCGS_OK;
     }
@@ -445,16 +477,16 @@ extern "C" int rcgs_adam_fused(const rcgs_scene* sc, float* d_sh, float* d_m, fl
                                const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                                double* d_reject_record, void* stream) {
     return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
-                           d_reject_record, nullptr, nullptr, stream);
+                           d_reject_record, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int rcgs_adam_fused_ex(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
                                   const float* const* h_d_accs, const double* h_centers, int32_t n_views,
                                   const rcgs_adam_config* cfg, int32_t* d_reject, int64_t* d_step,
                                   double* d_reject_record, rcgs_view* next_view, const rcgs_adam_publish* publish,
-                                  void* stream) {
+                                  uint32_t* d_tile_state, void* stream) {
     return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
-                           d_reject_record, next_view, publish, stream);
+                           d_reject_record, next_view, publish, d_tile_state, stream);
 }
 
 extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_m, float* d_v,
@@ -464,7 +496,7 @@ extern "C" int rcgs_adam_fused_next(const rcgs_scene* sc, float* d_sh, float* d_
     RCGS_CHECK_ARG(next_view != nullptr, "null next view");
     RCGS_CHECK_ARG(next_view->scene == sc, "next view belongs to another scene");
     return adam_fused_impl(sc, d_sh, d_m, d_v, h_d_accs, h_centers, n_views, cfg, d_reject, d_step,
-                           d_reject_record, next_view, nullptr, stream);
+                           d_reject_record, next_view, nullptr, nullptr, stream);
 }
 
 extern "C" int rcgs_adam_dense(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t n,

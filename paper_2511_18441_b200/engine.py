@@ -237,11 +237,18 @@ class RefitEngine:
     def __init__(self, dscene: D.DeviceScene, sh_dev: torch.Tensor, cameras, targets,
                  config, seed: int = 0, cache_views: bool = True, views=None, group=None,
                  raster=DEFAULT_CONFIG, max_pending: int = 4096, prefetch: int = 0,
-                 profile: bool = False, fuse_color: bool = True):
+                 profile: bool = False, fuse_color: bool = True, sparse_adam: bool = False):
         self.dscene = dscene
         self.sh = sh_dev                      # (N, 16, 3) fp32, updated in place
         self.m = torch.zeros_like(sh_dev)
         self.v = torch.zeros_like(sh_dev)
+        # 64-gaussian tiles whose Adam state may be nonzero (exact skipping of
+        # never-touched tiles, rcgs_adam_fused_ex); reset to ones by state loads
+        # off by default: at C3 every 64-gaussian tile is touched within a few steps
+        # (measured 99.8%), so the skip only pays for small edits
+        sparse_adam = sparse_adam or os.environ.get("RCGS_SPARSE_ADAM", "0") == "1"
+        self.tile_state = (torch.zeros((dscene.n + 63) // 64, dtype=torch.int32, device=sh_dev.device)
+                           if sparse_adam else None)
         self.cameras = list(cameras)          # [(intrinsics, pose)]
         self.targets = targets                # per view (H, W, 3) fp32 device or pinned host
         self.config = config
@@ -419,6 +426,8 @@ class RefitEngine:
                 raise ValueError(f"state {name} has shape {tuple(src.shape)}, engine {tuple(dst.shape)}")
             dst.copy_(src.to(dst.device))
         self.step_dev.fill_(int(st["step"]))
+        if self.tile_state is not None:
+            self.tile_state.fill_(1)  # m/v written from outside: every tile may be nonzero
         self.rng.bit_generator.state = st["rng"]
         self._replay = collections.deque([list(p) for p in st["ahead"]])
         torch.cuda.current_stream().synchronize()
@@ -511,13 +520,13 @@ class RefitEngine:
             if ev:
                 ev[5].record()
             # also records + re-arms the reject flag, and publishes snapshots
-            N.call("rcgs_adam_fused_ex", *args, nxt.handle, pub, D.stream_ptr())
+            N.call("rcgs_adam_fused_ex", *args, nxt.handle, pub, N.ptr(self.tile_state), D.stream_ptr())
             nxt._colored = True
             self._held = (nxt_picks, nxt, True, nxt_key, nxt_tgt)
         else:
             if ev:
                 ev[5].record()
-            N.call("rcgs_adam_fused_ex", *args, None, pub, D.stream_ptr())
+            N.call("rcgs_adam_fused_ex", *args, None, pub, N.ptr(self.tile_state), D.stream_ptr())
         if ev:
             ev[6].record()
             self._prof.append((ev, coloured))

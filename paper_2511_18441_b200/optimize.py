@@ -129,6 +129,8 @@ def optimize_iteration(scene, dataset, rng: np.random.Generator, state: AdamStat
                       [D.to_device(target.image)], config, cache_views=False)
     eng.m.copy_(D.to_device(state.m))
     eng.v.copy_(D.to_device(state.v))
+    if eng.tile_state is not None:
+        eng.tile_state.fill_(1)  # Adam state from the caller: no tile may be skipped
     eng.step_dev.fill_(state.step)
     eng.step(picks=[0])
     (_, _, l1, ss, total, rejected), = eng.drain()

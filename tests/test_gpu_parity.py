@@ -540,6 +540,37 @@ def test_engine_pipelines_bit_identical():
         assert recs == out[0][3]
 
 
+def test_sparse_adam_bit_identical_to_dense():
+    """Skipping the 64-gaussian tiles whose Adam state and gradient are exactly
+    zero (rcgs_adam_fused_ex tile state) leaves SH, m, v and the metrics
+    bit-identical to the dense update, with and without the fused colour epilogue."""
+    import sys
+    import torch
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2511_18441_b200 import device as D
+    from paper_2511_18441_b200.engine import RefitEngine
+    cfg = dict(n=30_000, deg=3, views=6, width=320, height=240)
+    scene, cams, ds, sh0, gt, cloud, _ = bench.build_workload(cfg, 0, torch.device("cuda", 0))
+    sp = P.SelectionPass(ds, cams, gt)
+    sp.run(D.to_device(cloud.points, torch.float64), (1.0, 0.2, 0.2))
+    targets = [sp.edited[i] for i in range(len(cams))]
+    for prefetch in (0, 2):
+        out = []
+        for sparse in (False, True):
+            eng = RefitEngine(ds, sh0.clone(), cams, targets, P.OptimizerConfig(), seed=5, cache_views=False,
+                              prefetch=prefetch, sparse_adam=sparse)
+            for _ in range(9):
+                eng.step()
+            recs = [repr(r) for r in eng.drain()]
+            touched = None if eng.tile_state is None else float(eng.tile_state.float().mean())
+            eng.close()
+            out.append((eng.sh.clone(), eng.m.clone(), eng.v.clone(), recs, touched))
+        assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+        assert torch.equal(out[0][2], out[1][2]) and out[0][3] == out[1][3]
+        assert 0.0 < out[1][4] <= 1.0
+
+
 def test_weight_records_bit_identical():
     """rcgs_render_train + record-streaming backward + SpMV re-render equal the
     traversal render / backward bit for bit (weights depend on geometry only)."""
