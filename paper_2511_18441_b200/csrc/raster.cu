@@ -626,7 +626,8 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 const bool pass = P2 >= q1.z;  // false: alpha is certainly 0 (skipped, T x 1 exactly)
                 // gate band (finished lanes included: a spurious slow call is harmless)
                 const bool gamb = pass && P2 < q1.w;
-                const float al = pass ? fminf(a.f_alpha_clamp, ex2_approx(P2)) : 0.f;
+                // ex2(-inf) = 0: the skip is folded into the exponent (no predicated MUFU)
+                const float al = fminf(a.f_alpha_clamp, ex2_approx(pass ? P2 : -INFINITY));
                 if (kInstr) {
                     n_eval += live;
                     ++n_iter;
