@@ -164,8 +164,13 @@ def test_random_scenes_match_oracle():
             specs.append(dict(position=rng.uniform(-0.9, 0.9, 3) + [0, 0, 2.0],
                               color=rng.uniform(0.0, 1.0, 3), scale=rng.uniform(0.01, 0.3, 3),
                               opacity=rng.uniform(0.02, 0.99), quat=q / np.linalg.norm(q)))
+        # near-clip cases (render.py:176: kept iff z > 0.2) and very close large footprints
+        for z in (0.2, 0.2001, np.nextafter(0.2, 1.0), 0.23, 0.35):
+            specs.append(dict(position=(rng.uniform(-0.05, 0.05), rng.uniform(-0.05, 0.05), z),
+                              color=rng.uniform(0.0, 1.0, 3), scale=rng.uniform(0.002, 0.02, 3),
+                              opacity=rng.uniform(0.3, 0.99), quat=(1.0, 0.0, 0.0, 0.0)))
         ns = make_scene(specs)
-        ns.sh[:, 1:, :] = rng.normal(0, 0.2, (60, 15, 3))
+        ns.sh[:, 1:, :] = rng.normal(0, 0.2, (len(specs), 15, 3))
         scene = p_from_ns(ns)
         intr, pose = p_cam_ns(*identity_camera(w, h, fx=float(max(w, h))))
         assert_image_close(P.render(scene, intr, pose), OR.render(ns, intr, pose))
@@ -506,7 +511,7 @@ def test_config1_refit_trajectory():
     dc = np.abs(final.sh[:, 0, :] - d["traj_dc"]).max()
     print(f"c1 trajectory: worst metric diff {worst:.2e}, final render PSNR {p:.1f} dB, max |dDC| {dc:.2e}")
     assert worst < 1e-3
-    assert p > 50.0
+    assert p > 60.0  # SURVEY.md 8(c)(iv) gate
 
 
 # ---------------------------------------------------------------- engine pipelines
