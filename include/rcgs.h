@@ -70,6 +70,11 @@ typedef struct {
 } rcgs_view_info;
 
 int rcgs_version(void);
+/* Checked builds (-DRCGS_CHECKED): number of device bound-check failures since
+ * the last reset; RCGS_EINVAL in release builds. */
+int rcgs_debug_violations(uint64_t* h_count, int reset);
+/* Checked builds: run one device check that fails when fail != 0 (self-test). */
+int rcgs_debug_selftest(int fail);
 const char* rcgs_last_error(void);
 /* Pre-grow the device's stream-ordered memory pool (used for the per-view and
  * temporary buffers) to `bytes`, so steady-state steps never map new memory. */

@@ -104,6 +104,8 @@ _SIGNATURES = {
     "rcgs_raster_trace": [c_void_p, c_i64],
     "rcgs_fp32_peak": [c_i32, P(c_double), c_void_p],
     "rcgs_pool_reserve": [c_i64, c_void_p],
+    "rcgs_debug_violations": [P(ctypes.c_uint64), c_int],
+    "rcgs_debug_selftest": [c_int],
 }
 EXPORTED = tuple(_SIGNATURES) + ("rcgs_version", "rcgs_last_error")
 

@@ -108,6 +108,41 @@ void release_records(rcgs_view* v, cudaStream_t s);  // raster.cu: drop or free 
 int radix_sort_u32(uint32_t** key_cur, uint32_t** key_alt, uint32_t** val_cur, uint32_t** val_alt,
                    bool vals_are_index, int64_t n, int end_bit, cudaStream_t s);
 
+// ---- checked builds (compute-sanitizer is unavailable on this pool) --------------
+// `make EXTRA=-DRCGS_CHECKED ...` compiles device-side bound checks on the computed
+// indices of the hot kernels (pair / record / scene / sort-destination indices):
+// a failed check increments a device counter (no trap, so a bad index is counted,
+// not fatal) that rcgs_debug_violations() reads.  Release builds compile them out.
+#ifdef RCGS_CHECKED
+// one counter per translation unit (no relocatable device code), each TU's host
+// reader registered at load time; rcgs_debug_violations sums them
+static __device__ unsigned long long g_rcgs_violations = 0;
+void register_violation_reader(unsigned long long (*fn)(bool reset));
+namespace {
+unsigned long long read_violations_tu(bool reset) {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, g_rcgs_violations, sizeof(v));
+    if (reset) {
+        const unsigned long long zero = 0;
+        cudaMemcpyToSymbol(g_rcgs_violations, &zero, sizeof(zero));
+    }
+    return v;
+}
+struct ViolationReg {
+    ViolationReg() { register_violation_reader(&read_violations_tu); }
+};
+static ViolationReg g_violation_reg;
+}  // namespace
+#define RCGS_DCHECK(cond)                                          \
+    do {                                                           \
+        if (!(cond)) atomicAdd(&::rcgs::g_rcgs_violations, 1ull); \
+    } while (0)
+#else
+#define RCGS_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 // ---- small device math ----------------------------------------------------------
 // world->camera transform exactly as numpy/OpenBLAS evaluates P @ R.T + t
 // (oracle/c/rcgs_oracle.c restates it).

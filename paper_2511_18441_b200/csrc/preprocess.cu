@@ -319,7 +319,8 @@ __global__ void k1_rank_kernel(const uint32_t* __restrict__ gid, int64_t k, cons
 // counts.  Slot order is the per-gaussian row-major tile order, as before.
 __global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __restrict__ rect,
                                const uint32_t* __restrict__ offs, int64_t k, int tiles_x,
-                               uint32_t* __restrict__ tile_key, uint32_t* __restrict__ emit_g) {
+                               uint32_t* __restrict__ tile_key, uint32_t* __restrict__ emit_g,
+                               int64_t k_total = INT64_MAX) {
     const int lane = threadIdx.x & 31;
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) >= k) return;  // whole warp beyond k
@@ -358,6 +359,7 @@ __global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __r
         if (p < total) {
             const uint32_t q = p - exL;
             const uint32_t ty = (uint32_t)y0L + q / wL, tx = (uint32_t)x0L + q % wL;
+            RCGS_DCHECK(tx < (uint32_t)tiles_x && gL < (uint32_t)k_total);
             tile_key[base + p] = ty * (uint32_t)tiles_x + tx;
             emit_g[base + p] = gL;
         }
@@ -696,7 +698,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&tkey_alt, pairs, s));
     RCGS_TRY(dalloc(&emit_g, pairs, s));
     RCGS_TRY(dalloc(&g_alt, pairs, s));
-    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g);
+    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g, v->n);
     RCGS_LAUNCH_CHECK();
     dfree(rect, s);
     int tile_bits = 1;

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kRNT) radix_downsweep_kernel(
             const K kk = sk[i];
             const uint32_t d = (uint32_t)(kk >> shift) & mask;
             const uint32_t pos = s_base[d] + (uint32_t)i - s_start[d];
+            RCGS_DCHECK(pos < (uint64_t)n);
             kout[pos] = kk;
             vout[pos] = sv[i];
         }

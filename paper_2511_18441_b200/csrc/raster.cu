@@ -124,6 +124,7 @@ struct RasterArgs {
     const double* z;
     unsigned* counter;
     int W, H, tiles_x, n_items;
+    int64_t n, pairs;  // scene size and tile-list pairs (checked builds' bounds)
     double alpha_clamp, alpha_skip, t_floor, tau;
     float f_alpha_clamp, f_floor, f_tau;
     float f_gate2;  // log2(alpha_skip): the alpha gate in log2 units
@@ -571,6 +572,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra, rcol = ra;
             if (j < range.y) {
                 s = st.pg[buf][lane];
+                RCGS_DCHECK(j < (uint64_t)a.pairs && s < (uint64_t)a.n);
                 ra = st.ra[lane];
                 keep = touches_block(ra, fbx0, fby0);
                 if (keep) {
@@ -612,7 +614,11 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 }
                 st.g[slot] = s;
                 st.j[slot] = j;
-                if (M == FWDREC) a.wrec_s[rbase + nrec + slot] = s;  // record ids, one per staged entry
+                if (M == FWDREC) {  // record ids, one per staged entry
+                    RCGS_DCHECK((uint64_t)rbase + nrec + slot < 8ull * (uint64_t)a.pairs &&
+                                nrec + slot < range.y - range.x);
+                    a.wrec_s[rbase + nrec + slot] = s;
+                }
             }
             __syncwarp();
             const int n = __popc(bal);
@@ -662,6 +668,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 } else if (M == CAP_WRITE) {
                     if (comp) {
                         const uint32_t o = cap_base + ncap++;
+                        RCGS_DCHECK(inside);
                         a.cap_pixel[o] = pix;
                         a.cap_kept[o] = a.rank_of[st.g[k]];  // the API reports depth ranks
                         a.cap_weight[o] = (double)wc;
@@ -775,6 +782,7 @@ struct RecArgs {
     const uint32_t* wrec_s;
     const float* wrec_w;
     const uint32_t* wrec_off;  // per-block first record (view-owned compact records) or null
+    int64_t n;                 // scene size (checked builds' bound)
     // render
     const float4* color;
     const float* t_in;
@@ -847,6 +855,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
                     wd[q] = ok ? __ldcs(a.wrec_w + (size_t)(m.base + r0 + q) * 32 + lane) : 0.f;
                 }
                 sd = (lane < kU && r0 + lane < m.n) ? a.wrec_s[m.base + r0 + lane] : 0u;
+                RCGS_DCHECK(!(lane < kU && r0 + lane < m.n) || sd < (uint32_t)a.n);
             };
             load(0, w, sl);
             for (uint32_t r0 = 0; r0 < m.n; r0 += kU) {
@@ -935,6 +944,7 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
                 const bool ok = r0 + q < n;
                 w[q] = ok ? __ldcs(a.wrec_w + (size_t)(base + r0 + q) * 32 + lane) : 0.f;
                 s[q] = ok ? a.wrec_s[base + r0 + q] : 0u;
+                RCGS_DCHECK(s[q] < (uint32_t)a.n);
             }
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
@@ -1086,6 +1096,7 @@ static RecArgs rec_args(const rcgs_view* v) {
     a.wrec_s = v->wrec_s;
     a.wrec_w = v->wrec_w;
     a.wrec_off = v->wrec_owned ? v->wrec_off : nullptr;
+    a.n = v->n;
     a.color = v->color;
     a.t_in = v->wrec_tf;
     return a;
@@ -1108,6 +1119,8 @@ static RasterArgs base_args(const rcgs_view* v) {
     a.H = v->cam.height;
     a.tiles_x = v->tiles_x;
     a.n_items = v->tiles_x * v->tiles_y * kBlocksPerTile;
+    a.n = v->n;
+    a.pairs = v->pairs;
     a.alpha_clamp = v->cfg.alpha_clamp;
     a.alpha_skip = v->cfg.alpha_skip;
     a.t_floor = v->cfg.transmittance_floor;

@@ -186,6 +186,53 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_
 extern "C" const char* rcgs_last_error(void) { return rcgs::last_error(); }
 extern "C" int rcgs_version(void) { return RCGS_VERSION; }
 
+#ifdef RCGS_CHECKED
+#include <vector>
+namespace rcgs {
+static std::vector<unsigned long long (*)(bool)>& violation_readers() {
+    static std::vector<unsigned long long (*)(bool)> v;
+    return v;
+}
+void register_violation_reader(unsigned long long (*fn)(bool)) { violation_readers().push_back(fn); }
+}  // namespace rcgs
+#endif
+
+#ifdef RCGS_CHECKED
+namespace rcgs {
+__global__ void debug_selftest_kernel(int fail) { RCGS_DCHECK(fail == 0); }
+}  // namespace rcgs
+#endif
+
+// Checked builds: one deliberate check (fail != 0 counts one violation), to
+// prove the counter works before a suite run relies on it reading zero.
+extern "C" int rcgs_debug_selftest(int fail) {
+#ifdef RCGS_CHECKED
+    rcgs::debug_selftest_kernel<<<1, 1>>>(fail);
+    RCGS_LAUNCH_CHECK();
+    return RCGS_OK;
+#else
+    (void)fail;
+    RCGS_CHECK_ARG(false, "release build: no device checks");
+#endif
+}
+
+// Checked builds: device bound-check failures since the last reset (and reset
+// them when reset != 0); returns RCGS_EINVAL in release builds, which have no checks.
+extern "C" int rcgs_debug_violations(uint64_t* h_count, int reset) {
+    RCGS_CHECK_ARG(h_count != nullptr, "null argument");
+#ifdef RCGS_CHECKED
+    RCGS_CUDA(cudaDeviceSynchronize());
+    unsigned long long v = 0;
+    for (auto fn : rcgs::violation_readers()) v += fn(reset != 0);
+    *h_count = v;
+    return RCGS_OK;
+#else
+    (void)reset;
+    *h_count = 0;
+    RCGS_CHECK_ARG(false, "release build: no device checks (build with EXTRA=-DRCGS_CHECKED)");
+#endif
+}
+
 extern "C" int rcgs_pool_reserve(int64_t bytes, void* stream) {
     RCGS_CHECK_ARG(bytes >= 0, "negative size");
     return rcgs::pool_reserve(bytes, rcgs::as_stream(stream));

@@ -81,3 +81,22 @@ def make_scene(specs, sh_degree=3):
     return SimpleNamespace(positions=np.array(pos).reshape(-1, 3), rotations=np.array(rot).reshape(-1, 4),
                            scales=np.array(scl).reshape(-1, 3), opacities=np.array(opa),
                            sh=np.array(sh).reshape(-1, 16, 3), sh_degree=sh_degree)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Checked library builds (RCGS_LIB_PATH=.../checked/librcgs.so, compiled with
+    -DRCGS_CHECKED): fail the run if any device bound check failed."""
+    path = os.environ.get("RCGS_LIB_PATH", "")
+    if "checked" not in path:
+        return
+    import ctypes
+    lib = ctypes.CDLL(path)
+    count = ctypes.c_uint64(0)
+    rc = lib.rcgs_debug_violations(ctypes.byref(count), 1)
+    # the counter itself: one deliberate failure must read back as 1
+    lib.rcgs_debug_selftest(1)
+    probe = ctypes.c_uint64(0)
+    lib.rcgs_debug_violations(ctypes.byref(probe), 1)
+    print(f"\nchecked build: rcgs_debug_violations rc={rc} count={count.value} (self-test reads {probe.value})")
+    if rc != 0 or count.value != 0 or probe.value != 1:
+        session.exitstatus = 1
