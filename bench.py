@@ -332,19 +332,23 @@ def run_gpu(args):
     roof = None if dom is None else dict(rooflines[dom], kernel=dom, traffic=traffic,
                 peak_kind=(peak_kind if rooflines[dom]["bound"] == "hbm" else "measured (rcgs_fp32_peak FFMA probe)"),
                 work_per_launch=stages["kernels"][dom].get("work"))
+    # raster unit = evaluated (pixel, entry) pair at ~16 FP32-pipe
+    # instructions; roof = FP32-pipe issue rate (128 lanes/SM/clk) at the live clock.
+    # Reported for the recording raster whichever kernel ranks first.
+    rwork = stages["kernels"].get("raster_fwd", {}).get("work") or {}
+    if rwork.get("evals") and "raster_fwd" in rooflines:
+        sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_gi = sms * 128 * sm_mhz * 1e6 / 1e9
+        ach_gi = rwork["evals"] * 16 / (rooflines["raster_fwd"]["ms_per_launch"] / 1000.0) / 1e9
+        rooflines["raster_fwd"]["issue_model"] = {"instr_per_eval": 16, "achieved_ginstr_s": round(ach_gi, 1),
+                                                  "peak_ginstr_s": round(peak_gi, 1),
+                                                  "frac": round(ach_gi / peak_gi, 4)}
     if roof is not None and roof["bound"] == "fp32":
         roof["note"] = ("FP32 FLOP roofline (algorithmic FLOPs / measured FFMA peak); the rasteriser is "
-                        "warp-issue bound (see profiles/, ~80% issue-active), so the FLOP fraction is low")
-        # raster unit = evaluated (pixel, entry) pair at ~16 FP32-pipe
-        # instructions; roof = FP32-pipe issue rate (128 lanes/SM/clk) at the live clock
-        work = stages["kernels"][dom].get("work") or {}
-        if work.get("evals"):
-            sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            peak_gi = sms * 128 * sm_mhz * 1e6 / 1e9
-            ach_gi = work["evals"] * 16 / (roof["ms_per_launch"] / 1000.0) / 1e9
-            roof["issue_model"] = {"instr_per_eval": 16, "achieved_ginstr_s": round(ach_gi, 1),
-                                   "peak_ginstr_s": round(peak_gi, 1), "frac": round(ach_gi / peak_gi, 4)}
+                        "warp-issue bound (see profiles/, ~76% issue-active), so the FLOP fraction is low")
+        if "issue_model" in rooflines.get(dom, {}):
+            roof["issue_model"] = rooflines[dom]["issue_model"]
         ncu = measured_stage_ncu().get(dom, {})
         if "sm_throughput_pct" in ncu:
             roof["ncu"] = {"kernel": ncu.get("top_kernel"), "sm_throughput_frac": round(ncu["sm_throughput_pct"] / 100, 4),

@@ -243,6 +243,12 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
 
 // ---------------------------------------------------------------- depth order, 32-bit keys
 constexpr int kRetryFullSort = 100;
+// depth keys: the top 24 varying bits of the rebased fp64 z (3 radix passes);
+// equal truncated keys are repaired by the exact fp64 key (depth_fixup_kernel)
+#ifndef RCGS_DEPTH_KEY_BITS
+#define RCGS_DEPTH_KEY_BITS 24
+#endif
+constexpr int kDepthKeyBits = RCGS_DEPTH_KEY_BITS;
 
 __global__ void key32_kernel(const uint64_t* __restrict__ key, int64_t k, uint64_t kmin, int shift,
                              uint32_t* __restrict__ k32) {
@@ -255,18 +261,40 @@ __global__ void key_rebase_kernel(uint64_t* __restrict__ key, int64_t k, uint64_
     if (i < k) key[i] -= kmin;
 }
 
-// Runs of equal top-32-bit keys (at most 32 long) are re-sorted by the full fp64
-// key, ties by scene index (the stable input order of np.argsort, render.py:216).
+// Runs of equal truncated keys are re-sorted by the full fp64 key, ties by scene
+// index (the stable input order of np.argsort, render.py:216): runs of at most 32
+// by one thread (insertion sort); longer ones, up to kLongRun, are queued for
+// long_run_sort_kernel (one CTA per run); longer still is left to the order check
+// (which then triggers the full 64-bit sort).
+constexpr int kLongRun = 2048;
+
 __global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ gid,
-                                   const uint64_t* __restrict__ key_of, int64_t k) {
+                                   const uint64_t* __restrict__ key_of, int64_t k, uint2* __restrict__ long_runs,
+                                   uint32_t* __restrict__ n_long, uint32_t max_long) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
     const uint32_t h = k32[i];
     if ((i > 0 && k32[i - 1] == h) || i + 1 >= k || k32[i + 1] != h) return;  // run starts only
     int64_t e = i + 1;
     while (e < k && k32[e] == h && e - i <= 32) ++e;
+    if (e - i > 32) {  // a long run (rare): queue it unless already in (key, index) order
+        uint32_t gp = gid[i];
+        uint64_t kp = key_of[gp];
+        bool sorted = true;
+        for (e = i + 1; e < k && k32[e] == h && e - i <= kLongRun; ++e) {
+            const uint32_t gc = gid[e];
+            const uint64_t kc = key_of[gc];
+            sorted = sorted && (kp < kc || (kp == kc && gp < gc));
+            gp = gc;
+            kp = kc;
+        }
+        if (!sorted && e - i <= kLongRun) {
+            const uint32_t slot = atomicAdd(n_long, 1u);
+            if (slot < max_long) long_runs[slot] = make_uint2((uint32_t)i, (uint32_t)(e - i));
+        }
+        return;
+    }
     const int len = (int)(e - i);
-    if (len > 32) return;  // long runs: verified by depth_check_kernel
     uint64_t kk[32];
     uint32_t gg[32];
     for (int a = 0; a < len; ++a) {
@@ -288,8 +316,59 @@ __global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* _
     for (int a = 0; a < len; ++a) gid[i + a] = gg[a];
 }
 
+// One CTA per queued long run: bitonic sort of its (fp64 key, scene index) pairs
+// in shared memory (padded to kLongRun with +inf keys); keys are unique per index,
+// so the result is the stable order.  Runs beyond the queue capacity are left to
+// the order check.
+__global__ void __launch_bounds__(1024) long_run_sort_kernel(uint32_t* __restrict__ gid,
+                                                             const uint64_t* __restrict__ key_of,
+                                                             const uint2* __restrict__ long_runs,
+                                                             const uint32_t* __restrict__ n_long, uint32_t max_long) {
+    __shared__ uint64_t sk[kLongRun];
+    __shared__ uint32_t sg[kLongRun];
+    const uint32_t nr = min(*n_long, max_long);
+    for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+        const uint2 run = long_runs[r];
+        int np2 = 64;  // the run padded to a power of two
+        while (np2 < (int)run.y) np2 <<= 1;
+        for (int a = threadIdx.x; a < np2; a += blockDim.x) {
+            if (a < (int)run.y) {
+                const uint32_t g = gid[run.x + a];
+                sg[a] = g;
+                sk[a] = key_of[g];
+            } else {
+                sg[a] = 0xffffffffu;
+                sk[a] = ~0ull;
+            }
+        }
+        __syncthreads();
+        for (int size = 2; size <= np2; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int a = threadIdx.x; a < np2; a += blockDim.x) {
+                    const int b = a ^ stride;
+                    if (b > a) {
+                        const bool up = (a & size) == 0;
+                        const bool gt = sk[a] > sk[b] || (sk[a] == sk[b] && sg[a] > sg[b]);
+                        if (gt == up) {
+                            const uint64_t tk = sk[a];
+                            sk[a] = sk[b];
+                            sk[b] = tk;
+                            const uint32_t tg = sg[a];
+                            sg[a] = sg[b];
+                            sg[b] = tg;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int a = threadIdx.x; a < (int)run.y; a += blockDim.x) gid[run.x + a] = sg[a];
+        __syncthreads();
+    }
+}
+
 // Flags any adjacent pair out of (fp64 key, index) order (only possible inside a
-// tie run longer than 32 with differing low bits).
+// tie run longer than kLongRun with differing low bits).
 __global__ void depth_check_kernel(const uint32_t* __restrict__ k32, const uint32_t* __restrict__ gid,
                                    const uint64_t* __restrict__ key_of, int64_t k, int32_t* __restrict__ bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -641,19 +720,29 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&fix_flag, 1, s));
     RCGS_CUDA(cudaMemsetAsync(fix_flag, 0, sizeof(int32_t), s));
     if (v->sort_bits > 0) {
-        if (v->sort_bits <= 32 || !v->full_sort) {
-            // 4-byte keys: the varying bits themselves (exact when <= 32 of them), else
-            // their top 32 bits followed by the tie-run repair and the order check
-            const int shift = v->sort_bits > 32 ? v->sort_bits - 32 : 0;
+        if (v->sort_bits <= kDepthKeyBits || !v->full_sort) {
+            // 4-byte keys holding the top kDepthKeyBits varying bits (3 radix passes;
+            // exact when the span has no more bits), then the tie-run repair of runs
+            // with equal truncated keys and the order check
+            const int shift = v->sort_bits > kDepthKeyBits ? v->sort_bits - kDepthKeyBits : 0;
             uint32_t *k32 = nullptr, *k32_alt = nullptr;
             RCGS_TRY(dalloc(&k32, k, s));
             RCGS_TRY(dalloc(&k32_alt, k, s));
             key32_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin, shift, k32);
             RCGS_TRY(radix_sort_u32(&k32, &k32_alt, &kgid, &kgid_alt, false, k,
-                                    v->sort_bits < 32 ? v->sort_bits : 32, s));
+                                    v->sort_bits < kDepthKeyBits ? v->sort_bits : kDepthKeyBits, s));
             if (shift > 0) {
-                depth_fixup_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k);
+                const uint32_t max_long = (uint32_t)(k / 33 + 1);
+                uint2* long_runs = nullptr;
+                uint32_t* n_long = nullptr;
+                RCGS_TRY(dalloc(&long_runs, max_long, s));
+                RCGS_TRY(dalloc(&n_long, 1, s));
+                RCGS_CUDA(cudaMemsetAsync(n_long, 0, sizeof(uint32_t), s));
+                depth_fixup_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k, long_runs, n_long, max_long);
+                long_run_sort_kernel<<<64, 1024, 0, s>>>(kgid, key, long_runs, n_long, max_long);
                 depth_check_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k, fix_flag);
+                dfree(long_runs, s);
+                dfree(n_long, s);
             }
             RCGS_LAUNCH_CHECK();
             dfree(k32, s);
