@@ -223,6 +223,73 @@ def test_loss_grad_local_differences_match_oracle():
     assert abs(lb.l1 - l1) < 1e-13 and abs(lb.ssim - ss) < 1e-12 and abs(lb.total - total) < 1e-12
 
 
+def _window_clean(img, tgt, radius):
+    """True where the (2 radius + 1)^2 window (zero padded) has img == tgt everywhere."""
+    from scipy.ndimage import maximum_filter
+    diff = np.any(img != tgt, axis=2).astype(np.uint8)
+    return maximum_filter(diff, size=2 * radius + 1, mode="constant", cval=0) == 0
+
+
+@pytest.mark.parametrize("shape", [(150, 170), (37, 300), (11, 11), (205, 64), (131, 129)])
+def test_device_loss_fp32_matches_oracle(shape):
+    """The optimizer's loss (rcgs_loss_grad: fp32 images and gradient, the fused
+    strip kernel) against the fp64 oracle: loss terms within 1e-12, gradient
+    within 1e-6 of its scale; exact zeros where the 21x21 window has no
+    difference, and identical images give (0, 1, 0) and an all-zero gradient."""
+    import torch
+    from paper_2511_18441_b200 import device as D
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    h, w = shape
+    img = rng.uniform(0.05, 0.95, (h, w, 3)).astype(np.float32)
+    tgt = img.copy()
+    # local edits (one straddling strip / band boundaries) plus a region of noise
+    tgt[h // 3:h // 3 + 7, w // 2 - 3:w // 2 + 4] *= np.float32(0.4)
+    tgt[-5:, -9:, 1] = np.clip(tgt[-5:, -9:, 1] + 0.1, 0, 1)
+    tgt[:3, :4, 2] = 0.0
+    for lam in (0.2, 0.0):
+        y_d = torch.from_numpy(img).cuda()
+        g_d = torch.from_numpy(tgt).cuda()
+        loss3, grad = D.loss_grad(y_d, g_d, lam)
+        l1, ss, total = (float(v) for v in loss3.cpu())
+        y64, g64 = img.astype(np.float64), tgt.astype(np.float64)
+        rl1, rss, rtotal = OL.photometric(y64, g64, lam=lam)
+        assert abs(l1 - rl1) < 1e-12 and abs(ss - rss) < 1e-12 and abs(total - rtotal) < 1e-12
+        ref = OL.loss_grad(y64, g64, lam=lam)
+        gd = grad.double().cpu().numpy()
+        assert np.abs(gd - ref).max() <= 1e-6 * np.abs(ref).max()
+        if lam > 0:
+            clean = _window_clean(img, tgt, 10)
+            assert np.all(gd[clean] == 0.0)
+            assert np.all(np.abs(ref[clean]) < 1e-15)
+    same = torch.from_numpy(img).cuda()
+    loss3, grad = D.loss_grad(same, same.clone(), 0.2)
+    assert [float(v) for v in loss3.cpu()] == [0.0, 1.0, 0.0]
+    assert torch.count_nonzero(grad).item() == 0
+
+
+def test_device_loss_fp32_full_hd_sampled():
+    """1080p (the C3 frame): fp32 fused loss vs the fp64 oracle on the whole frame
+    (loss terms) and the gradient everywhere."""
+    import torch
+    from paper_2511_18441_b200 import device as D
+    rng = np.random.default_rng(3)
+    h, w = 1080, 1920
+    img = rng.uniform(0.0, 1.0, (h, w, 3)).astype(np.float32)
+    tgt = img.copy()
+    tgt[200:700, 300:1500] = np.clip(tgt[200:700, 300:1500] * np.float32(0.7) + np.float32(0.1), 0, 1)
+    tgt[900:, :, 0] = rng.uniform(0.0, 1.0, (h - 900, w)).astype(np.float32)
+    loss3, grad = D.loss_grad(torch.from_numpy(img).cuda(), torch.from_numpy(tgt).cuda(), 0.2)
+    y64, g64 = img.astype(np.float64), tgt.astype(np.float64)
+    rl1, rss, rtotal = OL.photometric(y64, g64)
+    l1, ss, total = (float(v) for v in loss3.cpu())
+    assert abs(l1 - rl1) < 1e-12 and abs(ss - rss) < 1e-12 and abs(total - rtotal) < 1e-12
+    ref = OL.loss_grad(y64, g64)
+    gd = grad.double().cpu().numpy()
+    assert np.abs(gd - ref).max() <= 1e-6 * np.abs(ref).max()
+    clean = _window_clean(img, tgt, 10)
+    assert clean.any() and np.all(gd[clean] == 0.0)
+
+
 def test_backward_matches_oracle(two_blobs):
     scene = p_scene(two_blobs)
     intr, pose = p_cam(two_blobs, "v0_")
