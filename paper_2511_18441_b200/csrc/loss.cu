@@ -21,7 +21,6 @@
 // thread produces 4 rows of one column from 14 shared-memory rows).
 #include <math.h>
 
-#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -81,15 +80,21 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
     }
 }
 
+// The window in the gradient-map filter type (fp32 for the fp32 entry point).
+template <typename F>
+struct WindowT {
+    F w[kWin];
+};
+
 // Vertical 11-tap pass for kRows consecutive output rows of one column from a
 // horizontally filtered plane h[kLH][kLT] (rows r0 .. r0 + kRows + 9).
-__device__ __forceinline__ void vfilter(const double* __restrict__ h, int r0, int c, const Window& win,
-                                        double out[kRows]) {
+template <typename F, typename Win>
+__device__ __forceinline__ void vfilter(const F* __restrict__ h, int r0, int c, const Win& win, F out[kRows]) {
 #pragma unroll
-    for (int i = 0; i < kRows; ++i) out[i] = 0.0;
+    for (int i = 0; i < kRows; ++i) out[i] = F(0);
 #pragma unroll
     for (int rr = 0; rr < kRows + kWin - 1; ++rr) {
-        const double v = h[(r0 + rr) * kLT + c];
+        const F v = h[(r0 + rr) * kLT + c];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             const int k = rr - i;
@@ -228,15 +233,19 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
                 ig[i] = in ? g[gi] : T(0);
             }
             __syncthreads();
-            // horizontal pass: each thread a strip of kHS adjacent outputs of one row
-            // from a register-resident segment (squares formed once per input);
-            // every accumulator keeps its k = 0..10 FMA sequence
+            // horizontal pass: each item a strip of kHS adjacent outputs of one row
+            // from a register-resident segment (squares formed once per input) for
+            // one of three moment groups -- y (s1, s11), g (s2, s22), y g (s12) --
+            // so the 3 x 336 items spread evenly over the 256 threads; every
+            // accumulator keeps its k = 0..10 FMA sequence
             constexpr int kP = kLH * kLT;
-            for (int i = t; i < kLH * (kLT / kHS); i += kLNT) {
-                const int r = i / (kLT / kHS), c0 = (i % (kLT / kHS)) * kHS;
+            constexpr int kHI = kLH * (kLT / kHS);
+            for (int i = t; i < 3 * kHI; i += kLNT) {
+                const int kind = i / kHI, ii = i - kind * kHI;
+                const int r = ii / (kLT / kHS), c0 = (ii % (kLT / kHS)) * kHS;
                 double* out = hs + r * kLT + c0;
-                {
-                    const T* src = iy + r * kLH + c0;  // s1, s11 (image)
+                if (kind < 2) {
+                    const T* src = (kind == 0 ? iy : ig) + r * kLH + c0;  // s1, s11 / s2, s22
                     double x[kHS + kWin - 1], xx[kHS + kWin - 1];
 #pragma unroll
                     for (int j = 0; j < kHS + kWin - 1; ++j) {
@@ -251,31 +260,10 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
                             s1 = fma(win.w[k], x[o + k], s1);
                             s11 = fma(win.w[k], xx[o + k], s11);
                         }
-                        out[o] = s1;
-                        out[2 * kP + o] = s11;
+                        out[kind * kP + o] = s1;
+                        out[(2 + kind) * kP + o] = s11;
                     }
-                }
-                {
-                    const T* src = ig + r * kLH + c0;  // s2, s22 (target)
-                    double x[kHS + kWin - 1], xx[kHS + kWin - 1];
-#pragma unroll
-                    for (int j = 0; j < kHS + kWin - 1; ++j) {
-                        x[j] = (double)src[j];
-                        xx[j] = x[j] * x[j];
-                    }
-#pragma unroll
-                    for (int o = 0; o < kHS; ++o) {
-                        double s2 = 0, s22 = 0;
-#pragma unroll
-                        for (int k = 0; k < kWin; ++k) {
-                            s2 = fma(win.w[k], x[o + k], s2);
-                            s22 = fma(win.w[k], xx[o + k], s22);
-                        }
-                        out[kP + o] = s2;
-                        out[3 * kP + o] = s22;
-                    }
-                }
-                {
+                } else {
                     const T* sa = iy + r * kLH + c0;  // s12
                     const T* sb = ig + r * kLH + c0;
                     double xy[kHS + kWin - 1];
@@ -295,7 +283,7 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
         double m[5][kRows];
         if (SSIM) {
 #pragma unroll
-            for (int q = 0; q < 5; ++q) vfilter(hs + q * kLH * kLT, r0, c, win, m[q]);
+            for (int q = 0; q < 5; ++q) vfilter<double>(hs + q * kLH * kLT, r0, c, win, m[q]);
         }
         const int gx = x0 + c;
 #pragma unroll
@@ -350,14 +338,17 @@ __device__ __forceinline__ void cp_async_elem(E* dst, const E* src, bool in) {
 }
 
 // ---------------------------------------------------------------- pass B
+// The separable filter of the three maps runs in MT: fp64 for the fp64 entry
+// point, fp32 for the fp32 one (whose maps are already stored in fp32; the
+// combination with y and g below stays fp64).
 template <bool SSIM, typename T, typename G, typename MT>
 __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restrict__ y, const T* __restrict__ g, int H,
-                                                    int W, Window win, double lam,
+                                                    int W, WindowT<MT> win, double lam,
                                                     const MT* __restrict__ maps,
                                                     const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* hs = reinterpret_cast<double*>(smem_raw);   // [3][42][32]
-    MT* imb = reinterpret_cast<MT*>(hs + 3 * kLH * kLT); // [2][3][42][42]: double-buffered map planes
+    MT* hs = reinterpret_cast<MT*>(smem_raw);            // [3][42][32]
+    MT* imb = hs + 3 * kLH * kLT;                        // [2][3][42][42]: double-buffered map planes
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
@@ -404,17 +395,18 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
             __syncthreads();
             const MT* im = imb + (ch & 1) * 3 * kLH * kLH;
             // horizontal pass in kHS-output strips from register-resident segments
-            for (int i = t; i < kLH * (kLT / kHS); i += kLNT) {
-                const int r = i / (kLT / kHS), c0 = (i % (kLT / kHS)) * kHS;
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
+            constexpr int kHI = kLH * (kLT / kHS);
+            for (int i = t; i < 3 * kHI; i += kLNT) {  // items (map, row, strip): even spread
+                const int q = i / kHI, ii = i - q * kHI;
+                const int r = ii / (kLT / kHS), c0 = (ii % (kLT / kHS)) * kHS;
+                {
                     const MT* src = im + q * kLH * kLH + r * kLH + c0;
-                    double x[kHS + kWin - 1];
+                    MT x[kHS + kWin - 1];
 #pragma unroll
-                    for (int j = 0; j < kHS + kWin - 1; ++j) x[j] = (double)src[j];
+                    for (int j = 0; j < kHS + kWin - 1; ++j) x[j] = src[j];
 #pragma unroll
                     for (int o = 0; o < kHS; ++o) {
-                        double s = 0.0;
+                        MT s = MT(0);
 #pragma unroll
                         for (int k = 0; k < kWin; ++k) s = fma(win.w[k], x[o + k], s);
                         hs[q * kLH * kLT + r * kLT + c0 + o] = s;
@@ -423,10 +415,10 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
             }
             __syncthreads();
         }
-        double f[3][kRows];
+        MT f[3][kRows];
         if (SSIM && any) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) vfilter(hs + q * kLH * kLT, r0, c, win, f[q]);
+            for (int q = 0; q < 3; ++q) vfilter<MT>(hs + q * kLH * kLT, r0, c, win, f[q]);
         }
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
@@ -443,363 +435,12 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
             const double d = (double)fy - (double)fg;
             const double sgn = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == 0.0 ? 0.0 : d));
             double out = (1.0 - lam) * sgn / n;
-            if (SSIM) out -= lam * ((f[0][i] + 2.0 * (double)fy * f[1][i] + (double)fg * f[2][i]) / n);
+            if (SSIM)
+                out -= lam * (((double)f[0][i] + 2.0 * (double)fy * (double)f[1][i] + (double)fg * (double)f[2][i]) / n);
             grad[o] = (G)out;
         }
         if (SSIM && any) __syncthreads();
     }
-}
-
-// ---------------------------------------------------------------- fused loss
-// One kernel for the dirty test, pass A and pass B: a CTA walks a strip of kSW
-// output columns of one channel down a segment of rows, kB rows per band, with
-// rings in shared memory so every row is filtered once per strip:
-//   input band j (rows [12j+10, 12j+22) of the segment) -> ring (prefetched with
-//   cp.async one band ahead);
-//   step 2: vertical 11-tap filter of y, g, y^2, g^2, y g (fp64) for the map rows
-//           [12k+5, 12k+17) over kIW input columns (register sliding window);
-//   step 3: horizontal filter -> the five moments at kMW map columns -> SSIM map
-//           (summed over the strip's own pixels) and the three gradient maps
-//           M1..M3 (losses.py:104-115, collapsed as in the header) -> map ring;
-//   step 4: separable filter of M1..M3 (MT precision) for the output rows
-//           [12i, 12i+12) and the gradient (losses.py:118-134), L1 summed.
-// The gradient maps never leave shared memory (pass A wrote and pass B re-read
-// three full-image maps), and y / g are read once per strip.
-// Exactness where the result is exact in the reference: a map pixel whose
-// 11x11 input window has y == g everywhere has SSIM exactly 1 (a1 == b1 and
-// a2 == b2 bitwise, so the reference's division is 1); an output pixel whose
-// 21x21 window has y == g everywhere gets an exact 0 (the reference leaves
-// round-off residue there, and returns exact zeros for identical images,
-// losses.py:127-130).  The windows are tracked with per-pixel difference flags
-// that go through the same two separable passes (OR instead of FMA).
-namespace fl {
-constexpr int kSW = 64;                        // output columns per strip
-constexpr int kB = 12;                         // rows per band
-constexpr int kMW = kSW + 2 * kR;              // 74 map columns (col mc <-> x0 - 5 + mc)
-constexpr int kMS = 76;                        // map columns the 4-wide strips of step 3 cover (2 spare)
-constexpr int kIW = kMW + 2 * kR;              // 84 input columns (col ic <-> x0 - 10 + ic)
-constexpr int kIR = 3 * kB;                    // input ring rows: bands j-1, j and the prefetched j+1
-constexpr int kMR = 2 * kB;                    // map ring rows: bands k-1, k
-constexpr int kNT = 256;
-constexpr int kVG = 4;                         // map rows per thread in step 2 (three row groups)
-constexpr int kHS4 = 4;                        // adjacent outputs per thread in the horizontal passes
-// bank skew for rows read as 4-wide strips (one pad word per 16)
-__host__ __device__ constexpr int skew(int c) { return c + (c >> 4); }
-constexpr int kIWs = 92;                       // >= skew(kMS + 2 kR - 1) + 1: the strips read 2 spare columns
-constexpr int kMWs = 82;                       // >= skew(kMS - 1) + 1
-static_assert(skew(kMS + 2 * kR - 1) < kIWs && skew(kMS - 1) < kMWs, "skewed rows");
-constexpr int kVR = 3 * kMWs + 11;             // vmap row stride: 1 mod 32 words (fp32), so the two
-                                               // rows of a warp in step 4b use disjoint banks
-constexpr int kG4 = 96;                        // step 4a: threads per row group (warp aligned)
-constexpr int kR4 = kB / 2;                    // step 4a: rows per thread (two groups)
-static_assert(kMW <= kG4 && 2 * kG4 <= kNT, "step 4a mapping");
-static_assert(kB % kVG == 0 && (kB / kVG) * kIW <= kNT && (kMS / kHS4) * kB <= kNT && 3 * kMS <= kNT &&
-                  (kSW / kHS4) * kB <= kNT,
-              "threads");
-
-template <typename T, typename MT>
-struct Smem {
-    T in_y[kIR][kIW], in_g[kIR][kIW];          // input ring (col ic <-> x0 - 10 + ic)
-    double vmom[kB][5][kIWs];                  // step 2 -> 3: vertically filtered moments (skewed)
-    MT maps[kMR][3][kMWs];                     // map ring (col mc <-> x0 - 5 + mc, skewed)
-    MT vmap[kB][kVR];                          // step 4a -> 4b: [q * kMWs + skew(mc)] per row
-    double inv_mcol[kMWs];                     // (skewed)
-    uint8_t vd[kB][kIW + 4];                   // (2 spare columns read by the last strip)
-    uint8_t mflag[kMR][kMS];                   // map pixel's 11x11 window has a difference
-    uint8_t vflag[kB][kMS];                    // step 4a: a flagged map pixel within +-5 rows
-    double red[2 * kNT / 32];
-};
-
-struct Args {
-    int H, W, ch_count;
-    int seg_rows, nseg, nstrip;
-    double lam, n, inv_n, inv_full;
-    bool grad_ssim;
-    double* part;                              // 2 per job
-    LossTail lt;
-};
-
-__device__ __forceinline__ int mod(int a, int m) { return ((a % m) + m) % m; }
-__device__ __forceinline__ uint32_t win11(uint32_t bits, int o) { return (bits >> o) & 0x7ffu; }
-
-}  // namespace fl
-
-// W2: the window in MT (float for the fp32 entry point)
-template <typename MT>
-struct WindowT {
-    MT w[kWin];
-};
-
-template <typename T, typename G, typename MT>
-__global__ void __launch_bounds__(fl::kNT, sizeof(MT) == 4 ? 2 : 1)
-    loss_fused_kernel(const T* __restrict__ y, const T* __restrict__ g, Window win, WindowT<MT> wm, fl::Args a,
-                      G* __restrict__ grad) {
-    using namespace fl;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem<T, MT>& sm = *reinterpret_cast<Smem<T, MT>*>(smem_raw);
-    const int t = threadIdx.x;
-    // job = (strip, segment, channel), channel fastest: the three channel jobs of a
-    // strip read the same lines, adjacent in time (L2)
-    const int job = blockIdx.x;
-    const int ch = job % 3, seg = (job / 3) % a.nseg, strip = job / (3 * a.nseg);
-    const int H = a.H, W = a.W;
-    const int x0 = strip * kSW;
-    const int R0 = seg * a.seg_rows, R1 = min(H, R0 + a.seg_rows);
-    const int nb = (R1 - R0 + kB - 1) / kB;
-
-    if (t < kMS) {
-        const int gx = x0 - kR + t;
-        sm.inv_mcol[skew(t)] = (t < kMW && gx >= 0 && gx < W) ? 1.0 / mass1d(win, gx, W) : 0.0;
-    }
-    // the spare columns the last 4-wide strip reads (their outputs are never used)
-    for (int e = t; e < kB * 5; e += kNT) {
-        const int rr = e / 5, q = e % 5;
-        for (int c = kIW; c < kMS + 2 * kR; ++c) sm.vmom[rr][q][skew(c)] = 0.0;
-    }
-    if (t < kB) {
-        for (int c = kIW; c < kIW + 4; ++c) sm.vd[t][c] = 0;
-    }
-    // input band j: segment rows [12j + 10, 12j + 22) -> ring rows [12 (j mod 3), +12)
-    auto load_band = [&](int j) {
-        const int rbase = mod(j, 3) * kB;
-        for (int e = t; e < kB * kIW; e += kNT) {
-            const int rr = e / kIW, ic = e - rr * kIW;
-            const int gy = R0 + kB * j + 10 + rr, gx = x0 - 2 * kR + ic;
-            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const int64_t o = in ? ((int64_t)gy * W + gx) * 3 + ch : 0;
-            cp_async_elem(&sm.in_y[rbase + rr][ic], y + o, in);
-            cp_async_elem(&sm.in_g[rbase + rr][ic], g + o, in);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-
-    double l1 = 0.0, ss = 0.0;
-
-    // step 2 + 3 for map band k (segment rows [12k+5, 12k+17))
-    auto map_band = [&](int k) {
-        if (t < (kB / kVG) * kIW) {
-            const int ic = t % kIW, gp = t / kIW;
-            double acc[5][kVG];
-#pragma unroll
-            for (int q = 0; q < 5; ++q)
-#pragma unroll
-                for (int o = 0; o < kVG; ++o) acc[q][o] = 0.0;
-            uint32_t dbits = 0;
-            // ring row of tap 0 of output 0 (segment row 12k + 4gp); rows wrap once at most
-            const int rb = mod(kB * k + kVG * gp - 10, kIR);
-#pragma unroll
-            for (int q = 0; q < kVG + kWin - 1; ++q) {
-                const int rr = rb + q >= kIR ? rb + q - kIR : rb + q;
-                const T ty = sm.in_y[rr][ic], tg = sm.in_g[rr][ic];
-                dbits |= (uint32_t)(ty != tg) << q;
-                const double yv = (double)ty, gv = (double)tg;
-                const double v[5] = {yv, gv, yv * yv, gv * gv, yv * gv};
-#pragma unroll
-                for (int o = 0; o < kVG; ++o) {
-                    const int kk = q - o;
-                    if (kk >= 0 && kk < kWin) {
-#pragma unroll
-                        for (int m = 0; m < 5; ++m) acc[m][o] = fma(win.w[kk], v[m], acc[m][o]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 0; o < kVG; ++o) {
-                const int rr = kVG * gp + o;
-#pragma unroll
-                for (int m = 0; m < 5; ++m) sm.vmom[rr][m][skew(ic)] = acc[m][o];
-                sm.vd[rr][ic] = win11(dbits, o) != 0u;
-            }
-        }
-        __syncthreads();
-        if (t < (kMS / kHS4) * kB) {
-            // strips 0..15 of a row in one half-warp (the 8-byte loads of a half-warp
-            // are conflict-free on the skewed rows), the 3 remaining strips after them
-            const int rr = t < 16 * kB ? t >> 4 : (t - 16 * kB) / 3;
-            const int s = t < 16 * kB ? t & 15 : 16 + (t - 16 * kB) % 3;
-            const int m = kB * k + 5 + rr;  // segment map row
-            const int gy = R0 + m;
-            const bool row_in = gy >= 0 && gy < H;
-            double mo[5][kHS4];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                double v[kHS4 + kWin - 1];
-#pragma unroll
-                for (int j = 0; j < kHS4 + kWin - 1; ++j) v[j] = sm.vmom[rr][q][skew(kHS4 * s + j)];
-#pragma unroll
-                for (int o = 0; o < kHS4; ++o) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int kk = 0; kk < kWin; ++kk) acc = fma(win.w[kk], v[o + kk], acc);
-                    mo[q][o] = acc;
-                }
-            }
-            uint32_t fbits = 0;
-#pragma unroll
-            for (int j = 0; j < kHS4 + kWin - 1; ++j) fbits |= (uint32_t)sm.vd[rr][kHS4 * s + j] << j;
-            const double inv_mrow =
-                !row_in ? 0.0 : (gy >= kR && gy < H - kR) ? a.inv_full : 1.0 / mass1d(win, gy, H);
-            const int mrr = mod(m - 5, kMR);
-            const bool row_core = m >= 0 && m < R1 - R0;
-#pragma unroll
-            for (int o = 0; o < kHS4; ++o) {
-                const int mc = kHS4 * s + o;
-                const int gx = x0 - kR + mc;
-                const bool in = row_in && mc < kMW && gx >= 0 && gx < W;
-                const bool dirty = win11(fbits, o) != 0u;
-                double M1 = 0.0, M2 = 0.0, M3 = 0.0;
-                if (in) {
-                    const double im = inv_mrow * sm.inv_mcol[skew(mc)];
-                    const double mu1 = mo[0][o] * im, mu2 = mo[1][o] * im;
-                    const double var1 = mo[2][o] * im - mu1 * mu1;
-                    const double var2 = mo[3][o] * im - mu2 * mu2;
-                    const double cov = mo[4][o] * im - mu1 * mu2;
-                    const double a1 = 2.0 * mu1 * mu2 + 1e-4, a2 = 2.0 * cov + 9e-4;
-                    const double b1 = mu1 * mu1 + mu2 * mu2 + 1e-4, b2 = var1 + var2 + 9e-4;
-                    const double ib = 1.0 / (b1 * b2), ib1 = b2 * ib, ib2 = b1 * ib;
-                    const double a12 = a1 * a2;
-                    if (row_core && mc >= kR && mc < kR + kSW) ss += dirty ? a12 * ib : 1.0;
-                    const double d_mu1 = 2.0 * (mu2 * a2) * ib - 2.0 * mu1 * a12 * ib * ib1;
-                    const double d_var1 = -a12 * ib * ib2;
-                    const double d_cov = 2.0 * a1 * ib;
-                    M1 = (d_mu1 - 2.0 * d_var1 * mu1 - d_cov * mu2) * im;
-                    M2 = d_var1 * im;
-                    M3 = d_cov * im;
-                }
-                sm.maps[mrr][0][skew(mc)] = (MT)M1;
-                sm.maps[mrr][1][skew(mc)] = (MT)M2;
-                sm.maps[mrr][2][skew(mc)] = (MT)M3;
-                sm.mflag[mrr][mc] = in && dirty;
-            }
-        }
-    };
-
-    // prologue: input bands -2, -1 (and 0 prefetched), map band -1
-    load_band(-2);
-    load_band(-1);
-    load_band(0);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncthreads();
-    map_band(-1);
-    for (int i = 0; i < nb; ++i) {
-        load_band(i + 1);  // into band i-2's slot (last read in iteration i-1)
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();  // band i landed; map band i-1 written
-        map_band(i);
-        __syncthreads();
-        // step 4a: vertical filter of the maps for output rows [12i, 12i+12)
-        if (a.grad_ssim && t < 2 * kG4 && t % kG4 < kMW) {
-            const int mc = t % kG4, gp = t / kG4;  // rows kR4 gp .. kR4 gp + kR4 - 1
-            MT f[3][kR4];
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-#pragma unroll
-                for (int o = 0; o < kR4; ++o) f[q][o] = MT(0);
-            uint32_t fb = 0;
-            const int mb = mod(kB * i + kR4 * gp - kR - 5, kMR);  // ring row of segment map row 12i + 6gp - 5
-#pragma unroll
-            for (int q = 0; q < kR4 + kWin - 1; ++q) {
-                const int mr = mb + q >= kMR ? mb + q - kMR : mb + q;
-                const MT v0 = sm.maps[mr][0][skew(mc)], v1 = sm.maps[mr][1][skew(mc)], v2 = sm.maps[mr][2][skew(mc)];
-                fb |= (uint32_t)sm.mflag[mr][mc] << q;
-#pragma unroll
-                for (int o = 0; o < kR4; ++o) {
-                    const int kk = q - o;
-                    if (kk >= 0 && kk < kWin) {
-                        f[0][o] = fma(wm.w[kk], v0, f[0][o]);
-                        f[1][o] = fma(wm.w[kk], v1, f[1][o]);
-                        f[2][o] = fma(wm.w[kk], v2, f[2][o]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 0; o < kR4; ++o) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) sm.vmap[kR4 * gp + o][q * kMWs + skew(mc)] = f[q][o];
-                sm.vflag[kR4 * gp + o][mc] = win11(fb, o) != 0u;
-            }
-        }
-        __syncthreads();
-        // step 4b: horizontal filter + gradient for output rows [12i, 12i+12)
-        if (t < (kSW / kHS4) * kB) {
-            const int rr = t / (kSW / kHS4), s = t % (kSW / kHS4);
-            const int r = kB * i + rr;
-            const int gy = R0 + r;
-            if (gy < R1) {
-                double f[3][kHS4];
-                uint32_t fb = 0;
-                if (a.grad_ssim) {
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        MT v[kHS4 + kWin - 1];
-#pragma unroll
-                        for (int j = 0; j < kHS4 + kWin - 1; ++j) v[j] = sm.vmap[rr][q * kMWs + skew(kHS4 * s + j)];
-#pragma unroll
-                        for (int o = 0; o < kHS4; ++o) {
-                            MT acc = MT(0);
-#pragma unroll
-                            for (int kk = 0; kk < kWin; ++kk) acc = fma(wm.w[kk], v[o + kk], acc);
-                            f[q][o] = (double)acc;
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < kHS4 + kWin - 1; ++j) fb |= (uint32_t)sm.vflag[rr][kHS4 * s + j] << j;
-                }
-                const int ir = mod(r - 10, kIR);
-                const double cl1 = (1.0 - a.lam) * a.inv_n, cs = a.lam * a.inv_n;
-#pragma unroll
-                for (int o = 0; o < kHS4; ++o) {
-                    const int c = kHS4 * s + o;
-                    const int gx = x0 + c;
-                    if (gx >= W) continue;
-                    const T fy = sm.in_y[ir][c + 2 * kR], fg = sm.in_g[ir][c + 2 * kR];
-                    const double d = (double)fy - (double)fg;
-                    l1 += fabs(d);
-                    // np.sign(y - gt): NaN propagates (optimize.py:72-74 rejects the step)
-                    const double sgn = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == 0.0 ? 0.0 : d));
-                    double out = cl1 * sgn;
-                    if (a.grad_ssim) {
-                        if (win11(fb, o) == 0u) {
-                            out = 0.0;  // 21x21 window without a difference: exactly zero
-                        } else {
-                            out -= cs * (f[0][o] + 2.0 * (double)fy * f[1][o] + (double)fg * f[2][o]);
-                        }
-                    }
-                    grad[((int64_t)gy * W + gx) * 3 + ch] = (G)out;
-                }
-            }
-        }
-        __syncthreads();  // vmom / vmap / ring slots are reused by the next band
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    block_sum2(l1, ss, sm.red);
-    if (t == 0) {
-        a.part[2 * job] = l1;
-        a.part[2 * job + 1] = ss;
-    }
-    __syncthreads();
-    loss_tail(a.part, gridDim.x, a.lt, sm.red);
-}
-
-// Images smaller than the SSIM window (lam must be 0): L1 and its sign gradient.
-template <typename T, typename G>
-__global__ void __launch_bounds__(kLNT) loss_l1_kernel(const T* __restrict__ y, const T* __restrict__ g, int64_t n3,
-                                                       double* __restrict__ part, G* __restrict__ grad, LossTail lt) {
-    __shared__ double red[2 * kLNT / 32];
-    double l1 = 0.0, zero = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)kLNT + threadIdx.x; i < n3; i += (int64_t)gridDim.x * kLNT) {
-        const double d = (double)y[i] - (double)g[i];
-        l1 += fabs(d);
-        const double sgn = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == 0.0 ? 0.0 : d));
-        grad[i] = (G)((1.0 - lt.lam) * sgn / lt.n);
-    }
-    block_sum2(l1, zero, red);
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = l1;
-        part[2 * blockIdx.x + 1] = 0.0;
-    }
-    __syncthreads();
-    loss_tail(part, gridDim.x, lt, red);
 }
 
 static Window make_window() {
@@ -864,7 +505,9 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     lt.out3 = d_loss3;
     loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty);
     const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
-    const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(double);
+    const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(MT);
+    WindowT<MT> wm;
+    for (int k = 0; k < kWin; ++k) wm.w[k] = (MT)win.w[k];
     if (ssim_ok) {
         RCGS_TRY(dalloc(&maps, 3 * npix * 3, s));
         RCGS_CUDA(cudaFuncSetAttribute(loss_pass_a<true, T, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -875,17 +518,17 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
                                                             lt);
         RCGS_LAUNCH_CHECK();
         if (lam > 0.0) {
-            loss_pass_b<true, T, G, MT><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, win, lam, maps,
+            loss_pass_b<true, T, G, MT><<<grid, kLNT, smem_b, s>>>(d_image, d_target, height, width, wm, lam, maps,
                                                                    dirty, d_grad);
         } else {
-            loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, maps,
+            loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, wm, lam, maps,
                                                                dirty, d_grad);
         }
         RCGS_LAUNCH_CHECK();
     } else {
         loss_pass_a<false, T, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, nullptr, part,
                                                          dirty, lt);
-        loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, win, lam, nullptr,
+        loss_pass_b<false, T, G, MT><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, wm, lam, nullptr,
                                                            dirty, d_grad);
         RCGS_LAUNCH_CHECK();
     }
@@ -895,99 +538,12 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     return RCGS_OK;
 }
 
-// The fused path (default; RCGS_LOSS_LEGACY=1 selects the three-kernel path above
-// for A/B measurements).
-static bool loss_legacy() {
-    static const bool v = [] {
-        const char* e = getenv("RCGS_LOSS_LEGACY");
-        return e && atoi(e) != 0;
-    }();
-    return v;
-}
-
-template <typename T, typename G, typename MT>
-static int loss_fused_impl(const T* d_image, const T* d_target, int32_t height, int32_t width, double lam,
-                           double* d_loss3, G* d_grad, void* stream) {
-    RCGS_CHECK_ARG(d_image && d_target && d_loss3 && d_grad, "null argument");
-    RCGS_CHECK_ARG(height > 0 && width > 0, "expected (H, W, 3) images, got (%d, %d, 3)", height, width);
-    RCGS_CHECK_ARG(lam >= 0.0 && lam <= 1.0, "lam must be in [0, 1]");
-    const bool ssim_ok = height >= kWin && width >= kWin;
-    RCGS_CHECK_ARG(ssim_ok || lam == 0.0, "images must be at least %dpx on each side for SSIM", kWin);
-    cudaStream_t s = as_stream(stream);
-    const Window win = make_window();
-    const int64_t npix = (int64_t)height * width;
-    LossTail lt;
-    lt.ticket = stream_ticket(s);
-    RCGS_CHECK_ARG(lt.ticket != nullptr, "loss ticket allocation failed");
-    lt.n = (double)(npix * 3);
-    lt.lam = lam;
-    lt.ssim_valid = ssim_ok;
-    lt.out3 = d_loss3;
-    double* part = nullptr;
-    if (!ssim_ok) {
-        const int nb = (int)std::min<int64_t>(div_up(npix * 3, kLNT), 1024);
-        RCGS_TRY(dalloc(&part, 2 * nb, s));
-        loss_l1_kernel<T, G><<<nb, kLNT, 0, s>>>(d_image, d_target, npix * 3, part, d_grad, lt);
-        RCGS_LAUNCH_CHECK();
-        dfree(part, s);
-        return RCGS_OK;
-    }
-    using SM = fl::Smem<T, MT>;
-    auto kern = loss_fused_kernel<T, G, MT>;
-    static int slots = 0;  // resident CTAs on the device (per instantiation)
-    if (slots == 0) {
-        RCGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SM)));
-        int dev = 0, sms = 0, per_sm = 0;
-        RCGS_CUDA(cudaGetDevice(&dev));
-        RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fl::kNT, sizeof(SM)));
-        slots = std::max(1, sms * per_sm);
-    }
-    fl::Args a;
-    a.H = height;
-    a.W = width;
-    a.ch_count = 3;
-    a.nstrip = (int)div_up(width, fl::kSW);
-    // row segments: about one wave of (strip, segment, channel) jobs over the
-    // resident CTA slots (each segment re-filters one 12-row band above it)
-    const int bands = (int)div_up(height, fl::kB);
-    const int want = std::max(1, std::min(bands, slots / (3 * a.nstrip)));
-    static const int max_seg_bands = [] {
-        const char* e = getenv("RCGS_LOSS_SEG_BANDS");
-        return e ? std::max(1, atoi(e)) : 1 << 20;
-    }();
-    const int seg_bands = std::min((int)div_up(bands, want), max_seg_bands);
-    a.seg_rows = seg_bands * fl::kB;
-    a.nseg = (int)div_up(height, a.seg_rows);
-    a.lam = lam;
-    a.n = lt.n;
-    a.inv_n = 1.0 / lt.n;
-    double full = 0.0;
-    for (int k = 0; k < kWin; ++k) full += win.w[k];
-    a.inv_full = 1.0 / full;
-    a.grad_ssim = lam > 0.0;
-    const int jobs = a.nstrip * a.nseg * 3;
-    RCGS_TRY(dalloc(&part, 2 * jobs, s));
-    a.part = part;
-    a.lt = lt;
-    WindowT<MT> wm;
-    for (int k = 0; k < kWin; ++k) wm.w[k] = (MT)win.w[k];
-    kern<<<jobs, fl::kNT, sizeof(SM), s>>>(d_image, d_target, win, wm, a, d_grad);
-    RCGS_LAUNCH_CHECK();
-    dfree(part, s);
-    return RCGS_OK;
-}
-
 extern "C" int rcgs_loss_grad(const float* d_image, const float* d_target, int32_t height, int32_t width,
                               double lam, double* d_loss3, float* d_grad, void* stream) {
-    if (loss_legacy())
-        return loss_grad_impl<float, float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
-    return loss_fused_impl<float, float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
+    return loss_grad_impl<float, float, float>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
 }
 
 extern "C" int rcgs_loss_grad_f64(const double* d_image, const double* d_target, int32_t height,
                                   int32_t width, double lam, double* d_loss3, double* d_grad, void* stream) {
-    if (loss_legacy())
-        return loss_grad_impl<double, double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
-    return loss_fused_impl<double, double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
+    return loss_grad_impl<double, double, double>(d_image, d_target, height, width, lam, d_loss3, d_grad, stream);
 }

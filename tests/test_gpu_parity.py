@@ -232,10 +232,12 @@ def _window_clean(img, tgt, radius):
 
 @pytest.mark.parametrize("shape", [(150, 170), (37, 300), (11, 11), (205, 64), (131, 129)])
 def test_device_loss_fp32_matches_oracle(shape):
-    """The optimizer's loss (rcgs_loss_grad: fp32 images and gradient, the fused
-    strip kernel) against the fp64 oracle: loss terms within 1e-12, gradient
-    within 1e-6 of its scale; exact zeros where the 21x21 window has no
-    difference, and identical images give (0, 1, 0) and an all-zero gradient."""
+    """The optimizer's loss (rcgs_loss_grad: fp32 images and gradient, fp32
+    gradient maps between the passes) against the fp64 oracle: loss terms within
+    1e-12, gradient within 1e-6 of its scale; where the 21x21 window has no
+    difference the gradient is zero up to the reference's own round-off residue
+    (exactly zero beyond one 32-px block of a difference), and identical images
+    give (0, 1, 0) and an all-zero gradient."""
     import torch
     from paper_2511_18441_b200 import device as D
     rng = np.random.default_rng(shape[0] * 1000 + shape[1])
@@ -259,8 +261,8 @@ def test_device_loss_fp32_matches_oracle(shape):
         assert np.abs(gd - ref).max() <= 1e-6 * np.abs(ref).max()
         if lam > 0:
             clean = _window_clean(img, tgt, 10)
-            assert np.all(gd[clean] == 0.0)
             assert np.all(np.abs(ref[clean]) < 1e-15)
+            assert np.all(np.abs(gd[clean]) < 1e-15)
     same = torch.from_numpy(img).cuda()
     loss3, grad = D.loss_grad(same, same.clone(), 0.2)
     assert [float(v) for v in loss3.cpu()] == [0.0, 1.0, 0.0]
@@ -287,7 +289,7 @@ def test_device_loss_fp32_full_hd_sampled():
     gd = grad.double().cpu().numpy()
     assert np.abs(gd - ref).max() <= 1e-6 * np.abs(ref).max()
     clean = _window_clean(img, tgt, 10)
-    assert clean.any() and np.all(gd[clean] == 0.0)
+    assert clean.any() and np.all(np.abs(gd[clean]) < 1e-15)
 
 
 def test_backward_matches_oracle(two_blobs):

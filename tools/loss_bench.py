@@ -1,6 +1,6 @@
 """Standalone timing of the optimizer's loss (rcgs_loss_grad, fp32) on a 1080p
-frame pair: mean of CUDA-event timed launches after warm-up.  Run twice with
-RCGS_LOSS_LEGACY=0/1 to A/B the fused strip kernel against the three-kernel path."""
+frame pair: mean of CUDA-event timed launches after warm-up (L2 flushed between
+launches)."""
 import json
 import os
 import sys
@@ -32,7 +32,7 @@ def main():
         e.record()
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e) * 1e3)
-    print(json.dumps({"legacy": os.environ.get("RCGS_LOSS_LEGACY", "0"), "us_mean": round(float(np.mean(times)), 1),
+    print(json.dumps({"us_mean": round(float(np.mean(times)), 1),
                       "us_p50": round(float(np.median(times)), 1), "loss": [float(v) for v in loss3.cpu()]}))
 
 
