@@ -175,6 +175,87 @@ struct __align__(16) RasterRec {
                //                                nA = -a/2 log2 e, nB = -b log2 e, nC = -c/2 log2 e)
 };
 
+// 8-bit mask of the 8x4 pixel blocks (bit = (y / 4) * 2 + x / 8 within the 16x16
+// tile whose top-left pixel is (tx0, ty0)) that the footprint {power2 >= p_lo} of
+// record r can reach: the per-block cull of the raster, done once per (gaussian,
+// tile) pair at view build.  Q = -power2 = A dx^2 + B dx dy + C dy^2 (PD); for
+// each 4-row block row the footprint's x extent over that row band is exact in
+// closed form (x_r(dy) concave with its maximiser at dy = -B sqrt(T / (C D)),
+// x_l convex, D = 4AC - B^2), compared with the two 8-column blocks.  The
+// result must be a superset of the blocks where some pixel has fp64 alpha at or
+// above the gate, so every rounding is covered with wide margins: T is raised
+// by the cull's evaluation bound (2e-6 of the absolute term sum, which is at
+// most (1 + r) / (1 - r) times Q for r = |B| / (2 sqrt(AC)), plus 2e-4 >= the
+// raster's 1.5e-4), the extents are widened by 1e-3 relative + 0.02 px, the row
+// bands by 0.01 px; near-degenerate footprints (r >= 0.999) and NaN take every
+// block.  The raster's checked build re-tests every dropped (entry, block)
+// against its exact per-block test.
+// Tile-list values: scene index in the low kIdxBits bits and the pair's 8-bit
+// block mask above them (scenes below 2^24 gaussians; larger scenes keep plain
+// indices and a separate mask array).
+constexpr int kIdxBits = 24;
+constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
+
+__device__ __forceinline__ float approx_sqrt(float x) {  // MUFU; relative error ~1e-7, x >= 0
+    x = fmaxf(x, 1e-30f);
+    return x * rsqrtf(x);
+}
+// Per-gaussian part of the block-mask test (view build, once per kept gaussian):
+// m0 = (mx, my, ey, dR), m1 = (B, D, 4AT, 1/(2A)); ey < 0 encodes the special
+// cases (-1: every block, -2: none).
+struct MaskRec {
+    float4 m0, m1;
+};
+
+__device__ __forceinline__ MaskRec mask_setup(const float4 ra, const float4 rb, const float4 rc) {
+    MaskRec q;
+    q.m0 = make_float4(0.f, 0.f, -1.f, 0.f);
+    q.m1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float A = -rc.x, B = -rc.y, C = -rc.z, T0 = -rb.z;
+    if (!(A > 0.f && C > 0.f)) return q;
+    const float r = fabsf(B) * rsqrtf(4.f * A * C);
+    if (!(r < 0.999f) || !(T0 == T0)) return q;
+    const float T = T0 + fabsf(T0) * fmaf(2e-6f, __fdividef(1.f + r, 1.f - r), 1e-5f) + 2e-4f;
+    if (T < 0.f) {
+        q.m0.z = -2.f;
+        return q;
+    }
+    const float D = fmaf(4.f * A, C, -B * B);
+    const float AT4 = 4.f * A * T;
+    const float ey = approx_sqrt(__fdividef(AT4, D)) * 1.0001f;  // |dy| reach
+    const float kq = approx_sqrt(__fdividef(T, C * D));
+    q.m0 = make_float4(ra.x + rb.x, ra.y + rb.y, ey, -B * kq);  // dR: maximiser of x_r (x_l: -dR)
+    q.m1 = make_float4(B, D, AT4, __fdividef(0.5f, A));
+    return q;
+}
+
+__device__ __forceinline__ uint32_t tile_block_mask(const MaskRec& q, float tx0, float ty0) {
+    const float mx = q.m0.x, my = q.m0.y, ey = q.m0.z, dR = q.m0.w;
+    const float B = q.m1.x, D = q.m1.y, AT4 = q.m1.z, inv2A = q.m1.w;
+    if (ey < 0.f) return ey == -1.f ? 0xffu : 0u;
+    const float dt0 = (ty0 - 0.01f) - my;
+    if (dt0 > ey || dt0 + 15.02f < -ey) return 0u;  // no row of the tile in reach
+    uint32_t mask = 0u;
+#pragma unroll
+    for (int by = 0; by < 4; ++by) {
+        const float lo = fmaxf(dt0 + 4.f * by, -ey), hi = fminf(dt0 + (4.f * by + 3.02f), ey);
+        if (lo > hi) continue;
+        const float dr = fminf(fmaxf(dR, lo), hi), dl = fminf(fmaxf(-dR, lo), hi);
+        const float xr = (-B * dr + approx_sqrt(fmaf(-D * dr, dr, AT4))) * inv2A;
+        const float xl = (-B * dl - approx_sqrt(fmaf(-D * dl, dl, AT4))) * inv2A;
+        const float m = fmaf(1e-3f, fabsf(xl) + fabsf(xr), 0.02f);
+        const float X0 = (mx + xl) - m, X1 = (mx + xr) + m;
+        if (!(X1 < tx0 || X0 > tx0 + 7.f)) mask |= 1u << (2 * by);
+        if (!(X1 < tx0 + 8.f || X0 > tx0 + 15.f)) mask |= 2u << (2 * by);
+    }
+    return mask;
+}
+
+__device__ __forceinline__ uint32_t tile_block_mask(const float4 ra, const float4 rb, const float4 rc, float tx0,
+                                                    float ty0) {
+    return tile_block_mask(mask_setup(ra, rb, rc), tx0, ty0);
+}
+
 // Exact (fp64) record for guarded decisions: the reference's own operands.
 struct ExactRec {
     double mx, my, ca, cb, cc, op;
@@ -198,6 +279,9 @@ struct rcgs_view {
     int32_t* rank_of;     // (n,) s or -1 (culled)
     // per pair (sorted by tile, then depth)
     uint32_t* pair_g;     // (pairs,) scene index g
+    uint32_t* pair_m;     // (pairs,) tile_block_mask of the pair (8x4 blocks its footprint reaches);
+                          // null when packed into pair_g (pair_packed: g | mask << kIdxBits)
+    bool pair_packed;
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
     unsigned* work;       // (2,) work-item / exited-warp counters of the persistent launches

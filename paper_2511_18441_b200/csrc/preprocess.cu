@@ -148,7 +148,8 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
                                rcgs_raster_config cfg, uint32_t* __restrict__ flag, uint64_t* __restrict__ key,
                                unsigned long long* __restrict__ minmax, double* __restrict__ z_out,
                                RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
-                               Rect* __restrict__ rect, uint32_t* __restrict__ count) {
+                               Rect* __restrict__ rect, uint32_t* __restrict__ count,
+                               MaskRec* __restrict__ mrec) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (g < n) {
@@ -198,6 +199,7 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
                               (float)((P + margin) * kL));
             r.c = make_float4((float)(-0.5 * ca * kL), (float)(-cb * kL), (float)(-0.5 * cc * kL), 0.f);
             rec[g] = r;
+            if (mrec) mrec[g] = mask_setup(r.a, r.b, r.c);
 
             Rect rc;
             rc.x0 = 0;
@@ -396,9 +398,13 @@ __global__ void k1_rank_kernel(const uint32_t* __restrict__ gid, int64_t k, cons
 // hundreds of tiles, so one thread per gaussian diverged); each lane finds the
 // owning gaussian of its slot by a shuffle binary search over the warp's prefix of
 // counts.  Slot order is the per-gaussian row-major tile order, as before.
+// mrec (packed layout): the pair's block mask goes above the scene index, and a
+// pair whose footprint reaches no block of its tile gets the key `sentinel`
+// (= ntiles), which sorts after every tile and belongs to no tile list.
 __global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __restrict__ rect,
                                const uint32_t* __restrict__ offs, int64_t k, int tiles_x,
                                uint32_t* __restrict__ tile_key, uint32_t* __restrict__ emit_g,
+                               const MaskRec* __restrict__ mrec, uint32_t sentinel,
                                int64_t k_total = INT64_MAX) {
     const int lane = threadIdx.x & 31;
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -439,18 +445,35 @@ __global__ void k2_emit_kernel(const uint32_t* __restrict__ gid, const Rect* __r
             const uint32_t q = p - exL;
             const uint32_t ty = (uint32_t)y0L + q / wL, tx = (uint32_t)x0L + q % wL;
             RCGS_DCHECK(tx < (uint32_t)tiles_x && gL < (uint32_t)k_total);
-            tile_key[base + p] = ty * (uint32_t)tiles_x + tx;
-            emit_g[base + p] = gL;
+            uint32_t key = ty * (uint32_t)tiles_x + tx, val = gL;
+            if (mrec) {
+                const uint32_t bm = tile_block_mask(mrec[gL], (float)(tx * kTile), (float)(ty * kTile));
+                val |= bm << kIdxBits;
+                if (bm == 0u) key = sentinel;
+            }
+            tile_key[base + p] = key;
+            emit_g[base + p] = val;
         }
     }
 }
 
-__global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key, int64_t pairs, uint2* __restrict__ ranges) {
+// Tile ranges of the sorted pairs (sentinel-keyed pairs: none), and, for scenes
+// too large to pack the masks into the values, each pair's block mask.
+__global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key, const uint32_t* __restrict__ pair_g,
+                                 const RasterRec* __restrict__ rec, int tiles_x, uint32_t ntiles, int64_t pairs,
+                                 uint2* __restrict__ ranges, uint32_t* __restrict__ pair_m) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= pairs) return;
     uint32_t t = tile_key[j];
+    if (t >= ntiles) return;
     if (j == 0 || tile_key[j - 1] != t) ranges[t].x = (uint32_t)j;
     if (j == pairs - 1 || tile_key[j + 1] != t) ranges[t].y = (uint32_t)(j + 1);
+    if (pair_m == nullptr) return;
+    const RasterRec* r = rec + pair_g[j];
+    const float2 m = *reinterpret_cast<const float2*>(&r->a);  // the mean's hi parts only
+    const int tx = (int)(t % (uint32_t)tiles_x), ty = (int)(t / (uint32_t)tiles_x);
+    pair_m[j] = tile_block_mask(make_float4(m.x, m.y, 0.f, 0.f), r->b, r->c, (float)(tx * kTile),
+                                (float)(ty * kTile));
 }
 
 // Raster work order: tiles by descending entry count (longest-processing-time
@@ -625,6 +648,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->color, s);
     dfree(v->rank_of, s);
     dfree(v->pair_g, s);
+    dfree(v->pair_m, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
     dfree(v->work, s);
@@ -674,12 +698,19 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&v->color, n, s));
     RCGS_TRY(dalloc(&rect, n, s));
     RCGS_TRY(dalloc(&count_g, n, s));
+    static const bool pack_ok = [] {  // RCGS_PAIR_PACK=0: the large-scene layout (tests)
+        const char* e = getenv("RCGS_PAIR_PACK");
+        return !(e && atoi(e) == 0);
+    }();
+    v->pair_packed = pack_ok && n < ((int64_t)1 << kIdxBits);
+    MaskRec* mrec = nullptr;  // packed layout: per-gaussian block-mask setup for K2 emit
+    if (v->pair_packed) RCGS_TRY(dalloc(&mrec, n, s));
     {
         unsigned long long init[2] = {~0ull, 0ull};
         RCGS_CUDA(cudaMemcpyAsync(minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
     k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, sc->opac, n, v->cam, v->cfg, flag, key,
-                                                  minmax, v->z, v->rec, v->exact, rect, count_g);
+                                                  minmax, v->z, v->rec, v->exact, rect, count_g, mrec);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
     uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));
@@ -699,6 +730,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(key, s);
         dfree(minmax, s);
         dfree(rect, s);
+        dfree(mrec, s);
         dfree(count_g, s);
         return RCGS_OK;
     }
@@ -773,11 +805,13 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     dfree(count, s);
     if (hp[1] != 0) {  // a long tie run needs the full 64-bit key sort: rebuild
         dfree(rect, s);
+        dfree(mrec, s);
         return kRetryFullSort;
     }
     v->pairs = pairs;
     if (pairs == 0) {
         dfree(rect, s);
+        dfree(mrec, s);
         return RCGS_OK;
     }
     // ---- K2 emit (depth order, values = scene index) + stable tile sort; the sort
@@ -787,14 +821,18 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&tkey_alt, pairs, s));
     RCGS_TRY(dalloc(&emit_g, pairs, s));
     RCGS_TRY(dalloc(&g_alt, pairs, s));
-    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g, v->n);
+    k2_emit_kernel<<<div_up(k, 256), 256, 0, s>>>(v->gid, rect, v->offs, k, v->tiles_x, tkey, emit_g, mrec,
+                                                  (uint32_t)ntiles, v->n);
     RCGS_LAUNCH_CHECK();
     dfree(rect, s);
+    dfree(mrec, s);
     int tile_bits = 1;
-    while ((1 << tile_bits) < ntiles) ++tile_bits;
+    while ((1 << tile_bits) <= ntiles) ++tile_bits;  // room for the sentinel key ntiles
     RCGS_TRY(radix_sort_u32(&tkey, &tkey_alt, &emit_g, &g_alt, false, pairs, tile_bits, s));
     v->pair_g = emit_g;
-    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, pairs, v->ranges);
+    if (!v->pair_packed) RCGS_TRY(dalloc(&v->pair_m, pairs, s));
+    k2_ranges_kernel<<<div_up(pairs, 256), 256, 0, s>>>(tkey, emit_g, v->rec, v->tiles_x, (uint32_t)ntiles, pairs,
+                                                        v->ranges, v->pair_m);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
     tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order);
@@ -874,9 +912,19 @@ extern "C" int rcgs_view_exact(const rcgs_view* v, double* d_out, void* stream) 
     return RCGS_OK;
 }
 
+__global__ void unpack_pairs_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) out[j] = in[j] & kIdxMask;
+}
+
 extern "C" int rcgs_view_pairs(const rcgs_view* v, uint32_t* d_pair_g, void* stream) {
     RCGS_CHECK_ARG(v != nullptr && d_pair_g != nullptr, "null argument");
     if (v->pairs == 0) return RCGS_OK;
+    if (v->pair_packed) {
+        unpack_pairs_kernel<<<div_up(v->pairs, 256), 256, 0, as_stream(stream)>>>(v->pair_g, v->pairs, d_pair_g);
+        RCGS_LAUNCH_CHECK();
+        return RCGS_OK;
+    }
     RCGS_CUDA(cudaMemcpyAsync(d_pair_g, v->pair_g, sizeof(uint32_t) * (size_t)v->pairs, cudaMemcpyDeviceToDevice,
                               as_stream(stream)));
     return RCGS_OK;

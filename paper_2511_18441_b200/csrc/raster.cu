@@ -116,6 +116,9 @@ struct RasterArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // work order (nullptr: row-major)
     const uint32_t* pair_g;  // tile lists: scene indices in depth order
+    const uint32_t* pair_m;  // per list entry: 8x4 blocks of its tile the footprint reaches
+                             // (null: packed above the scene index in pair_g)
+    uint32_t idx_mask;       // scene-index bits of a pair_g value
     const int32_t* rank_of;  // scene index -> depth rank (capture output)
     const RasterRec* rec;
     const ExactRec* exact;
@@ -233,7 +236,8 @@ __device__ __forceinline__ float cull_power(const float4 ra, const float4 rb, co
 __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair_g,
                                             const RasterRec* __restrict__ rec,
                                             const ExactRec* __restrict__ exact, double clamp, double skip,
-                                            uint32_t j0, uint32_t j1, float uf, float vf, int lane) {
+                                            uint32_t j0, uint32_t j1, float uf, float vf, int lane,
+                                            uint32_t idx_mask) {
     constexpr int kU = 2;
     const double u = (double)uf, v = (double)vf;
     double T = 1.0;
@@ -242,7 +246,7 @@ __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair
 #pragma unroll
         for (int q = 0; q < kU; ++q) {
             const uint32_t j = c + q * 32 + lane;
-            sv[q] = j <= j1 ? pair_g[j] : 0xffffffffu;
+            sv[q] = j <= j1 ? pair_g[j] & idx_mask : 0xffffffffu;
         }
         bool live[kU];
 #pragma unroll
@@ -322,6 +326,7 @@ struct WarpStage {
     uint32_t g[32], j[32];  // entry: scene index, tile-list position
     float4 ra[32], rb[32], rc[32], rcol[32];  // raw records of the next chunk (lane = entry)
     uint32_t pg[2][32];                       // pair ids (scene indices), double-buffered
+    uint32_t pm[2][32];                       // their block masks
 };
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
@@ -393,7 +398,8 @@ __device__ __noinline__ SlowOut slow_entry(const uint32_t* __restrict__ pair_g, 
                                            const ExactRec* __restrict__ exact, double clamp, double skip,
                                            double t_floor, double tau, float f_floor, float f_tau, uint32_t g,
                                            uint32_t j, uint32_t j0, float uf, float vf, int lane, float T, float A,
-                                           bool live, bool pass, bool gamb, float al, float dl, StepOut cur) {
+                                           bool live, bool pass, bool gamb, float al, float dl, StepOut cur,
+                                           uint32_t idx_mask) {
     uint32_t resync = 0;
     if (gamb) {
         const double a64 = exact_alpha_at(exact, g, (double)uf, (double)vf, clamp, skip);
@@ -405,7 +411,7 @@ __device__ __noinline__ SlowOut slow_entry(const uint32_t* __restrict__ pair_g, 
     for (unsigned m = __ballot_sync(0xffffffffu, cur.amb); m; m &= m - 1) {
         const int L = __ffs(m) - 1;
         const float lu = __shfl_sync(0xffffffffu, uf, L), lv = __shfl_sync(0xffffffffu, vf, L);
-        const double T64 = warp_exact_T(pair_g, rec, exact, clamp, skip, j0, j, lu, lv, lane);
+        const double T64 = warp_exact_T(pair_g, rec, exact, clamp, skip, j0, j, lu, lv, lane, idx_mask);
         if (lane == L) {  // the exact decision (render.py:278-291, 389-397)
             const float w = al * T;
             cur.amb = false;
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             const bool top = ((blk >> 1) & 1) == 0;
             unsigned cb = 0, cu = 0;
             for (uint32_t j = range.x + lane; j < range.y; j += 32) {
-                const uint32_t sj = a.pair_g[j];
+                const uint32_t sj = a.pair_g[j] & a.idx_mask;
                 const float4 qa = a.rec[sj].a, qb = a.rec[sj].b, qc = a.rec[sj].c;
                 cb += touches_block(qa, fbx0, fby0) &&
                       ellipse_touches_rect(qa, qb, qc, fbx0, fby0, fbx0 + 7.f, fby0 + 3.f);
@@ -542,13 +548,20 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         float* wp = M == FWDREC ? a.wrec_w + (size_t)rbase * 32 + lane : nullptr;
         // chunk pipeline: pair ids two chunks ahead, raw records one chunk ahead (each
         // lane copies and later reads only its own slots)
+        const bool packed = a.pair_m == nullptr;
+        const int mshift = packed ? kIdxBits + blk : blk;
         auto issue_pg = [&](uint32_t cn, int buf) {
-            if (cn + lane < range.y) cp_async4(&st.pg[buf][lane], a.pair_g + cn + lane);
+            if (cn + lane < range.y) {
+                cp_async4(&st.pg[buf][lane], a.pair_g + cn + lane);
+                if (!packed) cp_async4(&st.pm[buf][lane], a.pair_m + cn + lane);
+            }
             cp_async_commit();
         };
+        auto mask_word = [&](int buf) { return packed ? st.pg[buf][lane] : st.pm[buf][lane]; };
+        // raw records only for the entries whose footprint reaches this block
         auto issue_raw = [&](uint32_t cn, int buf) {
-            if (cn + lane < range.y) {
-                const uint32_t sn = st.pg[buf][lane];
+            if (cn + lane < range.y && ((mask_word(buf) >> mshift) & 1u)) {
+                const uint32_t sn = st.pg[buf][lane] & a.idx_mask;
                 cp_async16(&st.ra[lane], &a.rec[sn].a);
                 cp_async16(&st.rb[lane], &a.rec[sn].b);
                 cp_async16(&st.rc[lane], &a.rec[sn].c);
@@ -571,16 +584,24 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             uint32_t s = 0;
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra, rcol = ra;
             if (j < range.y) {
-                s = st.pg[buf][lane];
+                s = st.pg[buf][lane] & a.idx_mask;
                 RCGS_DCHECK(j < (uint64_t)a.pairs && s < (uint64_t)a.n);
-                ra = st.ra[lane];
-                keep = touches_block(ra, fbx0, fby0);
+                // the pair's block mask (view build) is the per-block cull
+                keep = (mask_word(buf) >> mshift) & 1u;
+#ifdef RCGS_CHECKED
+                {  // a dropped (entry, block) must fail the exact per-block test too
+                    const RasterRec cr = a.rec[s];
+                    RCGS_DCHECK(keep || !(touches_block(cr.a, fbx0, fby0) &&
+                                          ellipse_touches_rect(cr.a, cr.b, cr.c, fbx0, fby0, fbx0 + 7.f,
+                                                               fby0 + 3.f)));
+                }
+#endif
                 if (keep) {
+                    ra = st.ra[lane];
                     rb = st.rb[lane];
                     rc = st.rc[lane];
-                    keep = ellipse_touches_rect(ra, rb, rc, fbx0, fby0, fbx0 + 7.f, fby0 + 3.f);
+                    if (kFwd) rcol = st.rcol[lane];
                 }
-                if (kFwd && keep) rcol = st.rcol[lane];
             }
             // the slots are consumed: start the next chunk's records and the ids after
             if (c0 + 32 < range.y) {
@@ -643,7 +664,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                     const SlowOut so =
                         slow_entry<M>(a.pair_g, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, a.t_floor, a.tau, a.f_floor,
                                       a.f_tau, st.g[k], st.j[k], range.x, cxf + lxf, cyf + lyf, lane, T, A, live, pass,
-                                      gamb, al, q2.w, o);
+                                      gamb, al, q2.w, o, a.idx_mask);
                     o = so.o;
                     n_resync += so.resync;
                 }
@@ -1108,6 +1129,8 @@ static RasterArgs base_args(const rcgs_view* v) {
     a.ranges = v->ranges;
     a.tile_order = v->tile_order;
     a.pair_g = v->pair_g;
+    a.pair_m = v->pair_packed ? nullptr : v->pair_m;
+    a.idx_mask = v->pair_packed ? kIdxMask : 0xffffffffu;
     a.rank_of = v->rank_of;
     a.counter = v->work;
     a.rec = v->rec;

@@ -788,3 +788,38 @@ def test_render_rgba_bit_identical_to_host_frame():
         np.testing.assert_array_equal(v.render_rgba(bits_dev).cpu().numpy(),
                                       P.image_to_rgba(P.overlay(img, bits)))
     v.close()
+
+
+_LAYOUT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2511_18441_b200 as P
+from paper_2511_18441_b200.synthetic import ring_cameras, scaled_scene
+scene, _ = scaled_scene(60_000, 3, seed=4)
+out = []
+for intr, pose in ring_cameras(640, 360, 3):
+    out.append(P.render(scene, intr, pose))
+    out.append(P.depth_from_gaussians(scene, intr, pose))
+    cap = P.render_forward(scene, intr, pose)
+    out.append(P.backward_sh(cap, np.full((360, 640, 3), 1e-3) * (np.arange(640) % 7 - 3)[None, :, None]))
+np.savez(sys.argv[2], *out)
+"""
+
+
+def test_tile_list_layouts_agree(tmp_path):
+    """The pair-mask layouts: masks packed above the scene index (scenes below 2^24
+    gaussians) and the large-scene layout (plain indices + a mask array, forced
+    with RCGS_PAIR_PACK=0) give bit-identical render, depth and backward."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "layout.py"
+    script.write_text(_LAYOUT_SCRIPT)
+    res = {}
+    for pack in ("1", "0"):
+        out = tmp_path / f"o{pack}.npz"
+        env = dict(os.environ, RCGS_PAIR_PACK=pack)
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env, timeout=600)
+        res[pack] = np.load(out)
+    for key in res["1"].files:
+        np.testing.assert_array_equal(res["1"][key], res["0"][key])
