@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         // result, so ptxas keeps it in a register.
         const uint32_t rbase =
             __shfl_sync(0xffffffffu, kBlocksPerTile * range.x + (uint32_t)blk * (range.y - range.x), 0);
-        // FWDREC: nrec records so far; wp = this lane's weight slot of the next one
+        // FWDREC: nrec records so far; wp = this lane's weight slot of record nrec
         uint32_t nrec = 0;
         float* wp = M == FWDREC ? a.wrec_w + (size_t)rbase * 32 + lane : nullptr;
         // chunk pipeline: pair ids two chunks ahead, raw records one chunk ahead (each
@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             }
             __syncwarp();
             const int n = __popc(bal);
+            float* const wk = wp;  // record k of this chunk: wk[32 k] (one IMAD.WIDE per store)
             // one (pixel, entry) step of staged entry k for this lane
             auto entry = [&](int k) {
                 const float4 q0 = st.q0[k], q1 = st.q1[k], q2 = st.q2[k];
@@ -681,8 +682,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                     acc1 = fmaf(q2.y, wc, acc1);
                     acc2 = fmaf(q2.z, wc, acc2);
                     if (M == FWDREC) {
-                        *wp = wc;
-                        wp += 32;
+                        *reinterpret_cast<float*>(reinterpret_cast<char*>(wk) + (size_t)(uint32_t)k * 128u) = wc;
                     }
                 } else if (M == CAP_COUNT) {
                     ncap += comp;
@@ -695,7 +695,9 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                         a.cap_weight[o] = (double)wc;
                     }
                 } else if (M == BWD) {
-                    float v0 = wc * g0, v1 = wc * g1, v2 = wc * g2;
+                    // products rounded on their own (no FMA contraction into the tree below), as
+                    // in the record-streaming backward
+                    float v0 = __fmul_rn(wc, g0), v1 = __fmul_rn(wc, g1), v2 = __fmul_rn(wc, g2);
                     if (__any_sync(0xffffffffu, v0 != 0.f || v1 != 0.f || v2 != 0.f)) {
                         // transposed reduce-scatter of (v0, v1, v2, 0) over the warp: 6
                         // shuffles instead of 15; channel c ends summed in lanes 8c..8c+7
@@ -737,6 +739,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 all_done = __all_sync(0xffffffffu, !(T > 0.f));  // one vote: cheaper than a cadence test
             }
             nrec += (uint32_t)k;  // entries processed (one record each in FWDREC)
+            if (M == FWDREC) wp += (size_t)k * 32;
             __syncwarp();
         }
         cp_async_wait<0>();  // no copy may land in the slots once the next item uses them
@@ -845,8 +848,94 @@ __device__ __forceinline__ RecMeta rec_meta(const RecArgs& a, unsigned item, int
 #ifndef RCGS_REC_BWD_CTAS
 #define RCGS_REC_BWD_CTAS 4
 #endif
+// One block's records, all pixel gradients finite: batches of 8 records staged in
+// the warp's shared rows (cp.async, double-buffered; rows padded to 36 floats so
+// the 4 lanes of each record read conflict-free).  Lane (q, h) = (lane / 4, lane
+// % 4) owns record q's pixels h, h + 4, ..., h + 28 and sums w g over them in the
+// pairing of the xor-16, 8, 4 stages of the warp butterfly, then the xor-2 / xor-1
+// shuffles finish it: the same tree as a plain warp sum of the 32 products, so the
+// totals equal the traversal backward's bit for bit (and, with finite g, w = 0
+// gives an exact 0 product, as skipping the pixel does).  The sums of channels
+// 0 / 1 go through packed FADD2.
+__device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m, float (*sw)[8][36],
+                                              uint32_t (*ss)[8], int lane) {
+    const int q = lane >> 2, h = lane & 3;
+    float2 g01[8];
+    float g2[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int src = h + 4 * j;
+        g01[j] = make_float2(__shfl_sync(0xffffffffu, m.g0, src), __shfl_sync(0xffffffffu, m.g1, src));
+        g2[j] = __shfl_sync(0xffffffffu, m.g2, src);
+    }
+    // lane copies 32 bytes of one record of the batch: record lane / 4, quarter lane % 4
+    auto issue = [&](uint32_t r0, int buf) {
+        const uint32_t r = r0 + (uint32_t)q;
+        if (r < m.n) {
+            const float* src = a.wrec_w + (size_t)(m.base + r) * 32 + 8 * h;
+            cp_async16(&sw[buf][q][8 * h], src);
+            cp_async16(&sw[buf][q][8 * h + 4], src + 4);
+        }
+        if (lane < 8 && r0 + lane < m.n) cp_async4(&ss[buf][lane], a.wrec_s + m.base + r0 + lane);
+        cp_async_commit();
+    };
+    issue(0, 0);
+    int buf = 0;
+    for (uint32_t r0 = 0; r0 < m.n; r0 += 8, buf ^= 1) {
+        if (r0 + 8 < m.n) {
+            issue(r0 + 8, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const bool live = r0 + q < m.n;
+        float2 p01[8];
+        float p2[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float w = live ? sw[buf][q][h + 4 * j] : 0.f;
+            // scalar products: a packed FMUL2 here is contracted with the FADD2 below
+            p01[j] = make_float2(__fmul_rn(w, g01[j].x), __fmul_rn(w, g01[j].y));
+            p2[j] = __fmul_rn(w, g2[j]);  // no FMA contraction into the sums below
+        }
+        // pixel i = h + 4 j: xor-16 pairs j, j + 4; xor-8 pairs j, j + 2; xor-4 pairs j, j + 1
+        float2 a01[4];
+        float a2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a01[j] = __fadd2_rn(p01[j], p01[j + 4]);
+            a2[j] = p2[j] + p2[j + 4];
+        }
+        const float2 b0 = __fadd2_rn(a01[0], a01[2]), b1 = __fadd2_rn(a01[1], a01[3]);
+        float2 c01 = __fadd2_rn(b0, b1);
+        float c2 = (a2[0] + a2[2]) + (a2[1] + a2[3]);
+        c01.x += __shfl_xor_sync(0xffffffffu, c01.x, 2);
+        c01.y += __shfl_xor_sync(0xffffffffu, c01.y, 2);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, 2);
+        c01.x += __shfl_xor_sync(0xffffffffu, c01.x, 1);
+        c01.y += __shfl_xor_sync(0xffffffffu, c01.y, 1);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, 1);
+        const float val = h == 0 ? c01.x : (h == 1 ? c01.y : c2);
+        if (h < 3 && live && val != 0.f) {
+            const uint32_t sq = ss[buf][q];
+            RCGS_DCHECK(sq < (uint32_t)a.n);
+            if (isfinite(val)) {
+                atomicAdd(&a.acc_fx[3 * (int64_t)sq + h], (unsigned long long)to_fixed(val));
+            } else if (a.nonfinite) {
+                atomicOr(a.nonfinite, 1);
+            }
+        }
+        __syncwarp();  // the rows of `buf` are refilled by the issue two batches on
+    }
+}
+
 __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArgs a) {
     const int lane = threadIdx.x & 31;
+    __shared__ __align__(16) float s_w[kCTA / 32][2][8][36];
+    __shared__ uint32_t s_s[kCTA / 32][2][8];
+    float(*sw)[8][36] = s_w[threadIdx.x >> 5];
+    uint32_t(*ss)[8] = s_s[threadIdx.x >> 5];
     constexpr int kU = 8;  // records per batch (the 32-value reduce-scatter width)
     const unsigned nw = gridDim.x * (blockDim.x >> 5);
     const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -867,6 +956,11 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
         // the gradient is local to the edited region: blocks whose gradients are all
         // 0 have no term
         if (m.n > 0 && !__all_sync(0xffffffffu, m.g0 == 0.f && m.g1 == 0.f && m.g2 == 0.f)) {
+            if (__all_sync(0xffffffffu, isfinite(m.g0) && isfinite(m.g1) && isfinite(m.g2))) {
+                rec_bwd_block(a, m, sw, ss, lane);
+            } else {
+            // non-finite pixel gradients: a pixel that no record composites (w = 0)
+            // must contribute nothing, not 0 * inf
             float w[kU], wn[kU];
             uint32_t sl = 0u, sln = 0u;  // lane q < kU holds record q's scene index
             auto load = [&](uint32_t r0, float* wd, uint32_t& sd) {
@@ -889,9 +983,9 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
 #pragma unroll
                 for (int q = 0; q < kU; ++q) {
                     const bool comp = w[q] != 0.f;
-                    x[4 * q] = comp ? w[q] * m.g0 : 0.f;
-                    x[4 * q + 1] = comp ? w[q] * m.g1 : 0.f;
-                    x[4 * q + 2] = comp ? w[q] * m.g2 : 0.f;
+                    x[4 * q] = comp ? __fmul_rn(w[q], m.g0) : 0.f;
+                    x[4 * q + 1] = comp ? __fmul_rn(w[q], m.g1) : 0.f;
+                    x[4 * q + 2] = comp ? __fmul_rn(w[q], m.g2) : 0.f;
                     x[4 * q + 3] = 0.f;
                 }
 #pragma unroll
@@ -917,6 +1011,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
 #pragma unroll
                 for (int u = 0; u < kU; ++u) w[u] = wn[u];
                 sl = sln;
+            }
             }
         }
         if (!has_next) break;
@@ -988,9 +1083,9 @@ __global__ void __launch_bounds__(kCTA) rec_kernel(RecArgs a) {
 #pragma unroll
                 for (int q = 0; q < kU; ++q) {
                     const bool comp = w[q] != 0.f;
-                    x[4 * q] = comp ? w[q] * g0 : 0.f;
-                    x[4 * q + 1] = comp ? w[q] * g1 : 0.f;
-                    x[4 * q + 2] = comp ? w[q] * g2 : 0.f;
+                    x[4 * q] = comp ? __fmul_rn(w[q], g0) : 0.f;
+                    x[4 * q + 1] = comp ? __fmul_rn(w[q], g1) : 0.f;
+                    x[4 * q + 2] = comp ? __fmul_rn(w[q], g2) : 0.f;
                     x[4 * q + 3] = 0.f;
                 }
 #pragma unroll
