@@ -123,12 +123,30 @@ __device__ __forceinline__ void commit_step(unsigned* ticket, bool upd, int64_t*
     }
 }
 
-constexpr int kAG = 64;                     // gaussians per tile
+#ifndef RCGS_ADAM_TILE
+#define RCGS_ADAM_TILE 56
+#endif
+// gaussians per tile: 56 keeps a 2-stage ring (with the side arrays) under a third
+// of the SM's shared memory, i.e. 3 CTAs per SM at one view per step
+constexpr int kAG = RCGS_ADAM_TILE;
+static_assert(kAG % 8 == 0 && kAG <= 64, "whole warps of 8 gaussians; 16-byte side-array tiles");
 constexpr int kAThreads = 4 * kAG;          // 4 threads per gaussian, 12 coefficients each
+constexpr int kStateG = 64;                 // gaussians per tile_state entry (ABI: 64-gaussian blocks)
 constexpr int kAStages = 2;                 // tiles in flight per CTA
 constexpr uint32_t kARow = 48 * 4;          // bytes of one gaussian's SH (or m, or v)
 constexpr uint32_t kATileBytes = kAG * kARow;
-constexpr size_t kASmem = (size_t)kAStages * 3 * kATileBytes + kAStages * sizeof(uint64_t);
+// A stage holds, besides the SH / m / v tiles, the tile's positions (fp64 x 3),
+// next-view depth ranks and each view's acc (fp32 x 3), so the update and the
+// colour epilogue read no global memory on the critical path.
+constexpr uint32_t kAPosBytes = kAG * 24;   // 1536
+constexpr uint32_t kARankBytes = kAG * 4;   // 256
+constexpr uint32_t kAAccBytes = kAG * 12;   // 768 per view
+__host__ __device__ constexpr uint32_t adam_stage_bytes(int n_views) {
+    return 3 * kATileBytes + kAPosBytes + kARankBytes + (uint32_t)n_views * kAAccBytes;
+}
+__host__ __device__ constexpr size_t adam_smem_bytes(int n_views) {
+    return (size_t)kAStages * adam_stage_bytes(n_views) + kAStages * sizeof(uint64_t);
+}
 
 // Fused SH-gradient expansion + Adam over all N x 48 coefficients (optimize.py
 // Adam; recolor.py SH-only refit).  The step streams SH, m and v once each way
@@ -161,12 +179,22 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     // also writes the updated tiles to the snapshot (optimize.py:221-222)
     const bool snap = upd && snapshot != nullptr && snapshot_every > 0 && (*step + 1) % snapshot_every == 0;
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kAStages * 3 * kATileBytes);
+    const uint32_t stage_bytes = adam_stage_bytes(views.n);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kAStages * stage_bytes);
     const int t = threadIdx.x;
     const int64_t ntiles = (n + kAG - 1) / kAG;
     float* const arrays[3] = {sh, m, v};
+    auto stage_base = [&](int s) -> unsigned char* { return smem + (size_t)s * stage_bytes; };
     auto stage_buf = [&](int s, int arr) -> float4* {
-        return reinterpret_cast<float4*>(smem + ((size_t)s * 3 + arr) * kATileBytes);
+        return reinterpret_cast<float4*>(stage_base(s) + (size_t)arr * kATileBytes);
+    };
+    auto stage_pos = [&](int s) -> double* { return reinterpret_cast<double*>(stage_base(s) + 3 * kATileBytes); };
+    auto stage_rank = [&](int s) -> int32_t* {
+        return reinterpret_cast<int32_t*>(stage_base(s) + 3 * kATileBytes + kAPosBytes);
+    };
+    auto stage_acc = [&](int s, int vi) -> float* {
+        return reinterpret_cast<float*>(stage_base(s) + 3 * kATileBytes + kAPosBytes + kARankBytes +
+                                        (size_t)vi * kAAccBytes);
     };
     // per tile: 2 = full update (SH, m, v in and out), 1 = SH in only (an inactive
     // tile whose SH the fused colour epilogue needs), 0 = nothing.  A tile is
@@ -174,18 +202,34 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     // (tile_state, adam_active_kernel): Adam then leaves all of it bit-identical
     // (m' = v' = 0, theta' = theta - lr * 0 / (0 + eps)), so the skip is exact.
     auto mode_of = [&](int64_t tile) -> int {
-        const bool active = tile_state == nullptr || tile_state[tile] != 0u;
+        // the 64-gaussian state blocks overlapping this tile
+        const int64_t last = tile * kAG + kAG - 1 < n ? tile * kAG + kAG - 1 : n - 1;
+        const int64_t a0 = tile * kAG / kStateG, a1 = last / kStateG;
+        const bool active = tile_state == nullptr || tile_state[a0] != 0u || tile_state[a1] != 0u;
         return (upd && active) ? 2 : (next_color != nullptr ? 1 : 0);
     };
+    // Side arrays (positions, ranks, acc) ride the same barrier for full tiles; the
+    // last, partial tile (byte counts not multiples of 16) reads them from global.
     auto issue = [&](int64_t tile, int s) {  // one thread
         const int64_t g0 = tile * kAG;
-        const uint32_t bytes = (uint32_t)(n - g0 < kAG ? n - g0 : kAG) * kARow;
+        const bool full = n - g0 >= kAG;
+        const uint32_t bytes = (uint32_t)(full ? kAG : n - g0) * kARow;
         const uint32_t bar = smem_addr(&bars[s]);
         const int md = mode_of(tile);
         const int na = md == 2 ? 3 : md;
-        mbar_expect_tx(bar, (uint32_t)na * bytes);  // 0 bytes: the phase completes at once
+        const bool need_pos = full && md != 0;
+        const bool need_rank = full && md != 0 && next_color != nullptr;
+        const bool need_acc = full && md == 2;
+        const uint32_t tx = (uint32_t)na * bytes + (need_pos ? kAPosBytes : 0u) + (need_rank ? kARankBytes : 0u) +
+                            (need_acc ? (uint32_t)views.n * kAAccBytes : 0u);
+        mbar_expect_tx(bar, tx);  // 0 bytes: the phase completes at once
         for (int arr = 0; arr < na; ++arr)
             bulk_load(smem_addr(stage_buf(s, arr)), arrays[arr] + g0 * 48, bytes, bar);
+        if (need_pos) bulk_load(smem_addr(stage_pos(s)), pos + 3 * g0, kAPosBytes, bar);
+        if (need_rank) bulk_load(smem_addr(stage_rank(s)), next_rank_of + g0, kARankBytes, bar);
+        if (need_acc)
+            for (int vi = 0; vi < views.n; ++vi)
+                bulk_load(smem_addr(stage_acc(s, vi)), views.acc[vi] + 3 * g0, kAAccBytes, bar);
     };
     __shared__ float2 s_bc;
     if (t == 0) {
@@ -202,18 +246,21 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     }
     const float2 ibc = s_bc;
     const int gi = t >> 2, part = t & 3;  // gaussian in the tile, 12-coefficient quarter
+    const int lane = t & 31;
     const float invn = 1.0f / (float)views.n;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int s = it % kAStages;
         const int64_t g0 = tile * kAG;
         const int ng = (int)(n - g0 < kAG ? n - g0 : kAG);
+        const bool full = ng == kAG;
         mbar_wait(smem_addr(&bars[s]), (uint32_t)((it / kAStages) & 1));
         const int md = mode_of(tile);
+        // this tile's positions: staged (full tiles) or global (the partial one)
+        const double* tpos = full ? stage_pos(s) : pos + 3 * g0;
         float c12[12];  // this thread's 12 coefficients after the update (colour epilogue)
         if (md == 2 && gi < ng) {
-            const int64_t g = g0 + gi;
-            const double px = pos[3 * g], py = pos[3 * g + 1], pz = pos[3 * g + 2];
+            const double px = tpos[3 * gi], py = tpos[3 * gi + 1], pz = tpos[3 * gi + 2];
             float gr[12];
 #pragma unroll
             for (int e = 0; e < 12; ++e) gr[e] = 0.f;
@@ -231,7 +278,7 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     b[q] = part == 0 ? r[q] : (part == 1 ? r[4 + q] : (part == 2 ? r[8 + q] : r[12 + q]));
-                const float* acc = views.acc[vi] + 3 * (size_t)g;
+                const float* acc = (full ? stage_acc(s, vi) : views.acc[vi] + 3 * g0) + 3 * gi;
                 const float a3[3] = {acc[0], acc[1], acc[2]};
 #pragma unroll
                 for (int e = 0; e < 12; ++e) gr[e] += b[e / 3] * a3[e % 3];
@@ -260,17 +307,49 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
 #pragma unroll
             for (int e = 0; e < 12; ++e) c12[e] = P[e];
         }
+        // the colour epilogue's inputs leave the stage before it is refilled
+        const int64_t g = g0 + gi;
+        const bool ok = next_color != nullptr && gi < ng;
+        const int32_t rs = ok ? (full ? stage_rank(s)[gi] : next_rank_of[g]) : -1;
+        double dx = 1.0, dy = 0.0, dz = 0.0;
+        if (ok) {
+            dx = tpos[3 * gi] - next_cen.c[0];
+            dy = tpos[3 * gi + 1] - next_cen.c[1];
+            dz = tpos[3 * gi + 2] - next_cen.c[2];
+        }
+        // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0 && md == 2) {
+            const uint32_t bytes = (uint32_t)ng * kARow;
+#pragma unroll
+            for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
+            if (snap) bulk_store(snapshot + g0 * 48, smem_addr(stage_buf(s, 0)), bytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (t == 0) {
+            const int64_t next = tile + (int64_t)kAStages * gridDim.x;
+            if (next < ntiles) {
+                // the stage is refilled only after the store has read it
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                issue(next, s);
+            }
+        }
         if (next_color != nullptr) {
             // fused colour pass of the next step's view (render.py:209-214) from the
-            // updated coefficients in registers: each of a gaussian's 4 threads
-            // evaluates its basis-row quarter (fp64, the order color_kernel uses,
-            // bit-identical) and lane part 0 combines and writes the colour
-            const int64_t g = g0 + gi;
-            const int32_t rs = gi < ng ? next_rank_of[g] : -1;
+            // updated coefficients in registers, overlapping the stage's refill: each
+            // of a gaussian's 4 threads evaluates its basis-row quarter (fp64, the
+            // order color_kernel uses, bit-identical) and lane part 0 combines and
+            // writes the colour.  The normalised direction (view_dir's operations)
+            // costs one fp64 division per lane: lane part p divides component p, then
+            // the 4 lanes exchange.
+            const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+            const double q = (part == 0 ? dx : (part == 1 ? dy : dz)) / nrm;
+            const int lb = lane & ~3;
+            const double x = __shfl_sync(0xffffffffu, q, lb), y = __shfl_sync(0xffffffffu, q, lb + 1),
+                         z = __shfl_sync(0xffffffffu, q, lb + 2);
             double qv[3] = {0.0, 0.0, 0.0};
             if (rs >= 0) {
-                double x, y, z;
-                view_dir(pos, g, next_cen.c, x, y, z);
                 double b[16];
                 sh_basis16<double>(x, y, z, deg, b);
                 color_quarter(b, c12, part, qv);
@@ -294,24 +373,6 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
                 next_color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
             }
         }
-        // shared-memory writes -> visible to the bulk-copy (async) proxy, then store
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (t == 0 && md == 2) {
-            const uint32_t bytes = (uint32_t)ng * kARow;
-#pragma unroll
-            for (int arr = 0; arr < 3; ++arr) bulk_store(arrays[arr] + g0 * 48, smem_addr(stage_buf(s, arr)), bytes);
-            if (snap) bulk_store(snapshot + g0 * 48, smem_addr(stage_buf(s, 0)), bytes);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (t == 0) {
-            const int64_t next = tile + (int64_t)kAStages * gridDim.x;
-            if (next < ntiles) {
-                // the stage is refilled only after the store has read it
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                issue(next, s);
-            }
-        }
     }
     if (t == 0) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -331,8 +392,8 @@ __global__ void adam_active_kernel(AccViews views, int64_t n, uint32_t* __restri
             nz = nz || !(acc[0] == 0.f && acc[1] == 0.f && acc[2] == 0.f);
         }
     }
-    // a warp covers 32 gaussians of one 64-gaussian tile
-    if (__ballot_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) state[g / kAG] = 1u;
+    // a warp covers 32 gaussians of one 64-gaussian state block
+    if (__ballot_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) state[g / kStateG] = 1u;
 }
 
 __global__ void adam_dense_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
@@ -424,23 +485,25 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             av.acc[i] = h_d_accs[i];
             for (int j = 0; j < 3; ++j) av.cen[i][j] = h_centers[3 * i + j];
         }
-        static int grid = 0;
-        static std::once_flag once;
-        static int once_err = RCGS_OK;
-        std::call_once(once, [] {
-            int dev = 0, sms = 0, per_sm = 0;
-            if (cudaGetDevice(&dev) != cudaSuccess ||
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-                cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kASmem) !=
-                    cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, kASmem) !=
-                    cudaSuccess) {
-                once_err = RCGS_ECUDA;
-                return;
+        // persistent grid per staged-view count (the stage size depends on it)
+        static std::mutex grid_mu;
+        static int grids[kMaxViews + 1] = {0};
+        const size_t smem = adam_smem_bytes(n_views);
+        int grid = 0;
+        {
+            std::lock_guard<std::mutex> lock(grid_mu);
+            if (grids[n_views] == 0) {
+                int dev = 0, sms = 0, per_sm = 0;
+                RCGS_CUDA(cudaGetDevice(&dev));
+                RCGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                RCGS_CUDA(cudaFuncSetAttribute(adam_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)adam_smem_bytes(kMaxViews)));
+                RCGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_fused_kernel, kAThreads, smem));
+                grids[n_views] = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
             }
-            grid = sms * persistent_ctas(per_sm > 0 ? per_sm : 1);
-        });
-        RCGS_CHECK_ARG(once_err == RCGS_OK && grid > 0, "adam launch setup failed");
+            grid = grids[n_views];
+        }
+        RCGS_CHECK_ARG(grid > 0, "adam launch setup failed");
         // last-block ticket, one per stream: concurrent launches on different streams
         // must not mix their counts (reset by the last block of each launch)
         unsigned* ticket = stream_ticket(s);
@@ -459,7 +522,7 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             RCGS_LAUNCH_CHECK();
         }
         // bias corrections from and commit of the device step counter happen inside
-        adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, kASmem, s>>>(
+        adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, smem, s>>>(
             sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
             d_reject, nrank, nc, ncolor, d_reject_record, pub ? pub->d_snapshot : nullptr,
             pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0, d_tile_state);

@@ -149,10 +149,15 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
                                unsigned long long* __restrict__ minmax, double* __restrict__ z_out,
                                RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
                                Rect* __restrict__ rect, uint32_t* __restrict__ count,
-                               MaskRec* __restrict__ mrec) {
+                               MaskRec* __restrict__ mrec, int32_t* __restrict__ rank_of,
+                               uint2* __restrict__ ranges, int ntiles) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the view's empty tile ranges (k2_ranges fills the non-empty ones) and the
+    // culled default of rank_of (k1_rank writes the kept ranks), instead of memsets
+    if (g < ntiles) ranges[g] = make_uint2(0u, 0u);
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (g < n) {
+        rank_of[g] = -1;
         const ProjF64 p = project_one(pos, cov3d, g, cam, cfg);
         flag[g] = p.kept ? 1u : 0u;
         uint64_t k = (uint64_t)__double_as_longlong(p.z);  // z > near_clip > 0: bits order like values
@@ -226,8 +231,9 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     }
+    // zero-initialised control words: the minimum is kept complemented (max of ~key)
     if ((threadIdx.x & 31) == 0 && kmax != 0ull) {
-        atomicMin(&minmax[0], kmin);
+        atomicMax(&minmax[0], ~kmin);
         atomicMax(&minmax[1], kmax);
     }
 }
@@ -265,13 +271,15 @@ __global__ void key_rebase_kernel(uint64_t* __restrict__ key, int64_t k, uint64_
 
 // Runs of equal truncated keys are re-sorted by the full fp64 key, ties by scene
 // index (the stable input order of np.argsort, render.py:216): runs of at most 32
-// by one thread (insertion sort); longer ones, up to kLongRun, are queued for
-// long_run_sort_kernel (one CTA per run); longer still is left to the order check
-// (which then triggers the full 64-bit sort).
+// by one thread (insertion sort); the start of every longer run is queued for
+// long_run_sort_kernel, which measures, checks and (only if needed) sorts the run
+// with a whole CTA.  Long runs are mostly exact fp64 ties (gaussians of a plane on
+// a line of equal depth), already in index order from the stable LSD passes; a
+// serial per-run scan with dependent gathers had been the launch's tail.
 constexpr int kLongRun = 2048;
 
 __global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ gid,
-                                   const uint64_t* __restrict__ key_of, int64_t k, uint2* __restrict__ long_runs,
+                                   const uint64_t* __restrict__ key_of, int64_t k, uint32_t* __restrict__ long_runs,
                                    uint32_t* __restrict__ n_long, uint32_t max_long) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
@@ -279,21 +287,9 @@ __global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* _
     if ((i > 0 && k32[i - 1] == h) || i + 1 >= k || k32[i + 1] != h) return;  // run starts only
     int64_t e = i + 1;
     while (e < k && k32[e] == h && e - i <= 32) ++e;
-    if (e - i > 32) {  // a long run (rare): queue it unless already in (key, index) order
-        uint32_t gp = gid[i];
-        uint64_t kp = key_of[gp];
-        bool sorted = true;
-        for (e = i + 1; e < k && k32[e] == h && e - i <= kLongRun; ++e) {
-            const uint32_t gc = gid[e];
-            const uint64_t kc = key_of[gc];
-            sorted = sorted && (kp < kc || (kp == kc && gp < gc));
-            gp = gc;
-            kp = kc;
-        }
-        if (!sorted && e - i <= kLongRun) {
-            const uint32_t slot = atomicAdd(n_long, 1u);
-            if (slot < max_long) long_runs[slot] = make_uint2((uint32_t)i, (uint32_t)(e - i));
-        }
+    if (e - i > 32) {  // a long run: measured, checked and sorted by a CTA
+        const uint32_t slot = atomicAdd(n_long, 1u);
+        if (slot < max_long) long_runs[slot] = (uint32_t)i;
         return;
     }
     const int len = (int)(e - i);
@@ -318,30 +314,53 @@ __global__ void depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* _
     for (int a = 0; a < len; ++a) gid[i + a] = gg[a];
 }
 
-// One CTA per queued long run: bitonic sort of its (fp64 key, scene index) pairs
-// in shared memory (padded to kLongRun with +inf keys); keys are unique per index,
-// so the result is the stable order.  Runs beyond the queue capacity are left to
-// the order check.
-__global__ void __launch_bounds__(1024) long_run_sort_kernel(uint32_t* __restrict__ gid,
-                                                             const uint64_t* __restrict__ key_of,
-                                                             const uint2* __restrict__ long_runs,
+// One CTA per queued long run (grid-stride over the queue): the run's length by a
+// parallel scan of the truncated keys; runs already in (fp64 key, index) order
+// (checked in parallel) are left alone, others of at most kLongRun entries get a
+// bitonic sort of their (key, index) pairs in shared memory (padded to a power of
+// two with +inf keys; keys are unique per index, so the result is the stable
+// order).  Unsorted runs beyond kLongRun, or beyond the queue, are left to the
+// order check (which then triggers the full 64-bit sort).
+__global__ void __launch_bounds__(1024) long_run_sort_kernel(const uint32_t* __restrict__ k32,
+                                                             uint32_t* __restrict__ gid,
+                                                             const uint64_t* __restrict__ key_of, int64_t k,
+                                                             const uint32_t* __restrict__ long_runs,
                                                              const uint32_t* __restrict__ n_long, uint32_t max_long) {
     __shared__ uint64_t sk[kLongRun];
     __shared__ uint32_t sg[kLongRun];
+    __shared__ int s_len;
     const uint32_t nr = min(*n_long, max_long);
     for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
-        const uint2 run = long_runs[r];
+        const int64_t i0 = long_runs[r];
+        const uint32_t h = k32[i0];
+        // run length, capped at kLongRun + 1 (first differing position)
+        if (threadIdx.x == 0) s_len = kLongRun + 1;
+        __syncthreads();
+        for (int a = threadIdx.x; a <= kLongRun; a += blockDim.x) {
+            const int64_t e = i0 + a;
+            if (e >= k || k32[e] != h) atomicMin(&s_len, a);
+        }
+        __syncthreads();
+        const int len = s_len;
+        if (len > kLongRun) {  // too long to sort here; the order check decides
+            __syncthreads();
+            continue;
+        }
+        int unsorted = 0;
+        for (int a = threadIdx.x; a < len; a += blockDim.x) {
+            const uint32_t g = gid[i0 + a];
+            sg[a] = g;
+            sk[a] = key_of[g];
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a + 1 < len; a += blockDim.x)
+            unsorted |= sk[a] > sk[a + 1] || (sk[a] == sk[a + 1] && sg[a] > sg[a + 1]);
+        if (!__syncthreads_or(unsorted)) continue;
         int np2 = 64;  // the run padded to a power of two
-        while (np2 < (int)run.y) np2 <<= 1;
-        for (int a = threadIdx.x; a < np2; a += blockDim.x) {
-            if (a < (int)run.y) {
-                const uint32_t g = gid[run.x + a];
-                sg[a] = g;
-                sk[a] = key_of[g];
-            } else {
-                sg[a] = 0xffffffffu;
-                sk[a] = ~0ull;
-            }
+        while (np2 < len) np2 <<= 1;
+        for (int a = len + threadIdx.x; a < np2; a += blockDim.x) {
+            sg[a] = 0xffffffffu;
+            sk[a] = ~0ull;
         }
         __syncthreads();
         for (int size = 2; size <= np2; size <<= 1) {
@@ -364,7 +383,7 @@ __global__ void __launch_bounds__(1024) long_run_sort_kernel(uint32_t* __restric
                 __syncthreads();
             }
         }
-        for (int a = threadIdx.x; a < (int)run.y; a += blockDim.x) gid[run.x + a] = sg[a];
+        for (int a = threadIdx.x; a < len; a += blockDim.x) gid[i0 + a] = sg[a];
         __syncthreads();
     }
 }
@@ -671,14 +690,19 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     const int ntiles = v->tiles_x * v->tiles_y;
     RCGS_TRY(dalloc(&v->rank_of, n, s));
     RCGS_TRY(dalloc(&v->ranges, ntiles, s));
-    RCGS_TRY(dalloc(&v->work, 2, s));
-    RCGS_CUDA(cudaMemsetAsync(v->work, 0, 2 * sizeof(unsigned), s));
-    if (n > 0) RCGS_CUDA(cudaMemsetAsync(v->rank_of, 0xff, n * sizeof(int32_t), s));
-    RCGS_CUDA(cudaMemsetAsync(v->ranges, 0, ntiles * sizeof(uint2), s));
+    // the view's persistent work counters (words 0-1) and the build's control words,
+    // zeroed by one memset: key min (complemented) / max (u64 words 1, 2), the
+    // order-check flag and the long-run count (u32 words 6, 7)
+    RCGS_TRY(dalloc(&v->work, 8, s));
+    RCGS_CUDA(cudaMemsetAsync(v->work, 0, 8 * sizeof(unsigned), s));
+    unsigned long long* minmax = reinterpret_cast<unsigned long long*>(v->work) + 1;
+    int32_t* fix_flag = reinterpret_cast<int32_t*>(v->work + 6);
+    uint32_t* n_long = v->work + 7;
     v->k = 0;
     v->pairs = 0;
     v->sort_bits = 0;
     if (n == 0) {
+        RCGS_CUDA(cudaMemsetAsync(v->ranges, 0, ntiles * sizeof(uint2), s));
         RCGS_TRY(dalloc(&v->offs, 1, s));
         RCGS_CUDA(cudaMemsetAsync(v->offs, 0, sizeof(uint32_t), s));
         return RCGS_OK;
@@ -686,12 +710,10 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     // ---- K1: cull, keys and (for kept gaussians) the records, by scene index
     uint32_t *flag = nullptr, *kpos = nullptr, *kgid = nullptr, *kgid_alt = nullptr, *count_g = nullptr;
     uint64_t *key = nullptr, *kkey = nullptr, *kkey_alt = nullptr;
-    unsigned long long* minmax = nullptr;
     Rect* rect = nullptr;
     RCGS_TRY(dalloc(&flag, n, s));
     RCGS_TRY(dalloc(&kpos, n + 1, s));
     RCGS_TRY(dalloc(&key, n, s));
-    RCGS_TRY(dalloc(&minmax, 2, s));
     RCGS_TRY(dalloc(&v->z, n, s));
     RCGS_TRY(dalloc(&v->rec, n, s));
     RCGS_TRY(dalloc(&v->exact, n, s));
@@ -705,12 +727,9 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     v->pair_packed = pack_ok && n < ((int64_t)1 << kIdxBits);
     MaskRec* mrec = nullptr;  // packed layout: per-gaussian block-mask setup for K2 emit
     if (v->pair_packed) RCGS_TRY(dalloc(&mrec, n, s));
-    {
-        unsigned long long init[2] = {~0ull, 0ull};
-        RCGS_CUDA(cudaMemcpyAsync(minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    }
-    k1_cull_kernel<<<div_up(n, 256), 256, 0, s>>>(sc->pos, sc->cov3d, sc->opac, n, v->cam, v->cfg, flag, key,
-                                                  minmax, v->z, v->rec, v->exact, rect, count_g, mrec);
+    k1_cull_kernel<<<div_up(n > ntiles ? n : (int64_t)ntiles, 256), 256, 0, s>>>(
+        sc->pos, sc->cov3d, sc->opac, n, v->cam, v->cfg, flag, key, minmax, v->z, v->rec, v->exact, rect, count_g,
+        mrec, v->rank_of, v->ranges, ntiles);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
     uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));
@@ -720,7 +739,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_CUDA(cudaMemcpyAsync(hk, kpos + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     RCGS_CUDA(cudaStreamSynchronize(s));
     const int64_t k = *hk;
-    const uint64_t kmin = host[0], kmax = host[1];
+    const uint64_t kmin = ~host[0], kmax = host[1];
     v->k = k;
     RCGS_TRY(dalloc(&v->offs, k + 1, s));
     if (k == 0) {
@@ -728,7 +747,6 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(flag, s);
         dfree(kpos, s);
         dfree(key, s);
-        dfree(minmax, s);
         dfree(rect, s);
         dfree(mrec, s);
         dfree(count_g, s);
@@ -742,15 +760,11 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_LAUNCH_CHECK();
     dfree(flag, s);
     dfree(kpos, s);
-    dfree(minmax, s);
     // ---- stable depth sort over the varying key bits
     // keys relative to the smallest kept key (order preserving): the exponent
     // carry between e.g. [1, 2) and [2, 4) no longer widens the sorted range
     const uint64_t span = kmax - kmin;
     v->sort_bits = span ? 64 - __builtin_clzll(span) : 0;
-    int32_t* fix_flag = nullptr;
-    RCGS_TRY(dalloc(&fix_flag, 1, s));
-    RCGS_CUDA(cudaMemsetAsync(fix_flag, 0, sizeof(int32_t), s));
     if (v->sort_bits > 0) {
         if (v->sort_bits <= kDepthKeyBits || !v->full_sort) {
             // 4-byte keys holding the top kDepthKeyBits varying bits (3 radix passes;
@@ -765,16 +779,12 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
                                     v->sort_bits < kDepthKeyBits ? v->sort_bits : kDepthKeyBits, s));
             if (shift > 0) {
                 const uint32_t max_long = (uint32_t)(k / 33 + 1);
-                uint2* long_runs = nullptr;
-                uint32_t* n_long = nullptr;
+                uint32_t* long_runs = nullptr;
                 RCGS_TRY(dalloc(&long_runs, max_long, s));
-                RCGS_TRY(dalloc(&n_long, 1, s));
-                RCGS_CUDA(cudaMemsetAsync(n_long, 0, sizeof(uint32_t), s));
                 depth_fixup_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k, long_runs, n_long, max_long);
-                long_run_sort_kernel<<<64, 1024, 0, s>>>(kgid, key, long_runs, n_long, max_long);
+                long_run_sort_kernel<<<128, 1024, 0, s>>>(k32, kgid, key, k, long_runs, n_long, max_long);
                 depth_check_kernel<<<div_up(k, 256), 256, 0, s>>>(k32, kgid, key, k, fix_flag);
                 dfree(long_runs, s);
-                dfree(n_long, s);
             }
             RCGS_LAUNCH_CHECK();
             dfree(k32, s);
@@ -801,7 +811,6 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_CUDA(cudaMemcpyAsync(hp + 1, fix_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RCGS_CUDA(cudaStreamSynchronize(s));
     const int64_t pairs = hp[0];
-    dfree(fix_flag, s);
     dfree(count, s);
     if (hp[1] != 0) {  // a long tie run needs the full 64-bit key sort: rebuild
         dfree(rect, s);
