@@ -284,6 +284,7 @@ struct rcgs_view {
     bool pair_packed;
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
+    uint4* tile_meta;     // (tiles,) per work-order position: {tile, range start, range end, 0}
     unsigned* work;       // (2,) work-item / exited-warp counters of the persistent launches
     // composite-weight records (rcgs_render_train; geometry + camera only), in the
     // process-wide record arena (raster.cu) while this view owns it

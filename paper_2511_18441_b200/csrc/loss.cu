@@ -180,6 +180,15 @@ __device__ void loss_tail(const double* __restrict__ part, int nb, const LossTai
     }
 }
 
+// 4- or 8-byte asynchronous global -> shared copy (LDGSTS); `in` false zero-fills
+template <typename E>
+__device__ __forceinline__ void cp_async_elem(E* dst, const E* src, bool in) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(sizeof(E)),
+                 "r"(in ? (int)sizeof(E) : 0)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- pass A
 template <bool SSIM, typename T, typename MT>
 __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restrict__ y, const T* __restrict__ g, int H,
@@ -222,16 +231,33 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
 #pragma unroll
         for (int i = 0; i < kRows; ++i) inv_mass[i] = 1.0 / (mrow[r0 + i] * mcol[c]);
     }
+    // a channel's y / g planes (with the halo, zero outside the image) stream into
+    // iy / ig with async copies: channel 0 up front, channel c + 1 as soon as the
+    // horizontal pass of channel c has consumed the planes, so its load overlaps
+    // channel c's vertical pass and SSIM algebra
+    // (halo row r, column cc) of element i advanced incrementally (no divisions);
+    // 32-bit element offsets (the host checks 3 H W < 2^31)
+    auto stage = [&](int ch) {
+        int r = t / kLH, cc = t - (t / kLH) * kLH;
+        for (int i = t; i < kLH * kLH; i += kLNT) {
+            const int gy = y0 - kR + r, gx = x0 - kR + cc;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const uint32_t gi = in ? ((uint32_t)gy * (uint32_t)W + (uint32_t)gx) * 3u + (uint32_t)ch : 0u;
+            cp_async_elem(iy + i, y + gi, in);
+            cp_async_elem(ig + i, g + gi, in);
+            cc += kLNT % kLH;
+            r += kLNT / kLH;
+            if (cc >= kLH) {
+                cc -= kLH;
+                ++r;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (SSIM) stage(0);
     for (int ch = 0; ch < 3; ++ch) {
         if (SSIM) {
-            for (int i = t; i < kLH * kLH; i += kLNT) {
-                const int r = i / kLH, cc = i % kLH;
-                const int gy = y0 - kR + r, gx = x0 - kR + cc;
-                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-                const int64_t gi = ((int64_t)gy * W + gx) * 3 + ch;
-                iy[i] = in ? y[gi] : T(0);
-                ig[i] = in ? g[gi] : T(0);
-            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncthreads();
             // horizontal pass: each item a strip of kHS adjacent outputs of one row
             // from a register-resident segment (squares formed once per input) for
@@ -279,6 +305,7 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
                 }
             }
             __syncthreads();
+            if (ch + 1 < 3) stage(ch + 1);  // iy / ig are free until the next horizontal pass
         }
         double m[5][kRows];
         if (SSIM) {
@@ -328,15 +355,6 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_a(const T* __restri
     loss_tail(block_part, gridDim.x * gridDim.y, lt, red);
 }
 
-// 4- or 8-byte asynchronous global -> shared copy (LDGSTS); `in` false zero-fills
-template <typename E>
-__device__ __forceinline__ void cp_async_elem(E* dst, const E* src, bool in) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(sizeof(E)),
-                 "r"(in ? (int)sizeof(E) : 0)
-                 : "memory");
-}
-
 // ---------------------------------------------------------------- pass B
 // The separable filter of the three maps runs in MT: fp64 for the fp64 entry
 // point, fp32 for the fp32 one (whose maps are already stored in fp32; the
@@ -362,13 +380,21 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
     // image) stream into the other buffer while this channel computes
     auto issue = [&](int ch) {
         MT* buf = imb + (ch & 1) * 3 * kLH * kLH;
+        const MT* m0 = maps + (int64_t)ch * npix;
+        const uint32_t mstride = (uint32_t)(npix * 3);
+        int r = t / kLH, cc = t - (t / kLH) * kLH;  // advanced incrementally, as in pass A
         for (int i = t; i < kLH * kLH; i += kLNT) {
-            const int r = i / kLH, cc = i % kLH;
             const int gy = y0 - kR + r, gx = x0 - kR + cc;
             const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const int64_t gi = in ? (int64_t)ch * npix + (int64_t)gy * W + gx : 0;
+            const uint32_t gi = in ? (uint32_t)gy * (uint32_t)W + (uint32_t)gx : 0u;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) cp_async_elem(buf + q * kLH * kLH + i, maps + q * npix * 3 + gi, in);
+            for (int q = 0; q < 3; ++q) cp_async_elem(buf + q * kLH * kLH + i, m0 + q * mstride + gi, in);
+            cc += kLNT % kLH;
+            r += kLNT / kLH;
+            if (cc >= kLH) {
+                cc -= kLH;
+                ++r;
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -484,6 +510,7 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     RCGS_CHECK_ARG(d_image && d_target && d_loss3 && d_grad, "null argument");
     RCGS_CHECK_ARG(height > 0 && width > 0, "expected (H, W, 3) images, got (%d, %d, 3)", height, width);
     RCGS_CHECK_ARG(lam >= 0.0 && lam <= 1.0, "lam must be in [0, 1]");
+    RCGS_CHECK_ARG((int64_t)height * width * 9 < ((int64_t)1 << 32), "image too large for 32-bit loss offsets");
     const bool ssim_ok = height >= kWin && width >= kWin;
     RCGS_CHECK_ARG(ssim_ok || lam == 0.0, "images must be at least %dpx on each side for SSIM", kWin);
     cudaStream_t s = as_stream(stream);

@@ -502,7 +502,7 @@ __global__ void k2_ranges_kernel(const uint32_t* __restrict__ tile_key, const ui
 // launch.  Any order gives identical results (items are independent), so a
 // single-CTA bucket scatter on count / max * 255 is enough.
 __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int ntiles,
-                                                          uint32_t* __restrict__ order) {
+                                                          uint32_t* __restrict__ order, uint4* __restrict__ meta) {
     __shared__ uint32_t hist[256];
     __shared__ uint32_t s_max;
     const int t = threadIdx.x;
@@ -533,7 +533,14 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
         }
     }
     __syncthreads();
-    for (int i = t; i < ntiles; i += blockDim.x) order[atomicAdd(&hist[bucket(i)], 1u)] = (uint32_t)i;
+    // meta: the raster's per-item tile and list range in one 16-byte load (instead of
+    // the dependent order -> ranges pair at the start of every work item)
+    for (int i = t; i < ntiles; i += blockDim.x) {
+        const uint32_t slot = atomicAdd(&hist[bucket(i)], 1u);
+        order[slot] = (uint32_t)i;
+        const uint2 r = ranges[i];
+        meta[slot] = make_uint4((uint32_t)i, r.x, r.y, 0u);
+    }
 }
 
 // ---------------------------------------------------------------- colour (per step)
@@ -670,6 +677,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->pair_m, s);
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
+    dfree(v->tile_meta, s);
     dfree(v->work, s);
     release_records(v, s);  // arena ownership, or the view-owned compact copy
     v->wrec_n = v->wrec_s = nullptr;
@@ -844,7 +852,8 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
                                                         v->ranges, v->pair_m);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
-    tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order);
+    RCGS_TRY(dalloc(&v->tile_meta, ntiles, s));
+    tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order, v->tile_meta);
     RCGS_LAUNCH_CHECK();
     dfree(g_alt, s);
     dfree(tkey, s);

@@ -115,6 +115,7 @@ __device__ __forceinline__ void write_pixel(const PixelOut& o, int W, int H, int
 struct RasterArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // work order (nullptr: row-major)
+    const uint4* tile_meta;      // per work-order position {tile, range} (nullptr: tile_order + ranges)
     const uint32_t* pair_g;  // tile lists: scene indices in depth order
     const uint32_t* pair_m;  // per list entry: 8x4 blocks of its tile the footprint reaches
                              // (null: packed above the scene index in pair_g)
@@ -468,7 +469,16 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         if (lane == 0) item = atomicAdd(a.counter, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (unsigned)a.n_items) break;
-        const int tile = a.tile_order ? (int)a.tile_order[item / kBlocksPerTile] : (int)(item / kBlocksPerTile);
+        int tile;
+        uint2 range;
+        if (a.tile_meta) {
+            const uint4 tm = a.tile_meta[item / kBlocksPerTile];
+            tile = (int)tm.x;
+            range = make_uint2(tm.y, tm.z);
+        } else {
+            tile = a.tile_order ? (int)a.tile_order[item / kBlocksPerTile] : (int)(item / kBlocksPerTile);
+            range = a.ranges[tile];
+        }
         const int blk = (int)(item % kBlocksPerTile);
         const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
         const int bx0 = tx * kTile + (blk & 1) * 8, by0 = ty * kTile + (blk >> 1) * 4;
@@ -502,7 +512,6 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         if (M == HITS && inside && a.mask[pix] == 0) T = 0.f;
         if (M == CAP_WRITE && inside) cap_base = a.cap_offs[pix];
 
-        const uint2 range = a.ranges[tile];
         const float fbx0 = (float)bx0, fby0 = (float)by0;
         const float cxf = fbx0 + 3.5f, cyf = fby0 + 1.5f;
         if (kInstr && M == FWDREC && a.counters) {
@@ -1223,6 +1232,7 @@ static RasterArgs base_args(const rcgs_view* v) {
     memset(&a, 0, sizeof(a));
     a.ranges = v->ranges;
     a.tile_order = v->tile_order;
+    a.tile_meta = v->tile_meta;
     a.pair_g = v->pair_g;
     a.pair_m = v->pair_packed ? nullptr : v->pair_m;
     a.idx_mask = v->pair_packed ? kIdxMask : 0xffffffffu;
