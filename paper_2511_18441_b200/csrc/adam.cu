@@ -45,6 +45,20 @@ __device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const flo
     }
 }
 
+// The fp64 colour (color_kernel's fallback) of the gaussians the Adam colour
+// epilogue queued in fix = {count, g...}; one CTA, which re-arms the count.
+__global__ void __launch_bounds__(256) color_fixup_kernel(uint32_t* __restrict__ fix, const double* __restrict__ pos,
+                                                          const float4* __restrict__ sh, Center cen, int deg,
+                                                          float4* __restrict__ color) {
+    const uint32_t cnt = fix[0];
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const int64_t g = fix[1 + i];
+        color[g] = color_f64(pos, sh, g, cen, deg);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) fix[0] = 0u;
+}
+
 // Bias corrections 1/(1 - beta^t) for t = step + 1, once per launch (fp64 pow).
 __global__ void adam_prep_kernel(const int64_t* __restrict__ step, double db1, double db2,
                                  float2* __restrict__ inv) {
@@ -162,7 +176,8 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
     float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
     unsigned* __restrict__ ticket, int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
-    Center next_cen, float4* __restrict__ next_color, double* __restrict__ reject_record,
+    Center next_cen, float4* __restrict__ next_color, uint32_t* __restrict__ next_fix,
+    double* __restrict__ reject_record,
     float* __restrict__ snapshot, int64_t* __restrict__ snapshot_step, int64_t snapshot_every,
     const uint32_t* __restrict__ tile_state) {
     // a rejected step (non-finite gradient) leaves SH/m/v untouched; with a fused
@@ -338,40 +353,44 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
         if (next_color != nullptr) {
             // fused colour pass of the next step's view (render.py:209-214) from the
             // updated coefficients in registers, overlapping the stage's refill: each
-            // of a gaussian's 4 threads evaluates its basis-row quarter (fp64, the
-            // order color_kernel uses, bit-identical) and lane part 0 combines and
-            // writes the colour.  The normalised direction (view_dir's operations)
-            // costs one fp64 division per lane: lane part p divides component p, then
-            // the 4 lanes exchange.
-            const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-            const double q = (part == 0 ? dx : (part == 1 ? dy : dz)) / nrm;
-            const int lb = lane & ~3;
-            const double x = __shfl_sync(0xffffffffu, q, lb), y = __shfl_sync(0xffffffffu, q, lb + 1),
-                         z = __shfl_sync(0xffffffffu, q, lb + 2);
-            double qv[3] = {0.0, 0.0, 0.0};
+            // of a gaussian's 4 threads evaluates its basis-row quarter in fp32 (the
+            // operations and order of color_kernel, so the same bits) and lane part 0
+            // combines and writes the colour.  A gaussian whose activation is too
+            // close to call in fp32 takes the fp64 colour (color_kernel's fallback);
+            // its direction costs one fp64 division per lane (lane part p divides
+            // component p, then the 4 lanes exchange).
+            float fx, fy, fz;
+            dir_f32(dx, dy, dz, fx, fy, fz);
+            float qf[3] = {0.f, 0.f, 0.f}, mf[3] = {0.f, 0.f, 0.f};
             if (rs >= 0) {
-                double b[16];
-                sh_basis16<double>(x, y, z, deg, b);
-                color_quarter(b, c12, part, qv);
+                float bf[16];
+                basis16_rn(fx, fy, fz, deg, bf);
+                color_quarter_f32(bf, c12, part, qf, mf);
             }
-            double q1[3], q2[3], q3[3];
+            float col[3];
+            int act = 0;
+            bool amb = false;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                q1[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 1);
-                q2[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 2);
-                q3[ch] = __shfl_down_sync(0xffffffffu, qv[ch], 3);
+                const float q1 = __shfl_down_sync(0xffffffffu, qf[ch], 1), q2 = __shfl_down_sync(0xffffffffu, qf[ch], 2),
+                            q3 = __shfl_down_sync(0xffffffffu, qf[ch], 3);
+                const float m1 = __shfl_down_sync(0xffffffffu, mf[ch], 1), m2 = __shfl_down_sync(0xffffffffu, mf[ch], 2),
+                            m3 = __shfl_down_sync(0xffffffffu, mf[ch], 3);
+                const float v = __fadd_rn(color_combine_f32(qf[ch], q1, q2, q3), 0.5f);
+                amb = amb || color_ambiguous(v, color_combine_f32(mf[ch], m1, m2, m3));
+                act |= (v > 0.f) << ch;
+                col[ch] = fmaxf(0.f, v);
             }
-            if (rs >= 0 && part == 0) {  // colours are stored by scene index
-                float col[3];
-                int act = 0;
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    const double val = color_combine(qv[ch], q1[ch], q2[ch], q3[ch]) + 0.5;
-                    act |= (val > 0.0) << ch;
-                    col[ch] = (float)fmax(0.0, val);
-                }
+            amb = amb && rs >= 0 && part == 0;
+            // rare (never at C3): the gaussian is queued for the fp64 colour, which
+            // color_fixup_kernel writes after this launch (an inline fp64 fallback
+            // cost the common path ~40% of the kernel through its registers alone)
+            if (amb) {
+                const uint32_t slot = atomicAdd(next_fix, 1u);
+                next_fix[1 + slot] = (uint32_t)g;
+            }
+            if (rs >= 0 && part == 0)  // colours are stored by scene index
                 next_color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
-            }
         }
     }
     if (t == 0) {
@@ -512,10 +531,12 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
         Center nc = {{0.0, 0.0, 0.0}};
         const int32_t* nrank = nullptr;
         float4* ncolor = nullptr;
+        uint32_t* nfix = nullptr;
         if (next_view != nullptr && next_view->k > 0) {
             nc = camera_center(next_view->cam);
             nrank = next_view->rank_of;
             ncolor = next_view->color;
+            nfix = next_view->fix;
         }
         if (d_tile_state != nullptr) {
             adam_active_kernel<<<div_up(sc->n, 256), 256, 0, s>>>(av, sc->n, d_tile_state);
@@ -524,9 +545,14 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
         // bias corrections from and commit of the device step counter happen inside
         adam_fused_kernel<<<(int)(ntiles < grid ? ntiles : grid), kAThreads, smem, s>>>(
             sc->pos, sc->n, sc->sh_degree, d_sh, d_m, d_v, av, hyper(cfg), d_step, cfg->beta1, cfg->beta2, ticket,
-            d_reject, nrank, nc, ncolor, d_reject_record, pub ? pub->d_snapshot : nullptr,
+            d_reject, nrank, nc, ncolor, nfix, d_reject_record, pub ? pub->d_snapshot : nullptr,
             pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0, d_tile_state);
         RCGS_LAUNCH_CHECK();
+        if (ncolor != nullptr) {
+            color_fixup_kernel<<<1, 256, 0, s>>>(nfix, sc->pos, reinterpret_cast<const float4*>(d_sh), nc,
+                                                 sc->sh_degree, ncolor);
+            RCGS_LAUNCH_CHECK();
+        }
         return RCGS_OK;
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step, d_reject_record, pub ? pub->d_snapshot_step : nullptr,

@@ -277,6 +277,7 @@ struct rcgs_view {
     uint32_t* offs;       // (k+1,) first emission slot of s; offs[k] = pairs
     float4* color;        // (n,) rgb + active bits (as float 0..7) per step
     int32_t* rank_of;     // (n,) s or -1 (culled)
+    uint32_t* fix;        // (n + 1,) {count, g...}: gaussians the Adam colour epilogue left to the fp64 fixup
     // per pair (sorted by tile, then depth)
     uint32_t* pair_g;     // (pairs,) scene index g
     uint32_t* pair_m;     // (pairs,) tile_block_mask of the pair (8x4 blocks its footprint reaches);

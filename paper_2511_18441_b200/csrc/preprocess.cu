@@ -150,11 +150,12 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
                                RasterRec* __restrict__ rec, ExactRec* __restrict__ exact,
                                Rect* __restrict__ rect, uint32_t* __restrict__ count,
                                MaskRec* __restrict__ mrec, int32_t* __restrict__ rank_of,
-                               uint2* __restrict__ ranges, int ntiles) {
+                               uint2* __restrict__ ranges, int ntiles, uint32_t* __restrict__ fix) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // the view's empty tile ranges (k2_ranges fills the non-empty ones) and the
     // culled default of rank_of (k1_rank writes the kept ranks), instead of memsets
     if (g < ntiles) ranges[g] = make_uint2(0u, 0u);
+    if (g == 0) *fix = 0u;  // the colour fixup queue (Adam colour epilogue) starts empty
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (g < n) {
         rank_of[g] = -1;
@@ -547,39 +548,46 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
 // Per-step colour (render.py:209-214), iterated in scene order so the 192-byte SH
 // rows are read fully coalesced; the 16-byte result goes to the gaussian's
 // depth-rank slot.
-__global__ void color_kernel(const double* __restrict__ pos, const float4* __restrict__ sh,
-                             const int32_t* __restrict__ rank_of, int64_t n, Center cen, int deg,
-                             float4* __restrict__ color) {
+__global__ void __launch_bounds__(256, 4) color_kernel(const double* __restrict__ pos, const float4* __restrict__ sh,
+                                                      const int32_t* __restrict__ rank_of, int64_t n, Center cen,
+                                                      int deg, float4* __restrict__ color) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     if (rank_of[g] < 0) return;  // culled in this view
-    double x, y, z;
-    view_dir(pos, g, cen.c, x, y, z);
-    double b[16];
-    sh_basis16<double>(x, y, z, deg, b);
-    float c[48];
+    // fp32 colour (shmath.cuh), quarters combined in the order the Adam colour
+    // epilogue uses, so both give the same bits
+    float fx, fy, fz;
+    dir_f32(pos[3 * g] - cen.c[0], pos[3 * g + 1] - cen.c[1], pos[3 * g + 2] - cen.c[2], fx, fy, fz);
+    float bf[16];
+    basis16_rn(fx, fy, fz, deg, bf);
     const float4* row = sh + g * 12;
+    float qf[4][3], mf[4][3];
 #pragma unroll
-    for (int i = 0; i < 12; ++i) {
-        const float4 f = row[i];
-        c[4 * i] = f.x;
-        c[4 * i + 1] = f.y;
-        c[4 * i + 2] = f.z;
-        c[4 * i + 3] = f.w;
+    for (int part = 0; part < 4; ++part) {
+        float c12[12];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const float4 f = row[3 * part + i];
+            c12[4 * i] = f.x;
+            c12[4 * i + 1] = f.y;
+            c12[4 * i + 2] = f.z;
+            c12[4 * i + 3] = f.w;
+        }
+        color_quarter_f32(bf, c12, part, qf[part], mf[part]);
     }
-    double qv[4][3];  // quarters in the order shared with the Adam colour epilogue
-#pragma unroll
-    for (int part = 0; part < 4; ++part) color_quarter(b, c + 12 * part, part, qv[part]);
-    double raw[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) raw[ch] = color_combine(qv[0][ch], qv[1][ch], qv[2][ch], qv[3][ch]);
     int act = 0;
     float col[3];
+    bool amb = false;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-        const double v = raw[ch] + 0.5;
-        act |= (v > 0.0) << ch;
-        col[ch] = (float)fmax(0.0, v);
+        const float v = __fadd_rn(color_combine_f32(qf[0][ch], qf[1][ch], qf[2][ch], qf[3][ch]), 0.5f);
+        amb = amb || color_ambiguous(v, color_combine_f32(mf[0][ch], mf[1][ch], mf[2][ch], mf[3][ch]));
+        act |= (v > 0.f) << ch;
+        col[ch] = fmaxf(0.f, v);
+    }
+    if (amb) {  // activation too close to call in fp32: the fp64 colour (exact decision)
+        color[g] = color_f64(pos, sh, g, cen, deg);
+        return;
     }
     color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
 }
@@ -673,6 +681,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->offs, s);
     dfree(v->color, s);
     dfree(v->rank_of, s);
+    dfree(v->fix, s);
     dfree(v->pair_g, s);
     dfree(v->pair_m, s);
     dfree(v->ranges, s);
@@ -697,6 +706,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     const int64_t n = sc->n;
     const int ntiles = v->tiles_x * v->tiles_y;
     RCGS_TRY(dalloc(&v->rank_of, n, s));
+    RCGS_TRY(dalloc(&v->fix, n + 1, s));
     RCGS_TRY(dalloc(&v->ranges, ntiles, s));
     // the view's persistent work counters (words 0-1) and the build's control words,
     // zeroed by one memset: key min (complemented) / max (u64 words 1, 2), the
@@ -710,6 +720,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     v->pairs = 0;
     v->sort_bits = 0;
     if (n == 0) {
+        RCGS_CUDA(cudaMemsetAsync(v->fix, 0, sizeof(uint32_t), s));
         RCGS_CUDA(cudaMemsetAsync(v->ranges, 0, ntiles * sizeof(uint2), s));
         RCGS_TRY(dalloc(&v->offs, 1, s));
         RCGS_CUDA(cudaMemsetAsync(v->offs, 0, sizeof(uint32_t), s));
@@ -737,7 +748,7 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     if (v->pair_packed) RCGS_TRY(dalloc(&mrec, n, s));
     k1_cull_kernel<<<div_up(n > ntiles ? n : (int64_t)ntiles, 256), 256, 0, s>>>(
         sc->pos, sc->cov3d, sc->opac, n, v->cam, v->cfg, flag, key, minmax, v->z, v->rec, v->exact, rect, count_g,
-        mrec, v->rank_of, v->ranges, ntiles);
+        mrec, v->rank_of, v->ranges, ntiles, v->fix);
     RCGS_LAUNCH_CHECK();
     RCGS_TRY(exclusive_scan_u32(flag, kpos, n, s));
     uint64_t* host = static_cast<uint64_t*>(pinned_scratch(4 * sizeof(uint64_t)));

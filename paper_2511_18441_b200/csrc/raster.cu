@@ -464,11 +464,21 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
     const float lxf = (float)(lane & 7) - 3.5f, lyf = (float)(lane >> 3) - 1.5f;
     const float G2 = a.f_gate2;
 
+#ifdef RCGS_RASTER_ITEM_PREFETCH
+    unsigned nraw = 0;
+    if (lane == 0) nraw = atomicAdd(a.counter, 1u);
+#endif
     for (;;) {
+#ifdef RCGS_RASTER_ITEM_PREFETCH
+        const unsigned item = __shfl_sync(0xffffffffu, nraw, 0);
+        if (item >= (unsigned)a.n_items) break;
+        if (lane == 0) nraw = atomicAdd(a.counter, 1u);
+#else
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(a.counter, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (unsigned)a.n_items) break;
+#endif
         int tile;
         uint2 range;
         if (a.tile_meta) {

@@ -823,3 +823,76 @@ def test_tile_list_layouts_agree(tmp_path):
         res[pack] = np.load(out)
     for key in res["1"].files:
         np.testing.assert_array_equal(res["1"][key], res["0"][key])
+
+
+@pytest.mark.gpu
+def test_color_activation_boundary_exact():
+    """The per-step colour is evaluated in fp32 with an fp64 fallback for the
+    activation decision raw + 0.5 > 0 (render.py:211-214): gaussians whose DC
+    coefficient puts raw + 0.5 within a few fp32 ulps of 0 must get the fp64
+    reference's decision, both from color_kernel and from the Adam colour
+    epilogue (which must also agree with color_kernel bit for bit)."""
+    import ctypes
+    import torch
+    from paper_2511_18441_b200 import _native as N, device as D
+    from oracle.raster import sh_basis, camera_center
+    rng = np.random.default_rng(5)
+    n = 4000
+    pos = np.column_stack([rng.uniform(-1.2, 1.2, n), rng.uniform(-0.9, 0.9, n), rng.uniform(2.0, 4.0, n)])
+    rot = rng.normal(size=(n, 4))
+    rot /= np.linalg.norm(rot, axis=1, keepdims=True)
+    scl = rng.uniform(0.005, 0.03, (n, 3))
+    opa = rng.uniform(0.3, 0.9, n)
+    sh = (rng.normal(size=(n, 16, 3)) * 0.05).astype(np.float32).astype(np.float64)
+    intr = P.CameraIntrinsics(300.0, 300.0, 159.5, 119.5, 320, 240)
+    pose = P.CameraPose(np.eye(3), np.zeros(3))
+    d = pos - camera_center(pose)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    basis = sh_basis(d, 3)
+    rest = np.einsum("nk,nkc->nc", basis[:, 1:], sh[:, 1:])
+    c0 = ((-0.5 - rest) / basis[:, :1]).astype(np.float32)  # raw + 0.5 ~ 0 in every channel
+    nudge = rng.integers(-3, 4, size=(n, 3))
+    for k in range(1, 4):  # move some channels by k fp32 ulps either way
+        c0 = np.where(nudge >= k, np.nextafter(c0, np.float32(np.inf)), c0)
+        c0 = np.where(nudge <= -k, np.nextafter(c0, np.float32(-np.inf)), c0)
+    sh[:, 0, :] = c0.astype(np.float64)
+    scene = P.Scene(pos, rot, scl, opa, sh, 3)
+    ref = OR.project(scene, intr, pose)
+    raw64 = np.einsum("nk,nkc->nc", ref.basis, sh[ref.index]) + 0.5
+    assert np.mean(np.abs(raw64) < 1e-5) > 0.9  # the fp32 band is exercised
+    clear = np.abs(raw64) > 1e-13                 # decisions independent of the fp64 sum order
+    cap = P.render_forward(scene, intr, pose)
+    np.testing.assert_array_equal(cap.kept_index, ref.index)
+    assert np.array_equal(cap.active[clear], ref.active[clear])
+
+    # the fused colour epilogue of a zero-gradient Adam step (SH unchanged) on the same view
+    ds = D.DeviceScene(scene.positions, scene.rotations, scene.scales, scene.opacities, 3)
+    sh_dev = torch.from_numpy(sh.astype(np.float32)).cuda().contiguous()
+    v_ref = D.View(ds, intr, pose, P.DEFAULT_CONFIG).color(sh_dev)
+    v_fused = D.View(ds, intr, pose, P.DEFAULT_CONFIG)
+    m = torch.zeros_like(sh_dev)
+    v = torch.zeros_like(sh_dev)
+    acc = torch.zeros((n, 3), dtype=torch.float32, device="cuda")
+    reject = torch.zeros(1, dtype=torch.int32, device="cuda")
+    step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rec = torch.zeros(1, dtype=torch.float64, device="cuda")
+    cfg = D.adam_config(P.OptimizerConfig())
+    ptrs = (ctypes.c_void_p * 1)(acc.data_ptr())
+    cen = (ctypes.c_double * 3)(*camera_center(pose))
+    sh_before = sh_dev.clone()
+    N.call("rcgs_adam_fused_next", ds.handle, N.ptr(sh_dev), N.ptr(m), N.ptr(v), ptrs, cen, 1, ctypes.byref(cfg),
+           N.ptr(reject), N.ptr(step), N.ptr(rec), v_fused.handle, D.stream_ptr())
+    v_fused._colored = True
+    assert torch.equal(sh_dev, sh_before)
+    assert torch.equal(v_fused.render(None, 0), v_ref.render(None, 0))
+    k = v_ref.n_kept
+    outs = []
+    for view in (v_ref, v_fused):
+        b = torch.empty((k, 16), dtype=torch.float64, device="cuda")
+        a = torch.empty((k, 3), dtype=torch.uint8, device="cuda")
+        N.call("rcgs_view_basis", view.handle, N.ptr(b), N.ptr(a), D.stream_ptr())
+        outs.append(a.cpu().numpy().astype(bool))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[1][clear], ref.active[clear])
+    v_ref.close()
+    v_fused.close()
