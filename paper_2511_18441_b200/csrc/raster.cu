@@ -446,7 +446,7 @@ __device__ __noinline__ SlowOut slow_entry(const uint32_t* __restrict__ pair_g, 
 // straddles the stop floor (or tau) -- raises one warp vote per entry that sends
 // the warp to the slow path for that entry.
 #ifndef RCGS_FWDREC_MIN_CTAS
-#define RCGS_FWDREC_MIN_CTAS 4
+#define RCGS_FWDREC_MIN_CTAS 3
 #endif
 template <int M, bool kInstr>
 __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : kMinCTAs) * 8 / kRWarps)
@@ -464,21 +464,25 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
     const float lxf = (float)(lane & 7) - 3.5f, lyf = (float)(lane >> 3) - 1.5f;
     const float G2 = a.f_gate2;
 
-#ifdef RCGS_RASTER_ITEM_PREFETCH
+    // FWDREC (3 CTAs/SM, 80 registers) takes its work items one ahead: the atomic
+    // for the next item is in flight while this one is processed (its round trip
+    // was ~7% of the warp samples).  At the 64-register budget of the other modes
+    // the extra live value made ptxas rematerialise lane constants inside the
+    // entry loop (+24%), so they fetch on demand.
+    constexpr bool kAhead = M == FWDREC;
     unsigned nraw = 0;
-    if (lane == 0) nraw = atomicAdd(a.counter, 1u);
-#endif
+    if (kAhead && lane == 0) nraw = atomicAdd(a.counter, 1u);
     for (;;) {
-#ifdef RCGS_RASTER_ITEM_PREFETCH
-        const unsigned item = __shfl_sync(0xffffffffu, nraw, 0);
-        if (item >= (unsigned)a.n_items) break;
-        if (lane == 0) nraw = atomicAdd(a.counter, 1u);
-#else
         unsigned item = 0;
-        if (lane == 0) item = atomicAdd(a.counter, 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= (unsigned)a.n_items) break;
-#endif
+        if (kAhead) {
+            item = __shfl_sync(0xffffffffu, nraw, 0);
+            if (item >= (unsigned)a.n_items) break;
+            if (lane == 0) nraw = atomicAdd(a.counter, 1u);
+        } else {
+            if (lane == 0) item = atomicAdd(a.counter, 1u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= (unsigned)a.n_items) break;
+        }
         int tile;
         uint2 range;
         if (a.tile_meta) {
