@@ -146,7 +146,10 @@ constexpr int kAG = RCGS_ADAM_TILE;
 static_assert(kAG % 8 == 0 && kAG <= 64, "whole warps of 8 gaussians; 16-byte side-array tiles");
 constexpr int kAThreads = 4 * kAG;          // 4 threads per gaussian, 12 coefficients each
 constexpr int kStateG = 64;                 // gaussians per tile_state entry (ABI: 64-gaussian blocks)
-constexpr int kAStages = 2;                 // tiles in flight per CTA
+#ifndef RCGS_ADAM_STAGES
+#define RCGS_ADAM_STAGES 2
+#endif
+constexpr int kAStages = RCGS_ADAM_STAGES;  // tiles in flight per CTA
 constexpr uint32_t kARow = 48 * 4;          // bytes of one gaussian's SH (or m, or v)
 constexpr uint32_t kATileBytes = kAG * kARow;
 // A stage holds, besides the SH / m / v tiles, the tile's positions (fp64 x 3),

@@ -1,6 +1,7 @@
 // Shared helpers for the rcgs CUDA library (sm_100a).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <stdint.h>
@@ -256,6 +257,41 @@ __device__ __forceinline__ uint32_t tile_block_mask(const float4 ra, const float
     return tile_block_mask(mask_setup(ra, rb, rc), tx0, ty0);
 }
 
+// Does the cull record's footprint box touch the 8x4 block at (bx0, by0)?
+__device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float by0) {
+    const unsigned packed = __float_as_uint(ra.z);
+    const float ex = __half2float(__ushort_as_half((unsigned short)(packed & 0xffffu)));
+    const float ey = __half2float(__ushort_as_half((unsigned short)(packed >> 16)));
+    return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 3.f;
+}
+
+// Can the footprint {power2 >= p_lo} reach any point of the rectangle
+// [x0, x1] x [y0, y1]?  Q = -power2 is a PSD quadratic of the offset from the
+// mean; its minimum over the box is 0 when the mean is inside, else it lies on
+// an edge, where the 1-D minimiser is a clamp.  The candidates' fp32 values are
+// lowered by their evaluation error bound (2e-6 of the absolute term sum, plus
+// 1.5e-4 = 1e-4 natural-log units), so the test only drops entries whose power
+// stays below the gate at every pixel of the rectangle -- alpha exactly 0 in
+// fp64 there -- and the results do not change.  NaN keeps the entry.
+__device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const float4 rb, const float4 rc, float x0,
+                                                     float y0, float x1, float y1) {
+    const float X0 = (x0 - ra.x) - rb.x, X1 = (x1 - ra.x) - rb.x;
+    const float Y0 = (y0 - ra.y) - rb.y, Y1 = (y1 - ra.y) - rb.y;
+    if (X0 <= 0.f && X1 >= 0.f && Y0 <= 0.f && Y1 >= 0.f) return true;
+    const float A = -rc.x, B = -rc.y, C = -rc.z;
+    const float hA = __fdividef(-0.5f * B, A), hC = __fdividef(-0.5f * B, C);
+    auto lower = [&](float dx, float dy) {  // lower bound of Q(dx, dy)
+        const float xx = A * dx * dx, yy = C * dy * dy, xy = B * dx * dy;
+        return (xx + yy + xy) - fmaf(2e-6f, xx + yy + fabsf(xy), 1.5e-4f);
+    };
+    auto clampf = [](float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); };
+    float m = lower(X0, clampf(hC * X0, Y0, Y1));
+    m = fminf(m, lower(X1, clampf(hC * X1, Y0, Y1)));
+    m = fminf(m, lower(clampf(hA * Y0, X0, X1), Y0));
+    m = fminf(m, lower(clampf(hA * Y1, X0, X1), Y1));
+    return !(m > -rb.z);
+}
+
 // Exact (fp64) record for guarded decisions: the reference's own operands.
 struct ExactRec {
     double mx, my, ca, cb, cc, op;
@@ -286,6 +322,8 @@ struct rcgs_view {
     uint2* ranges;        // (tiles,) [start, end)
     uint32_t* tile_order; // (tiles,) tiles by descending entry count (raster work order)
     uint4* tile_meta;     // (tiles,) per work-order position: {tile, range start, range end, 0}
+    uint32_t* blist;      // (8 * pairs,) per-block lists: block b of a tile at 8 range.x + b (range.y - range.x)
+    uint32_t* bcount;     // (tiles * 8,) their lengths, by work item (8 work position + block)
     unsigned* work;       // (2,) work-item / exited-warp counters of the persistent launches
     // composite-weight records (rcgs_render_train; geometry + camera only), in the
     // process-wide record arena (raster.cu) while this view owns it

@@ -239,6 +239,19 @@ __global__ void k1_cull_kernel(const double* __restrict__ pos, const double* __r
     }
 }
 
+// Compaction straight to the 4-byte truncated, rebased depth keys (the common
+// path; compact_kernel + key_rebase_kernel feed the full 64-bit sort).
+__global__ void compact_k32_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                                   const uint64_t* __restrict__ key, int64_t n, uint64_t kmin, int shift,
+                                   uint32_t* __restrict__ k32, uint32_t* __restrict__ kgid) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n && flag[g]) {
+        const uint32_t d = pos[g];
+        k32[d] = (uint32_t)((key[g] - kmin) >> shift);
+        kgid[d] = (uint32_t)g;
+    }
+}
+
 __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
                                const uint64_t* __restrict__ key, int64_t n,
                                uint64_t* __restrict__ kkey, uint32_t* __restrict__ kgid) {
@@ -258,12 +271,6 @@ constexpr int kRetryFullSort = 100;
 #define RCGS_DEPTH_KEY_BITS 24
 #endif
 constexpr int kDepthKeyBits = RCGS_DEPTH_KEY_BITS;
-
-__global__ void key32_kernel(const uint64_t* __restrict__ key, int64_t k, uint64_t kmin, int shift,
-                             uint32_t* __restrict__ k32) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < k) k32[i] = (uint32_t)((key[i] - kmin) >> shift);
-}
 
 __global__ void key_rebase_kernel(uint64_t* __restrict__ key, int64_t k, uint64_t kmin) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -525,12 +532,24 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
     };
     for (int i = t; i < ntiles; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
     __syncthreads();
-    if (t == 0) {
-        uint32_t run = 0;
-        for (int b = 0; b < 256; ++b) {
-            const uint32_t c = hist[b];
-            hist[b] = run;
-            run += c;
+    if (t < 32) {  // exclusive scan of the 256 buckets by one warp (8 per lane)
+        uint32_t c[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = hist[8 * t + j];
+            sum += c[j];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (t >= o) incl += y;
+        }
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            hist[8 * t + j] = run;
+            run += c[j];
         }
     }
     __syncthreads();
@@ -542,6 +561,76 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
         const uint2 r = ranges[i];
         meta[slot] = make_uint4((uint32_t)i, r.x, r.y, 0u);
     }
+}
+
+// Per-block lists, one CTA (8 warps) per work position: block b's list is the
+// tile list's entries (in depth order) whose block mask has bit b, stored at
+// blist[8 range.x + b len] (the raster's per-block record slots use the same
+// bound), with its length at bcount[8 position + b].  The raster then walks only
+// the entries that reach its 8x4 block (on the tile list ~70% of the entries a
+// block stepped through were masked out).  Each round covers 256 list entries:
+// per warp and block a ballot count, a cross-warp prefix in shared memory, then
+// the stable write-out (one warp per tile had made the heaviest tiles' serial
+// chunk chains the kernel's duration: 111 us).
+__global__ void __launch_bounds__(256) block_lists_kernel(const uint4* __restrict__ meta, int npos,
+                                                          const uint32_t* __restrict__ pair_g,
+                                                          const uint32_t* __restrict__ pair_m, uint32_t idx_mask,
+                                                          uint32_t* __restrict__ blist, uint32_t* __restrict__ bcount,
+                                                          const RasterRec* __restrict__ rec, int tiles_x) {
+    __shared__ uint32_t s_cnt[8][8];  // [warp][block] counts of the round
+    __shared__ uint32_t s_run[8];     // per block: entries written in earlier rounds
+    const int w = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (w >= npos) return;
+    const uint4 tm = meta[w];
+    const uint32_t x0 = tm.y, x1 = tm.z, len = x1 - x0;
+    const uint32_t lt = (1u << lane) - 1u;
+    if (threadIdx.x < 8) s_run[threadIdx.x] = 0u;
+    __syncthreads();
+    for (uint32_t c0 = x0; c0 < x1; c0 += 256) {
+        const uint32_t j = c0 + 32 * warp + lane;
+        uint32_t val = 0, mk = 0;
+        if (j < x1) {
+            val = pair_g[j];
+            mk = pair_m ? pair_m[j] : (val >> kIdxBits);
+        }
+        const uint32_t g = val & idx_mask;
+#ifdef RCGS_CHECKED
+        if (j < x1) {  // a dropped (entry, block) must fail the exact per-block test too
+            const RasterRec cr = rec[g];
+            const int tx = (int)(tm.x % (uint32_t)tiles_x), ty = (int)(tm.x / (uint32_t)tiles_x);
+            for (int b = 0; b < 8; ++b) {
+                const float bx0 = (float)(tx * kTile + (b & 1) * 8), by0 = (float)(ty * kTile + (b >> 1) * 4);
+                RCGS_DCHECK(((mk >> b) & 1u) || !(touches_block(cr.a, bx0, by0) &&
+                                                 ellipse_touches_rect(cr.a, cr.b, cr.c, bx0, by0, bx0 + 7.f, by0 + 3.f)));
+            }
+        }
+#endif
+        uint32_t bal[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            bal[b] = __ballot_sync(0xffffffffu, j < x1 && ((mk >> b) & 1u));
+            if (lane == b) s_cnt[warp][b] = __popc(bal[b]);
+        }
+        __syncthreads();
+        uint32_t base = 0;  // lane b < 8: block b's first slot for this warp
+        if (lane < 8) {
+            base = s_run[lane];
+            for (int q = 0; q < warp; ++q) base += s_cnt[q][lane];
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint32_t bb = __shfl_sync(0xffffffffu, base, b);
+            if ((bal[b] >> lane) & 1u) blist[8 * (size_t)x0 + (size_t)b * len + bb + __popc(bal[b] & lt)] = g;
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            uint32_t add = 0;
+            for (int q = 0; q < 8; ++q) add += s_cnt[q][threadIdx.x];
+            s_run[threadIdx.x] += add;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 8) bcount[8 * w + threadIdx.x] = s_run[threadIdx.x];
 }
 
 // ---------------------------------------------------------------- colour (per step)
@@ -687,6 +776,8 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->ranges, s);
     dfree(v->tile_order, s);
     dfree(v->tile_meta, s);
+    dfree(v->blist, s);
+    dfree(v->bcount, s);
     dfree(v->work, s);
     release_records(v, s);  // arena ownership, or the view-owned compact copy
     v->wrec_n = v->wrec_s = nullptr;
@@ -771,29 +862,27 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
         dfree(count_g, s);
         return RCGS_OK;
     }
-    RCGS_TRY(dalloc(&kkey, k, s));
-    RCGS_TRY(dalloc(&kkey_alt, k, s));
-    RCGS_TRY(dalloc(&kgid, k, s));
-    RCGS_TRY(dalloc(&kgid_alt, k, s));
-    compact_kernel<<<div_up(n, 256), 256, 0, s>>>(flag, kpos, key, n, kkey, kgid);
-    RCGS_LAUNCH_CHECK();
-    dfree(flag, s);
-    dfree(kpos, s);
     // ---- stable depth sort over the varying key bits
     // keys relative to the smallest kept key (order preserving): the exponent
     // carry between e.g. [1, 2) and [2, 4) no longer widens the sorted range
     const uint64_t span = kmax - kmin;
     v->sort_bits = span ? 64 - __builtin_clzll(span) : 0;
-    if (v->sort_bits > 0) {
-        if (v->sort_bits <= kDepthKeyBits || !v->full_sort) {
-            // 4-byte keys holding the top kDepthKeyBits varying bits (3 radix passes;
-            // exact when the span has no more bits), then the tie-run repair of runs
-            // with equal truncated keys and the order check
-            const int shift = v->sort_bits > kDepthKeyBits ? v->sort_bits - kDepthKeyBits : 0;
-            uint32_t *k32 = nullptr, *k32_alt = nullptr;
-            RCGS_TRY(dalloc(&k32, k, s));
-            RCGS_TRY(dalloc(&k32_alt, k, s));
-            key32_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin, shift, k32);
+    const bool k32_path = v->sort_bits <= kDepthKeyBits || !v->full_sort;
+    RCGS_TRY(dalloc(&kgid, k, s));
+    RCGS_TRY(dalloc(&kgid_alt, k, s));
+    if (k32_path) {
+        // 4-byte keys holding the top kDepthKeyBits varying bits (3 radix passes;
+        // exact when the span has no more bits), written by the compaction, then the
+        // tie-run repair of runs with equal truncated keys and the order check
+        const int shift = v->sort_bits > kDepthKeyBits ? v->sort_bits - kDepthKeyBits : 0;
+        uint32_t *k32 = nullptr, *k32_alt = nullptr;
+        RCGS_TRY(dalloc(&k32, k, s));
+        RCGS_TRY(dalloc(&k32_alt, k, s));
+        compact_k32_kernel<<<div_up(n, 256), 256, 0, s>>>(flag, kpos, key, n, kmin, shift, k32, kgid);
+        RCGS_LAUNCH_CHECK();
+        dfree(flag, s);
+        dfree(kpos, s);
+        if (v->sort_bits > 0) {
             RCGS_TRY(radix_sort_u32(&k32, &k32_alt, &kgid, &kgid_alt, false, k,
                                     v->sort_bits < kDepthKeyBits ? v->sort_bits : kDepthKeyBits, s));
             if (shift > 0) {
@@ -806,12 +895,18 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
                 dfree(long_runs, s);
             }
             RCGS_LAUNCH_CHECK();
-            dfree(k32, s);
-            dfree(k32_alt, s);
-        } else {
-            key_rebase_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin);
-            RCGS_TRY(radix_sort_u64(&kkey, &kkey_alt, &kgid, &kgid_alt, false, k, v->sort_bits, s));
         }
+        dfree(k32, s);
+        dfree(k32_alt, s);
+    } else {
+        RCGS_TRY(dalloc(&kkey, k, s));
+        RCGS_TRY(dalloc(&kkey_alt, k, s));
+        compact_kernel<<<div_up(n, 256), 256, 0, s>>>(flag, kpos, key, n, kkey, kgid);
+        RCGS_LAUNCH_CHECK();
+        dfree(flag, s);
+        dfree(kpos, s);
+        key_rebase_kernel<<<div_up(k, 256), 256, 0, s>>>(kkey, k, kmin);
+        RCGS_TRY(radix_sort_u64(&kkey, &kkey_alt, &kgid, &kgid_alt, false, k, v->sort_bits, s));
     }
     dfree(key, s);
     dfree(kkey, s);
@@ -865,6 +960,12 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     RCGS_TRY(dalloc(&v->tile_order, ntiles, s));
     RCGS_TRY(dalloc(&v->tile_meta, ntiles, s));
     tile_order_kernel<<<1, 1024, 0, s>>>(v->ranges, (int)ntiles, v->tile_order, v->tile_meta);
+    RCGS_LAUNCH_CHECK();
+    RCGS_TRY(dalloc(&v->blist, 8 * pairs, s));
+    RCGS_TRY(dalloc(&v->bcount, 8 * (int64_t)ntiles, s));
+    block_lists_kernel<<<ntiles, 256, 0, s>>>(
+        v->tile_meta, (int)ntiles, v->pair_g, v->pair_packed ? nullptr : v->pair_m, v->pair_packed ? kIdxMask : 0xffffffffu,
+        v->blist, v->bcount, v->rec, v->tiles_x);
     RCGS_LAUNCH_CHECK();
     dfree(g_alt, s);
     dfree(tkey, s);

@@ -116,6 +116,8 @@ struct RasterArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // work order (nullptr: row-major)
     const uint4* tile_meta;      // per work-order position {tile, range} (nullptr: tile_order + ranges)
+    const uint32_t* blist;       // per-block lists (block b of the tile at 8 range.x + b len), or null
+    const uint32_t* bcount;      // their lengths, by work item (= 8 work position + block)
     const uint32_t* pair_g;  // tile lists: scene indices in depth order
     const uint32_t* pair_m;  // per list entry: 8x4 blocks of its tile the footprint reaches
                              // (null: packed above the scene index in pair_g)
@@ -271,41 +273,6 @@ __device__ __forceinline__ double warp_exact_T(const uint32_t* __restrict__ pair
         }
     }
     return T;
-}
-
-// Does the cull record's footprint box touch the 8x4 block at (bx0, by0)?
-__device__ __forceinline__ bool touches_block(const float4 ra, float bx0, float by0) {
-    const unsigned packed = __float_as_uint(ra.z);
-    const float ex = __half2float(__ushort_as_half((unsigned short)(packed & 0xffffu)));
-    const float ey = __half2float(__ushort_as_half((unsigned short)(packed >> 16)));
-    return ra.x + ex >= bx0 && ra.x - ex <= bx0 + 7.f && ra.y + ey >= by0 && ra.y - ey <= by0 + 3.f;
-}
-
-// Can the footprint {power2 >= p_lo} reach any point of the rectangle
-// [x0, x1] x [y0, y1]?  Q = -power2 is a PSD quadratic of the offset from the
-// mean; its minimum over the box is 0 when the mean is inside, else it lies on
-// an edge, where the 1-D minimiser is a clamp.  The candidates' fp32 values are
-// lowered by their evaluation error bound (2e-6 of the absolute term sum, plus
-// 1.5e-4 = 1e-4 natural-log units), so the test only drops entries whose power
-// stays below the gate at every pixel of the rectangle -- alpha exactly 0 in
-// fp64 there -- and the results do not change.  NaN keeps the entry.
-__device__ __forceinline__ bool ellipse_touches_rect(const float4 ra, const float4 rb, const float4 rc, float x0,
-                                                     float y0, float x1, float y1) {
-    const float X0 = (x0 - ra.x) - rb.x, X1 = (x1 - ra.x) - rb.x;
-    const float Y0 = (y0 - ra.y) - rb.y, Y1 = (y1 - ra.y) - rb.y;
-    if (X0 <= 0.f && X1 >= 0.f && Y0 <= 0.f && Y1 >= 0.f) return true;
-    const float A = -rc.x, B = -rc.y, C = -rc.z;
-    const float hA = __fdividef(-0.5f * B, A), hC = __fdividef(-0.5f * B, C);
-    auto lower = [&](float dx, float dy) {  // lower bound of Q(dx, dy)
-        const float xx = A * dx * dx, yy = C * dy * dy, xy = B * dx * dy;
-        return (xx + yy + xy) - fmaf(2e-6f, xx + yy + fabsf(xy), 1.5e-4f);
-    };
-    auto clampf = [](float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); };
-    float m = lower(X0, clampf(hC * X0, Y0, Y1));
-    m = fminf(m, lower(X1, clampf(hC * X1, Y0, Y1)));
-    m = fminf(m, lower(clampf(hA * Y0, X0, X1), Y0));
-    m = fminf(m, lower(clampf(hA * Y1, X0, X1), Y1));
-    return !(m > -rb.z);
 }
 
 // One staged (entry, 8x4 block) pair.  The entry's log2 alpha over the block is
@@ -569,21 +536,30 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
         // FWDREC: nrec records so far; wp = this lane's weight slot of record nrec
         uint32_t nrec = 0;
         float* wp = M == FWDREC ? a.wrec_w + (size_t)rbase * 32 + lane : nullptr;
+        // The list this block walks: its own per-block list (view build: the tile-list
+        // entries whose block mask has this block's bit, in order), or the tile list
+        // with the mask tested per entry.  Entries left out reach no pixel of the block
+        // with alpha >= 1/255, i.e. multiply T by exactly 1 there.
+        const bool blists = a.blist != nullptr;
+        const uint32_t lo = blists ? 0u : range.x;
+        const uint32_t hi = blists ? a.bcount[item] : range.y;
+        const uint32_t* const list = blists ? a.blist + rbase : a.pair_g;
         // chunk pipeline: pair ids two chunks ahead, raw records one chunk ahead (each
         // lane copies and later reads only its own slots)
         const bool packed = a.pair_m == nullptr;
         const int mshift = packed ? kIdxBits + blk : blk;
         auto issue_pg = [&](uint32_t cn, int buf) {
-            if (cn + lane < range.y) {
-                cp_async4(&st.pg[buf][lane], a.pair_g + cn + lane);
-                if (!packed) cp_async4(&st.pm[buf][lane], a.pair_m + cn + lane);
+            if (cn + lane < hi) {
+                cp_async4(&st.pg[buf][lane], list + cn + lane);
+                if (!packed && !blists) cp_async4(&st.pm[buf][lane], a.pair_m + cn + lane);
             }
             cp_async_commit();
         };
         auto mask_word = [&](int buf) { return packed ? st.pg[buf][lane] : st.pm[buf][lane]; };
+        auto in_block = [&](int buf) { return blists || ((mask_word(buf) >> mshift) & 1u); };
         // raw records only for the entries whose footprint reaches this block
         auto issue_raw = [&](uint32_t cn, int buf) {
-            if (cn + lane < range.y && ((mask_word(buf) >> mshift) & 1u)) {
+            if (cn + lane < hi && in_block(buf)) {
                 const uint32_t sn = st.pg[buf][lane] & a.idx_mask;
                 cp_async16(&st.ra[lane], &a.rec[sn].a);
                 cp_async16(&st.rb[lane], &a.rec[sn].b);
@@ -592,27 +568,27 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
             }
             cp_async_commit();
         };
-        if (range.x < range.y) {
-            issue_pg(range.x, 0);
-            issue_pg(range.x + 32, 1);
+        if (lo < hi) {
+            issue_pg(lo, 0);
+            issue_pg(lo + 32, 1);
             cp_async_wait<1>();
-            issue_raw(range.x, 0);
+            issue_raw(lo, 0);
         }
         int buf = 0;
-        for (uint32_t c0 = range.x; c0 < range.y; c0 += 32, buf ^= 1) {
+        for (uint32_t c0 = lo; c0 < hi; c0 += 32, buf ^= 1) {
             if (__all_sync(0xffffffffu, !(T > 0.f))) break;
             cp_async_wait<0>();  // this chunk's records (and the next chunk's ids)
             const uint32_t j = c0 + lane;
             bool keep = false;
             uint32_t s = 0;
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra, rcol = ra;
-            if (j < range.y) {
+            if (j < hi) {
                 s = st.pg[buf][lane] & a.idx_mask;
-                RCGS_DCHECK(j < (uint64_t)a.pairs && s < (uint64_t)a.n);
+                RCGS_DCHECK(s < (uint64_t)a.n);
                 // the pair's block mask (view build) is the per-block cull
-                keep = (mask_word(buf) >> mshift) & 1u;
+                keep = in_block(buf);
 #ifdef RCGS_CHECKED
-                {  // a dropped (entry, block) must fail the exact per-block test too
+                if (!blists) {  // a dropped (entry, block) must fail the exact per-block test too
                     const RasterRec cr = a.rec[s];
                     RCGS_DCHECK(keep || !(touches_block(cr.a, fbx0, fby0) &&
                                           ellipse_touches_rect(cr.a, cr.b, cr.c, fbx0, fby0, fbx0 + 7.f,
@@ -627,9 +603,9 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 }
             }
             // the slots are consumed: start the next chunk's records and the ids after
-            if (c0 + 32 < range.y) {
+            if (c0 + 32 < hi) {
                 issue_raw(c0 + 32, buf ^ 1);
-                if (c0 + 64 < range.y) issue_pg(c0 + 64, buf);
+                if (c0 + 64 < hi) issue_pg(c0 + 64, buf);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
@@ -686,8 +662,8 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
                 StepOut o = composite_step<M>(T, A, live, pass, al, q2.w, a.f_floor, a.f_tau);
                 if (__any_sync(0xffffffffu, gamb || o.amb)) {
                     const SlowOut so =
-                        slow_entry<M>(a.pair_g, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, a.t_floor, a.tau, a.f_floor,
-                                      a.f_tau, st.g[k], st.j[k], range.x, cxf + lxf, cyf + lyf, lane, T, A, live, pass,
+                        slow_entry<M>(list, a.rec, a.exact, a.alpha_clamp, a.alpha_skip, a.t_floor, a.tau, a.f_floor,
+                                      a.f_tau, st.g[k], st.j[k], lo, cxf + lxf, cyf + lyf, lane, T, A, live, pass,
                                       gamb, al, q2.w, o, a.idx_mask);
                     o = so.o;
                     n_resync += so.resync;
@@ -1249,6 +1225,8 @@ static RasterArgs base_args(const rcgs_view* v) {
     a.tile_meta = v->tile_meta;
     a.pair_g = v->pair_g;
     a.pair_m = v->pair_packed ? nullptr : v->pair_m;
+    a.blist = v->blist;
+    a.bcount = v->bcount;
     a.idx_mask = v->pair_packed ? kIdxMask : 0xffffffffu;
     a.rank_of = v->rank_of;
     a.counter = v->work;
