@@ -62,8 +62,12 @@ class ViewPrefetcher:
     `workers` threads (RCGS_PREFETCH_WORKERS, default 2) take jobs in turn, each
     on its own stream: a build's wall time (its two host syncs, and kernels that
     only run between the main stream's CTAs) is about one step, so one worker
-    cannot stay ahead; two interleave.  The streams get the highest priority, so
-    the block scheduler starts build CTAs as soon as main-stream CTAs retire.
+    cannot stay ahead; two interleave.  The streams run at the main stream's
+    (normal) priority: at the highest priority (the round-1 choice) the queued build
+    kernels took every SM the recording raster released and the loss waited ~58 us
+    per step behind them (`tools/stream_gaps.py`); at equal priority the main
+    stream's kernels start first and the builds fill in (1084.5 vs 1072.9
+    view-steps/s).  RCGS_PREFETCH_PRIORITY overrides.
 
     Used views come back through `retire`: the worker that built a view frees it
     on ITS stream after an event recorded on the consumer's stream.  Allocation
@@ -91,7 +95,7 @@ class ViewPrefetcher:
             workers = int(os.environ.get("RCGS_PREFETCH_WORKERS", "2"))
         workers = max(1, int(workers))
         prio = os.environ.get("RCGS_PREFETCH_PRIORITY")
-        prio = int(prio) if prio is not None else torch.cuda.Stream.priority_range()[1]
+        prio = int(prio) if prio is not None else 0
         self.streams = [torch.cuda.Stream(device=device, priority=prio) for _ in range(workers)]
         # per-worker copy streams: with one, the ~25 MB target uploads (one per step,
         # ~21 GB/s from pinned host memory) were serialised at about the step rate
