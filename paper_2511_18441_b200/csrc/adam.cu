@@ -45,20 +45,6 @@ __device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const flo
     }
 }
 
-// The fp64 colour (color_kernel's fallback) of the gaussians the Adam colour
-// epilogue queued in fix = {count, g...}; one CTA, which re-arms the count.
-__global__ void __launch_bounds__(256) color_fixup_kernel(uint32_t* __restrict__ fix, const double* __restrict__ pos,
-                                                          const float4* __restrict__ sh, Center cen, int deg,
-                                                          float4* __restrict__ color) {
-    const uint32_t cnt = fix[0];
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const int64_t g = fix[1 + i];
-        color[g] = color_f64(pos, sh, g, cen, deg);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) fix[0] = 0u;
-}
-
 // Bias corrections 1/(1 - beta^t) for t = step + 1, once per launch (fp64 pow).
 __global__ void adam_prep_kernel(const int64_t* __restrict__ step, double db1, double db2,
                                  float2* __restrict__ inv) {
@@ -123,10 +109,11 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t byt
 // The last block to finish (every block has read *step and *reject by then)
 // commits the step: advances the counter unless rejected, records the outcome and
 // re-arms the flag.  One thread per block.
-__device__ __forceinline__ void commit_step(unsigned* ticket, bool upd, int64_t* step, int32_t* reject,
+__device__ __forceinline__ bool commit_step(unsigned* ticket, bool upd, int64_t* step, int32_t* reject,
                                             double* reject_record, int64_t* snapshot_step, int64_t new_step) {
     __threadfence();
-    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+    const bool last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (last) {
         if (upd) *step += 1;
         if (snapshot_step) *snapshot_step = new_step;
         *ticket = 0;
@@ -135,6 +122,7 @@ __device__ __forceinline__ void commit_step(unsigned* ticket, bool upd, int64_t*
             if (reject) *reject = 0;
         }
     }
+    return last;
 }
 
 #ifndef RCGS_ADAM_TILE
@@ -175,7 +163,7 @@ __host__ __device__ constexpr size_t adam_smem_bytes(int n_views) {
 // the stage before it is refilled.  Element order, products and Adam formulas
 // are the per-element ones of adam4, so results are bit-identical to an
 // elementwise update.
-__global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
+__global__ void __launch_bounds__(kAThreads, 3) adam_fused_kernel(
     const double* __restrict__ pos, int64_t n, int deg, float* __restrict__ sh, float* __restrict__ m,
     float* __restrict__ v, AccViews views, AdamHyper h, int64_t* __restrict__ step, double db1, double db2,
     unsigned* __restrict__ ticket, int32_t* __restrict__ reject, const int32_t* __restrict__ next_rank_of,
@@ -385,9 +373,10 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
                 col[ch] = fmaxf(0.f, v);
             }
             amb = amb && rs >= 0 && part == 0;
-            // rare (never at C3): the gaussian is queued for the fp64 colour, which
-            // color_fixup_kernel writes after this launch (an inline fp64 fallback
-            // cost the common path ~40% of the kernel through its registers alone)
+            // rare (never at C3): the gaussian is queued for the fp64 colour, which the
+            // last block writes once every block has finished (an inline fp64
+            // fallback cost the common path ~40% of the kernel through its registers
+            // alone; a separate fixup launch cost a kernel boundary per step)
             if (amb) {
                 const uint32_t slot = atomicAdd(next_fix, 1u);
                 next_fix[1 + slot] = (uint32_t)g;
@@ -396,9 +385,25 @@ __global__ void __launch_bounds__(kAThreads) adam_fused_kernel(
                 next_color[g] = make_float4(col[0], col[1], col[2], __int_as_float(act));
         }
     }
+    // this block's queue entries and colour stores are visible before its ticket
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned s_last;
     if (t == 0) {
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        commit_step(ticket, upd, step, reject, reject_record, snap ? snapshot_step : nullptr, *step + 1);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");     // SH stores complete
+        asm volatile("fence.proxy.async.global;" ::: "memory");         // ... and ordered before the ticket
+        s_last = commit_step(ticket, upd, step, reject, reject_record, snap ? snapshot_step : nullptr, *step + 1);
+    }
+    __syncthreads();
+    if (s_last && next_fix != nullptr) {  // the fp64 colours queued by the epilogue (color_f64)
+        __threadfence();
+        const uint32_t cnt = __ldcg(next_fix);
+        for (uint32_t i = t; i < cnt; i += blockDim.x) {
+            const int64_t g = __ldcg(next_fix + 1 + i);
+            next_color[g] = color_f64(pos, reinterpret_cast<const float4*>(sh), g, next_cen, deg);
+        }
+        __syncthreads();
+        if (t == 0) *next_fix = 0u;
     }
 }
 
@@ -551,11 +556,7 @@ static int adam_fused_impl(const rcgs_scene* sc, float* d_sh, float* d_m, float*
             d_reject, nrank, nc, ncolor, nfix, d_reject_record, pub ? pub->d_snapshot : nullptr,
             pub ? pub->d_snapshot_step : nullptr, pub ? pub->every : 0, d_tile_state);
         RCGS_LAUNCH_CHECK();
-        if (ncolor != nullptr) {
-            color_fixup_kernel<<<1, 256, 0, s>>>(nfix, sc->pos, reinterpret_cast<const float4*>(d_sh), nc,
-                                                 sc->sh_degree, ncolor);
-            RCGS_LAUNCH_CHECK();
-        }
+
         return RCGS_OK;
     }
     step_commit_kernel<<<1, 1, 0, s>>>(d_reject, d_step, d_reject_record, pub ? pub->d_snapshot_step : nullptr,

@@ -181,23 +181,25 @@ __device__ __forceinline__ bool color_ambiguous(float v, float mag) {
 // fp64 colour of one gaussian (out of line: the rare fallback of color_kernel)
 static __device__ __noinline__ float4 color_f64(const double* __restrict__ pos, const float4* __restrict__ sh, int64_t g,
                                          Center cen, int deg) {
-    float c[48];
-    const float4* row = sh + g * 12;
-#pragma unroll
-    for (int i = 0; i < 12; ++i) {
-        const float4 f = row[i];
-        c[4 * i] = f.x;
-        c[4 * i + 1] = f.y;
-        c[4 * i + 2] = f.z;
-        c[4 * i + 3] = f.w;
-    }
     double x, y, z;
     view_dir(pos, g, cen.c, x, y, z);
     double b[16];
     sh_basis16<double>(x, y, z, deg, b);
+    const float4* row = sh + g * 12;
     double qv[4][3];
 #pragma unroll
-    for (int part = 0; part < 4; ++part) color_quarter(b, c + 12 * part, part, qv[part]);
+    for (int part = 0; part < 4; ++part) {  // 12 coefficients at a time (registers)
+        float c12[12];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const float4 f = __ldcg(row + 3 * part + i);
+            c12[4 * i] = f.x;
+            c12[4 * i + 1] = f.y;
+            c12[4 * i + 2] = f.z;
+            c12[4 * i + 3] = f.w;
+        }
+        color_quarter(b, c12, part, qv[part]);
+    }
     int act = 0;
     float col[3];
 #pragma unroll
