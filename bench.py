@@ -766,7 +766,7 @@ def run_e2e(args, scene, cams, sp, group, world):
             done.set()
 
     opt = P.BackgroundOptimizer(scene, ds, cfg, seed=7, metrics_sink=sink, group=group, cache_views=False,
-                                stream_targets=True, prefetch=2)
+                                stream_targets=True, prefetch=3)
     torch.cuda.synchronize()
     if world == 1:
         opt.start()
@@ -942,7 +942,7 @@ def main():
     ap.add_argument("--no-clocks", dest="clocks", action="store_false", help="skip NVML clock sampling")
     ap.add_argument("--no-extras", dest="extras", action="store_false",
                     help="skip config 4 (3M selection sweep) and config 5 (interactive latency)")
-    ap.add_argument("--prefetch", type=int, default=2, help="views built ahead on a side stream (0 = inline)")
+    ap.add_argument("--prefetch", type=int, default=3, help="views built ahead on side streams (0 = inline)")
     ap.add_argument("--call-profile", action="store_true",
                     help="diagnostics: host time of every C-ABI call in the timed loop (stderr)")
     ap.add_argument("--no-profile", dest="profile", action="store_false",
