@@ -856,8 +856,29 @@ __device__ __forceinline__ RecMeta rec_meta(const RecArgs& a, unsigned item, int
 // totals equal the traversal backward's bit for bit (and, with finite g, w = 0
 // gives an exact 0 product, as skipping the pixel does).  The sums of channels
 // 0 / 1 go through packed FADD2.
-__device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m, float (*sw)[8][36],
-                                              uint32_t (*ss)[8], int lane) {
+// Copy of one 8-record batch of a block into the warp's shared rows `buf` (one
+// commit group, empty past the block's end): lane (q, h) copies 32 bytes of record
+// q, quarter h.
+__device__ __forceinline__ void rec_bwd_issue(const RecArgs& a, const RecMeta& m, uint32_t r0, float (*sw)[8][36],
+                                              uint32_t (*ss)[8], int buf, int lane) {
+    const int q = lane >> 2, h = lane & 3;
+    const uint32_t r = r0 + (uint32_t)q;
+    if (r < m.n) {
+        const float* src = a.wrec_w + (size_t)(m.base + r) * 32 + 8 * h;
+        cp_async16(&sw[buf][q][8 * h], src);
+        cp_async16(&sw[buf][q][8 * h + 4], src + 4);
+    }
+    if (lane < 8 && r0 + lane < m.n) cp_async4(&ss[buf][lane], a.wrec_s + m.base + r0 + lane);
+    cp_async_commit();
+}
+
+// Batch 0 of this block is already in flight in `buf` (issued while the previous
+// block's last batch was summed); while this block's last batch is summed, the
+// next block's batch 0 goes out (when `nm_pre`), so a warp's record stream does
+// not restart at every block (the per-block restart had been ~30% of the stall
+// samples).  On return `buf` is the buffer holding the next block's batch 0.
+__device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m, bool nm_pre, const RecMeta& nm,
+                                              float (*sw)[8][36], uint32_t (*ss)[8], int& buf, int lane) {
     const int q = lane >> 2, h = lane & 3;
     float2 g01[8];
     float g2[8];
@@ -867,26 +888,15 @@ __device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m
         g01[j] = make_float2(__shfl_sync(0xffffffffu, m.g0, src), __shfl_sync(0xffffffffu, m.g1, src));
         g2[j] = __shfl_sync(0xffffffffu, m.g2, src);
     }
-    // lane copies 32 bytes of one record of the batch: record lane / 4, quarter lane % 4
-    auto issue = [&](uint32_t r0, int buf) {
-        const uint32_t r = r0 + (uint32_t)q;
-        if (r < m.n) {
-            const float* src = a.wrec_w + (size_t)(m.base + r) * 32 + 8 * h;
-            cp_async16(&sw[buf][q][8 * h], src);
-            cp_async16(&sw[buf][q][8 * h + 4], src + 4);
-        }
-        if (lane < 8 && r0 + lane < m.n) cp_async4(&ss[buf][lane], a.wrec_s + m.base + r0 + lane);
-        cp_async_commit();
-    };
-    issue(0, 0);
-    int buf = 0;
     for (uint32_t r0 = 0; r0 < m.n; r0 += 8, buf ^= 1) {
         if (r0 + 8 < m.n) {
-            issue(r0 + 8, buf ^ 1);
-            cp_async_wait<1>();
+            rec_bwd_issue(a, m, r0 + 8, sw, ss, buf ^ 1, lane);
+        } else if (nm_pre) {
+            rec_bwd_issue(a, nm, 0, sw, ss, buf ^ 1, lane);
         } else {
-            cp_async_wait<0>();
+            cp_async_commit();  // keeps one group per batch
         }
+        cp_async_wait<1>();
         __syncwarp();
         const bool live = r0 + q < m.n;
         float2 p01[8];
@@ -945,6 +955,15 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
     if (item >= (unsigned)a.n_items) return;
     RecMeta m = rec_meta(a, item, tile_of(item), lane);
     int ntile = item + nw < (unsigned)a.n_items ? tile_of(item + nw) : 0;
+    // a block takes the streamed (fast) path when it has records, a nonzero gradient
+    // somewhere and only finite gradients; its batch 0 is then issued ahead
+    auto fast = [&](const RecMeta& mm) {
+        return mm.n > 0 && !__all_sync(0xffffffffu, mm.g0 == 0.f && mm.g1 == 0.f && mm.g2 == 0.f) &&
+               __all_sync(0xffffffffu, isfinite(mm.g0) && isfinite(mm.g1) && isfinite(mm.g2));
+    };
+    int buf = 0;
+    bool pre = fast(m);
+    if (pre) rec_bwd_issue(a, m, 0, sw, ss, buf, lane);
     while (true) {
         const unsigned nitem = item + nw;
         const bool has_next = nitem < (unsigned)a.n_items;
@@ -955,8 +974,15 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
         // the gradient is local to the edited region: blocks whose gradients are all
         // 0 have no term
         if (m.n > 0 && !__all_sync(0xffffffffu, m.g0 == 0.f && m.g1 == 0.f && m.g2 == 0.f)) {
-            if (__all_sync(0xffffffffu, isfinite(m.g0) && isfinite(m.g1) && isfinite(m.g2))) {
-                rec_bwd_block(a, m, sw, ss, lane);
+            if (pre) {
+                const bool npre = has_next && fast(nm);
+                rec_bwd_block(a, m, npre, nm, sw, ss, buf, lane);
+                pre = npre;
+                m = nm;
+                if (!has_next) break;
+                item = nitem;
+                ntile = nntile;
+                continue;
             } else {
             // non-finite pixel gradients: a pixel that no record composites (w = 0)
             // must contribute nothing, not 0 * inf
@@ -1013,11 +1039,17 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
             }
             }
         }
+        // (this block took no streamed path) issue the next block's batch 0
+        cp_async_wait<0>();
+        __syncwarp();
+        pre = has_next && fast(nm);
+        if (pre) rec_bwd_issue(a, nm, 0, sw, ss, buf, lane);
         if (!has_next) break;
         item = nitem;
         m = nm;
         ntile = nntile;
     }
+    cp_async_wait<0>();
 }
 
 // kMode: 0 SpMV render into an image, 1 backward, 2 SpMV render into an RGBA8 frame
