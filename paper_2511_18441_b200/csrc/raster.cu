@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kRCTA, (M == FWDREC ? RCGS_FWDREC_MIN_CTAS : k
     // was ~7% of the warp samples).  At the 64-register budget of the other modes
     // the extra live value made ptxas rematerialise lane constants inside the
     // entry loop (+24%), so they fetch on demand.
-    constexpr bool kAhead = M == FWDREC;
+    constexpr bool kAhead = M == FWDREC && RCGS_FWDREC_MIN_CTAS <= 3;
     unsigned nraw = 0;
     if (kAhead && lane == 0) nraw = atomicAdd(a.counter, 1u);
     for (;;) {
