@@ -32,6 +32,8 @@ constexpr int kR = 5;              // window half width
 constexpr int kWin = 2 * kR + 1;   // 11
 constexpr int kLT = 32;            // output tile edge
 constexpr int kLH = kLT + 2 * kR;  // 42
+constexpr int kMS = 48;            // pass B: map plane row stride (columns x0 - 8 .. x0 + 39)
+constexpr int kMO = 8 - kR;        // pass B: the halo's first column (x0 - 5) within a row
 constexpr int kRows = 4;           // output rows per thread in the vertical pass
 constexpr int kLNT = 256;          // = kLT * kLT / kRows
 #ifndef RCGS_LOSS_HS
@@ -187,6 +189,12 @@ __device__ __forceinline__ void cp_async_elem(E* dst, const E* src, bool in) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(sizeof(E)),
                  "r"(in ? (int)sizeof(E) : 0)
                  : "memory");
+}
+
+// 16-byte asynchronous copy; `in` false zero-fills
+__device__ __forceinline__ void cp_async16_z(void* dst, const void* src, bool in) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(in ? 16 : 0) : "memory");
 }
 
 // ---------------------------------------------------------------- pass A
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                                                     const uint8_t* __restrict__ dirty, G* __restrict__ grad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MT* hs = reinterpret_cast<MT*>(smem_raw);            // [3][42][32]
-    MT* imb = hs + 3 * kLH * kLT;                        // [2][3][42][42]: double-buffered map planes
+    MT* imb = hs + 3 * kLH * kLT;                        // [2][3][42][kMS]: double-buffered map planes
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
     const int64_t npix = (int64_t)H * W;
@@ -378,22 +386,39 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
     const int c = t % kLT, r0 = (t / kLT) * kRows;
     // the next channel's three map planes (with the 5-px halo, zero outside the
     // image) stream into the other buffer while this channel computes
+    // Map planes are staged as rows of kMS columns, the halo's first column at kMO:
+    // interior tiles of fp32 maps (row starts 16-byte aligned) copy 16-byte chunks
+    // of columns x0 - 8 .. x0 + 39 (a third of the copy instructions of element
+    // copies), edge tiles copy element by element.
     auto issue = [&](int ch) {
-        MT* buf = imb + (ch & 1) * 3 * kLH * kLH;
+        MT* buf = imb + (ch & 1) * 3 * kLH * kMS;
         const MT* m0 = maps + (int64_t)ch * npix;
         const uint32_t mstride = (uint32_t)(npix * 3);
-        int r = t / kLH, cc = t - (t / kLH) * kLH;  // advanced incrementally, as in pass A
-        for (int i = t; i < kLH * kLH; i += kLNT) {
-            const int gy = y0 - kR + r, gx = x0 - kR + cc;
-            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const uint32_t gi = in ? (uint32_t)gy * (uint32_t)W + (uint32_t)gx : 0u;
+        const bool vec = sizeof(MT) == 4 && (W & 3) == 0 && x0 >= 8 && x0 + 40 <= W;
+        if (vec) {
+            for (int i = t; i < kLH * 12; i += kLNT) {
+                const int r = i / 12, c4 = i - (i / 12) * 12;
+                const int gy = y0 - kR + r;
+                const bool in = gy >= 0 && gy < H;
+                const uint32_t gi = in ? (uint32_t)gy * (uint32_t)W + (uint32_t)(x0 - 8 + 4 * c4) : 0u;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) cp_async_elem(buf + q * kLH * kLH + i, m0 + q * mstride + gi, in);
-            cc += kLNT % kLH;
-            r += kLNT / kLH;
-            if (cc >= kLH) {
-                cc -= kLH;
-                ++r;
+                for (int q = 0; q < 3; ++q) cp_async16_z(buf + q * kLH * kMS + r * kMS + 4 * c4, m0 + q * mstride + gi, in);
+            }
+        } else {
+            int r = t / kLH, cc = t - (t / kLH) * kLH;  // advanced incrementally, as in pass A
+            for (int i = t; i < kLH * kLH; i += kLNT) {
+                const int gy = y0 - kR + r, gx = x0 - kR + cc;
+                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+                const uint32_t gi = in ? (uint32_t)gy * (uint32_t)W + (uint32_t)gx : 0u;
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    cp_async_elem(buf + q * kLH * kMS + r * kMS + kMO + cc, m0 + q * mstride + gi, in);
+                cc += kLNT % kLH;
+                r += kLNT / kLH;
+                if (cc >= kLH) {
+                    cc -= kLH;
+                    ++r;
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -419,14 +444,14 @@ __global__ void __launch_bounds__(kLNT, kLossCTAs) loss_pass_b(const T* __restri
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
             __syncthreads();
-            const MT* im = imb + (ch & 1) * 3 * kLH * kLH;
+            const MT* im = imb + (ch & 1) * 3 * kLH * kMS;
             // horizontal pass in kHS-output strips from register-resident segments
             constexpr int kHI = kLH * (kLT / kHS);
             for (int i = t; i < 3 * kHI; i += kLNT) {  // items (map, row, strip): even spread
                 const int q = i / kHI, ii = i - q * kHI;
                 const int r = ii / (kLT / kHS), c0 = (ii % (kLT / kHS)) * kHS;
                 {
-                    const MT* src = im + q * kLH * kLH + r * kLH + c0;
+                    const MT* src = im + q * kLH * kMS + r * kMS + kMO + c0;
                     MT x[kHS + kWin - 1];
 #pragma unroll
                     for (int j = 0; j < kHS + kWin - 1; ++j) x[j] = src[j];
@@ -532,7 +557,7 @@ static int loss_grad_impl(const T* d_image, const T* d_target, int32_t height, i
     lt.out3 = d_loss3;
     loss_dirty_kernel<T><<<grid, kLNT, 0, s>>>(d_image, d_target, height, width, dirty);
     const size_t smem_a = 2 * kLH * kLH * sizeof(T) + 5 * kLH * kLT * sizeof(double);
-    const size_t smem_b = 2 * 3 * kLH * kLH * sizeof(MT) + 3 * kLH * kLT * sizeof(MT);
+    const size_t smem_b = 2 * 3 * kLH * kMS * sizeof(MT) + 3 * kLH * kLT * sizeof(MT);
     WindowT<MT> wm;
     for (int k = 0; k < kWin; ++k) wm.w[k] = (MT)win.w[k];
     if (ssim_ok) {
