@@ -859,16 +859,32 @@ __device__ __forceinline__ RecMeta rec_meta(const RecArgs& a, unsigned item, int
 // Copy of one 8-record batch of a block into the warp's shared rows `buf` (one
 // commit group, empty past the block's end): lane (q, h) copies 32 bytes of record
 // q, quarter h.
-__device__ __forceinline__ void rec_bwd_issue(const RecArgs& a, const RecMeta& m, uint32_t r0, float (*sw)[8][36],
-                                              uint32_t (*ss)[8], int buf, int lane) {
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4_s(uint32_t dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(gsrc) : "memory");
+}
+
+// Shared-memory byte addresses of a warp's record rows (2 buffers x 8 rows of 36
+// floats) and record ids (2 x 8), computed once per warp.
+struct RecSmem {
+    uint32_t w, s;
+};
+constexpr uint32_t kRecRowB = 36 * 4, kRecBufB = 8 * kRecRowB;
+
+__device__ __forceinline__ void rec_bwd_issue(const RecArgs& a, const RecMeta& m, uint32_t r0, RecSmem sm, int buf,
+                                              int lane) {
     const int q = lane >> 2, h = lane & 3;
     const uint32_t r = r0 + (uint32_t)q;
     if (r < m.n) {
         const float* src = a.wrec_w + (size_t)(m.base + r) * 32 + 8 * h;
-        cp_async16(&sw[buf][q][8 * h], src);
-        cp_async16(&sw[buf][q][8 * h + 4], src + 4);
+        const uint32_t dst = sm.w + (uint32_t)buf * kRecBufB + (uint32_t)q * kRecRowB + (uint32_t)h * 32u;
+        cp_async16_s(dst, src);
+        cp_async16_s(dst + 16, src + 4);
     }
-    if (lane < 8 && r0 + lane < m.n) cp_async4(&ss[buf][lane], a.wrec_s + m.base + r0 + lane);
+    if (lane < 8 && r0 + lane < m.n)
+        cp_async4_s(sm.s + (uint32_t)buf * 32u + (uint32_t)lane * 4u, a.wrec_s + m.base + r0 + lane);
     cp_async_commit();
 }
 
@@ -878,7 +894,7 @@ __device__ __forceinline__ void rec_bwd_issue(const RecArgs& a, const RecMeta& m
 // not restart at every block (the per-block restart had been ~30% of the stall
 // samples).  On return `buf` is the buffer holding the next block's batch 0.
 __device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m, bool nm_pre, const RecMeta& nm,
-                                              float (*sw)[8][36], uint32_t (*ss)[8], int& buf, int lane) {
+                                              float (*sw)[8][36], uint32_t (*ss)[8], RecSmem sm, int& buf, int lane) {
     const int q = lane >> 2, h = lane & 3;
     float2 g01[8];
     float g2[8];
@@ -890,9 +906,9 @@ __device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m
     }
     for (uint32_t r0 = 0; r0 < m.n; r0 += 8, buf ^= 1) {
         if (r0 + 8 < m.n) {
-            rec_bwd_issue(a, m, r0 + 8, sw, ss, buf ^ 1, lane);
+            rec_bwd_issue(a, m, r0 + 8, sm, buf ^ 1, lane);
         } else if (nm_pre) {
-            rec_bwd_issue(a, nm, 0, sw, ss, buf ^ 1, lane);
+            rec_bwd_issue(a, nm, 0, sm, buf ^ 1, lane);
         } else {
             cp_async_commit();  // keeps one group per batch
         }
@@ -925,7 +941,9 @@ __device__ __forceinline__ void rec_bwd_block(const RecArgs& a, const RecMeta& m
         c01.x += __shfl_xor_sync(0xffffffffu, c01.x, 1);
         c01.y += __shfl_xor_sync(0xffffffffu, c01.y, 1);
         c2 += __shfl_xor_sync(0xffffffffu, c2, 1);
-        const float val = h == 0 ? c01.x : (h == 1 ? c01.y : c2);
+        float val = c2;  // selects, not branches
+        val = h == 1 ? c01.y : val;
+        val = h == 0 ? c01.x : val;
         if (h < 3 && live && val != 0.f) {
             const uint32_t sq = ss[buf][q];
             RCGS_DCHECK(sq < (uint32_t)a.n);
@@ -945,6 +963,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
     __shared__ uint32_t s_s[kCTA / 32][2][8];
     float(*sw)[8][36] = s_w[threadIdx.x >> 5];
     uint32_t(*ss)[8] = s_s[threadIdx.x >> 5];
+    const RecSmem sm = {(uint32_t)__cvta_generic_to_shared(&sw[0][0][0]), (uint32_t)__cvta_generic_to_shared(&ss[0][0])};
     constexpr int kU = 8;  // records per batch (the 32-value reduce-scatter width)
     const unsigned nw = gridDim.x * (blockDim.x >> 5);
     const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -963,7 +982,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
     };
     int buf = 0;
     bool pre = fast(m);
-    if (pre) rec_bwd_issue(a, m, 0, sw, ss, buf, lane);
+    if (pre) rec_bwd_issue(a, m, 0, sm, buf, lane);
     while (true) {
         const unsigned nitem = item + nw;
         const bool has_next = nitem < (unsigned)a.n_items;
@@ -976,7 +995,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
         if (m.n > 0 && !__all_sync(0xffffffffu, m.g0 == 0.f && m.g1 == 0.f && m.g2 == 0.f)) {
             if (pre) {
                 const bool npre = has_next && fast(nm);
-                rec_bwd_block(a, m, npre, nm, sw, ss, buf, lane);
+                rec_bwd_block(a, m, npre, nm, sw, ss, sm, buf, lane);
                 pre = npre;
                 m = nm;
                 if (!has_next) break;
@@ -1043,7 +1062,7 @@ __global__ void __launch_bounds__(kCTA, RCGS_REC_BWD_CTAS) rec_bwd_kernel(RecArg
         cp_async_wait<0>();
         __syncwarp();
         pre = has_next && fast(nm);
-        if (pre) rec_bwd_issue(a, nm, 0, sw, ss, buf, lane);
+        if (pre) rec_bwd_issue(a, nm, 0, sm, buf, lane);
         if (!has_next) break;
         item = nitem;
         m = nm;
