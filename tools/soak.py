@@ -1,5 +1,5 @@
 """Soak test of the pipelined refit engine: device memory in use (driver view)
-and step rate over a long run (C3, prefetch 2, two builder threads).
+and step rate over a long run (C3, prefetch 3, two builder threads).
 
     python tools/soak.py --steps 3000
 """
@@ -35,7 +35,7 @@ def main():
     sp = P.SelectionPass(ds, cams, gt)
     sp.run(D.to_device(cloud.points, torch.float64), (1.0, 0.2, 0.2))
     eng = RefitEngine(ds, sh0.clone(), cams, [sp.edited[i] for i in range(len(cams))], P.OptimizerConfig(),
-                      seed=7, cache_views=False, prefetch=2)
+                      seed=7, cache_views=False, prefetch=3)
     chunk = a.steps // 10
     for c in range(10):
         torch.cuda.synchronize()
