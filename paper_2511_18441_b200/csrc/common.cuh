@@ -314,6 +314,8 @@ struct rcgs_view {
     float4* color;        // (n,) rgb + active bits (as float 0..7) per step
     int32_t* rank_of;     // (n,) s or -1 (culled)
     uint32_t* fix;        // (n + 1,) {count, g...}: gaussians the Adam colour epilogue left to the fp64 fixup
+    unsigned long long* acc_fx;  // (3 n,) the backward's fixed-point sums, zeroed at build (off the optimizer's stream)
+    bool acc_dirty;              // acc_fx used since it was zeroed (the next backward clears it first)
     // per pair (sorted by tile, then depth)
     uint32_t* pair_g;     // (pairs,) scene index g
     uint32_t* pair_m;     // (pairs,) tile_block_mask of the pair (8x4 blocks its footprint reaches);

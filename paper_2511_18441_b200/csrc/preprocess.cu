@@ -771,6 +771,7 @@ static void view_free(rcgs_view* v, cudaStream_t s) {
     dfree(v->color, s);
     dfree(v->rank_of, s);
     dfree(v->fix, s);
+    dfree(v->acc_fx, s);
     dfree(v->pair_g, s);
     dfree(v->pair_m, s);
     dfree(v->ranges, s);
@@ -798,6 +799,9 @@ static int view_build(rcgs_view* v, cudaStream_t s) {
     const int ntiles = v->tiles_x * v->tiles_y;
     RCGS_TRY(dalloc(&v->rank_of, n, s));
     RCGS_TRY(dalloc(&v->fix, n + 1, s));
+    RCGS_TRY(dalloc(&v->acc_fx, 3 * n, s));
+    if (n > 0) RCGS_CUDA(cudaMemsetAsync(v->acc_fx, 0, 3 * n * sizeof(unsigned long long), s));
+    v->acc_dirty = false;
     RCGS_TRY(dalloc(&v->ranges, ntiles, s));
     // the view's persistent work counters (words 0-1) and the build's control words,
     // zeroed by one memset: key min (complemented) / max (u64 words 1, 2), the

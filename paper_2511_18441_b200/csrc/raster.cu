@@ -1537,9 +1537,11 @@ extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, floa
         RCGS_CUDA(cudaMemsetAsync(d_acc, 0, 3 * v->n * sizeof(float), s));
         return RCGS_OK;
     }
-    unsigned long long* acc_fx = nullptr;  // by scene index (entries carry g)
-    RCGS_TRY(dalloc(&acc_fx, 3 * v->n, s));
-    RCGS_CUDA(cudaMemsetAsync(acc_fx, 0, 3 * v->n * sizeof(unsigned long long), s));
+    // the view's fixed-point sums by scene index (entries carry g): zeroed when the
+    // view was built (on its builder stream), cleared here only for a second backward
+    unsigned long long* acc_fx = v->acc_fx;
+    if (v->acc_dirty) RCGS_CUDA(cudaMemsetAsync(acc_fx, 0, 3 * v->n * sizeof(unsigned long long), s));
+    const_cast<rcgs_view*>(v)->acc_dirty = true;
     if (v->pairs > 0 && records_valid(v)) {  // stream the recorded weights
         RecArgs ra = rec_args(v);
         ra.grad = d_grad_image;
@@ -1556,7 +1558,6 @@ extern "C" int rcgs_backward(const rcgs_view* v, const float* d_grad_image, floa
     bwd_finish_kernel<<<div_up(v->n, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(acc_fx), v->color,
                                                         v->rank_of, v->n, d_acc);
     RCGS_LAUNCH_CHECK();
-    dfree(acc_fx, s);
     return RCGS_OK;
 }
 
