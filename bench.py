@@ -321,6 +321,16 @@ def run_gpu(args):
             rooflines[name] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                                "frac": round(ach / hbm, 4), "ms_per_launch": round(kk["ms"], 4),
                                "note": kk.get("note", "")}
+    # north_star's per-kernel evidence: SM (L1 / pipe) throughput and issue activity of
+    # each stage's longest kernel, against the B200 peak, from the committed
+    # `ncu --set full` capture of one step (profiles/traffic.json)
+    for name, ncu_st in measured_stage_ncu().items():
+        if name in rooflines and "sm_throughput_pct" in ncu_st:
+            rooflines[name]["ncu"] = {"kernel": ncu_st.get("top_kernel"),
+                                      "sm_throughput_frac": round(ncu_st["sm_throughput_pct"] / 100, 4),
+                                      "issue_active_frac": round(ncu_st["issue_active_pct"] / 100, 4),
+                                      "dram_bytes_per_launch": ncu_st.get("dram_bytes_per_launch"),
+                                      "source": "profiles/traffic.json (ncu --set full of one step)"}
     # dominant kernel: the longest single-kernel main-stream stage (recording raster,
     # Adam).  Multi-kernel stages (loss: dirty scan + 3 passes; backward: record
     # stream + finish; view build on its side streams) are event intervals that
