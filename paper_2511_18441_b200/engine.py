@@ -88,6 +88,7 @@ class ViewPrefetcher:
         self.ring = [None] * (depth + 4)
         self.ring_free = [None] * (depth + 4)
         self.copy_stream = None  # one copy stream per worker (below): uploads of two steps run concurrently
+        self.gate_event = None   # optional main-stream event the next uploads wait for
         self.events = []  # (start, end) of each view build on its side stream
         self.host_build_ms = []
         self.host_wait_ms = []
@@ -191,6 +192,9 @@ class ViewPrefetcher:
                         with torch.cuda.stream(cs):
                             if free is not None:
                                 cs.wait_event(free)
+                            gate = self.gate_event
+                            if gate is not None:  # RCGS_UPLOAD_GATE: not under the loss
+                                cs.wait_event(gate)
                             if self.ring[slot] is None or self.ring[slot].shape != src.shape:
                                 self.ring[slot] = torch.empty(src.shape, dtype=torch.float32, device=self.device)
                             tgt = self.ring[slot]
@@ -235,6 +239,14 @@ class ViewPrefetcher:
             with torch.cuda.stream(self.streams[w]):
                 view.close()
         self.ready.clear()
+
+
+# Streamed targets: the next uploads wait for this step's backward ("bwd", default)
+# or loss ("loss") on the optimizer stream, so the 25 MB DMA runs under Adam and the
+# next raster instead of under the loss and the record stream (the loss's gradient
+# maps live in L2 between its passes).  e2e: none 1039, loss 1051, bwd 1058
+# view-steps/s ("none": no gate).
+_UPLOAD_GATE = os.environ.get("RCGS_UPLOAD_GATE", "bwd")
 
 
 class RefitEngine:
@@ -502,10 +514,18 @@ class RefitEngine:
         if ev:
             ev[2].record()
         D.loss_grad(img, target, self.config.lam, loss3=rec[:3], grad=grad)
+        if _UPLOAD_GATE == "loss" and self._pf is not None and self._pf.targets is not None:
+            gate = torch.cuda.Event()
+            gate.record()
+            self._pf.gate_event = gate
         # self.reject is 0 here: the previous step's Adam consumed and re-armed it
         if ev:
             ev[3].record()
         view.backward(grad, acc=self.acc, nonfinite=self.reject)
+        if _UPLOAD_GATE == "bwd" and self._pf is not None and self._pf.targets is not None:
+            gate = torch.cuda.Event()
+            gate.record()
+            self._pf.gate_event = gate
         accs = parallel.exchange_accs(self.acc, self.group, out=self.acc_all)
         parallel.any_rank(self.reject, self.group)
         if ev:
