@@ -57,7 +57,7 @@ class ClockSampler:
                "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
-    def __init__(self, index=0, period=0.05, enabled=True):
+    def __init__(self, index=0, period=0.01, enabled=True):
         self.enabled = enabled
         self.samples = []
         self.index = index
@@ -65,38 +65,56 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         self.max_mhz = None
+        self._nv = None
+        self.foreign = set()
 
-    def _run(self):
+    def _init(self):
+        # NVML is initialised before the timed region starts (its first import and
+        # nvmlInit can outlast a ~90 ms region, which had left runs unsampled)
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            masks = {k: getattr(nv, v) for k, v in self.REASONS.items()}
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._masks = {k: getattr(nv, v) for k, v in self.REASONS.items()}
+            self._nv = nv
         except Exception:
-            return
-        me = os.getpid()
-        self.foreign = set()
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, [k for k, m in masks.items() if r & m]))
+            self._nv = None
+
+    def _sample(self, procs=False):
+        nv, h = self._nv, self._h
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((sm, [k for k, m in self._masks.items() if r & m]))
+            if procs:
+                me = os.getpid()
                 for p in nv.nvmlDeviceGetComputeRunningProcesses(h):
                     if p.pid != me:
                         self.foreign.add(p.pid)
-            except Exception:
-                pass
+        except Exception:
+            pass
+
+    def _run(self):
+        i = 0
+        while not self._stop.is_set():
+            self._sample(procs=i % 10 == 0)
+            i += 1
             self._stop.wait(self.period)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run if self.enabled else (lambda: None), daemon=True)
+        if self.enabled:
+            self._init()
+        run = self._run if self._nv is not None else (lambda: None)
+        self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nv is not None:
+            self._sample(procs=True)  # the region's last instant (after its synchronize)
 
     def summary(self):
         if not self.samples:
@@ -765,13 +783,18 @@ def run_e2e(args, scene, cams, sp, group, world):
     marks = {}
     count = [0]
     done = threading.Event()
+    # at least 500 timed steps: the sink timestamps a step when the host sees its
+    # metrics, a few steps after it completed and with millisecond jitter (GC,
+    # snapshots, thread wake-ups), which over 100 steps (~90 ms) moved single
+    # runs by up to 10%
+    steps = max(args.steps, 500)
 
     def sink(m):
         count[0] += 1
         c = count[0]
         if c == args.warmup:
             marks["t0"] = time.perf_counter()
-        if c == args.warmup + args.steps:
+        if c == args.warmup + steps:
             marks["t1"] = time.perf_counter()
             done.set()
 
@@ -794,7 +817,7 @@ def run_e2e(args, scene, cams, sp, group, world):
         torch.cuda.synchronize()
         torch.distributed.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             opt._step()
             opt._flush(wait=False)
         opt._flush()
@@ -802,7 +825,7 @@ def run_e2e(args, scene, cams, sp, group, world):
         dt = sync_max(time.perf_counter() - t0, world)
         opt.stop()
     h, w = edited.shape[1], edited.shape[2]
-    return {"value": round(world * args.steps / dt, 3), "unit": UNIT,
+    return {"value": round(world * steps / dt, 3), "unit": UNIT, "steps": steps,
             "h2d_bytes_per_step": int(h * w * 3 * 4), "d2h_bytes_per_step": 32,
             "api": ("BackgroundOptimizer(stream_targets=True).start(): target H2D every step on the prefetch "
                     "stream, metrics D2H every step into the metrics sink (timed between the sink's calls)"
